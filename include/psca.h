@@ -1,0 +1,136 @@
+/*
+ * psca.h -- C ABI of the B200-native PSCA activity-detection hot path.
+ *
+ * The reference (arXiv 2503.15259, /root/reference/pkg/src/actdet) is a pure
+ * Python package; its "operator API" for this path is the set of Python
+ * solver functions listed below.  Each entry point here replaces one of them
+ * (reference file:line in the comment) and is what a ctypes / cffi binding in
+ * the reference package would call.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer (cudaMalloc'd or a torch CUDA tensor's
+ *     data_ptr) unless the comment says otherwise; complex128 arrays are
+ *     interleaved (re, im) doubles, C order, exactly numpy's complex128 layout;
+ *   - batched arrays carry a leading instance dimension B;
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *     every call is stream-ordered and re-entrant per stream, allocates
+ *     nothing, and uses only the caller's workspace;
+ *   - return value: PSCA_OK or a negative PSCA_E* code (argument / launch
+ *     errors).  Numerical failures never fail the call: they are reported per
+ *     instance in `status` (mirroring psca_run's trace.meta["abort"]).
+ */
+#ifndef PSCA_H
+#define PSCA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSCA_OK 0
+#define PSCA_E_ARG (-1)       /* bad shape / kind / pointer                  */
+#define PSCA_E_CUDA (-2)      /* kernel launch or CUDA runtime failure       */
+#define PSCA_E_WORKSPACE (-3) /* workspace smaller than *_workspace_bytes()  */
+#define PSCA_E_UNSUPPORTED (-4)
+
+/* problem kinds: estimators.py:27 KINDS */
+#define PSCA_ML_K 0
+#define PSCA_MAP_K 1
+#define PSCA_ML_UD 2
+#define PSCA_MAP_UR 3
+
+/* per-instance status (estimators.py:263-271, 285-286) */
+#define PSCA_RUNNING 0     /* ran to max_iter                                 */
+#define PSCA_CHOL_FAIL 1   /* Sigma not numerically PD (ConditioningError)    */
+#define PSCA_QFLOOR 2      /* min q < 0.5 L / ||Sigma||_F                      */
+#define PSCA_CONVERGED 3   /* update_norm < tol                               */
+
+/* Smoothed effective-pathloss prior, plain scalars (priors.py:173-281).
+ * phi(d) = p_lin * (k d)^-eta; area2 = d_outer^2 - d_inner^2;
+ * cv, cw = density value / slope targets of the Hermite bridge at g_low. */
+typedef struct {
+    double eps, g_low, g_high, dead_zone_grad;
+    double p_lin, k, eta, area2, cv, cw;
+} psca_eff_prior;
+
+/* Arguments of psca_solve (estimators.py:239-289 psca_run, batched;
+ * unroll.py:69-73 forward is the same call with explicit steps and tol=0). */
+typedef struct {
+    int kind;               /* PSCA_ML_K .. PSCA_MAP_UR                         */
+    int B, N, L;            /* instances, devices, pilot length                 */
+    int n_antennas;         /* M (MAP prior scale 1/M)                          */
+    int max_iter;           /* T                                               */
+    double tol;             /* early stop on update_norm < tol (0 = never)     */
+    int record_objective;   /* estimators.py:279-280                           */
+    int n_chunks;           /* column chunks per instance; 0 = automatic       */
+    const double* pilots;   /* [B][L][N] complex128                            */
+    const double* gains;    /* [B][N]   (known-pathloss kinds; else may be 0)  */
+    const double* emp_cov;  /* [B][L][L] complex128                            */
+    const double* noise;    /* [B] sigma^2 > 0                                 */
+    const double* steps;    /* [max_iter] rho_k in (0,1]                       */
+    const double* prior_lin;/* map-k: [N] = -log(p/(1-p))/M  (priors.py:154-158) */
+    const double* prior_p;  /* map-ur: [N] activation probabilities p_n      */
+    psca_eff_prior eff;     /* map-ur prior scalars                            */
+    double* x_out;          /* [B][N]  final estimate (trace.final)            */
+    double* update_norm;    /* [B][max_iter]                                    */
+    double* objective;      /* [B][max_iter] or 0                              */
+    double* iterates;       /* [B][max_iter+1][N] or 0                         */
+    int* status;            /* [B]                                             */
+    int* n_iter;            /* [B] completed iterations                        */
+    double* cond_est;       /* [B] condition estimate at a Cholesky abort       */
+} psca_solve_args;
+
+/* Workspace (device bytes) psca_solve needs for these arguments. */
+size_t psca_solve_workspace_bytes(const psca_solve_args* a);
+
+/* The PSCA iteration for a batch of independent instances
+ * (replaces estimators.psca_run, estimators.py:239-289, and
+ *  unroll.forward, unroll.py:69-73). */
+int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Sigma_hat = Y Y^H / n_antennas  (sysmodel.py:244-248 empirical_cov).
+ * y: [B][L][Mc] complex128 -> out: [B][L][L] complex128. */
+int psca_empirical_cov(const double* y, int B, int L, int Mc, int n_antennas, double* out,
+                       void* stream);
+
+/* Sigma = S diag(w) S^H + sigma^2 I  (covlinalg.py:43-57 cov_unknown; cov_known
+ * :60-67 passes w = alpha*g).  pilots [B][L][N], w [B][N], noise [B] -> out [B][L][L]. */
+size_t psca_cov_workspace_bytes(int B, int N, int L);
+int psca_cov_unknown(const double* pilots, const double* w, const double* noise, int B, int N,
+                     int L, double* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Hermitian PD inverse  (covlinalg.py:91-115 frobenius_inverse).
+ * sigma [B][L][L] -> out [B][L][L] exactly Hermitian; status[b] = PSCA_CHOL_FAIL
+ * with cond_est[b] when a pivot is not positive; logdet[b] = log|Sigma| (may be 0). */
+size_t psca_inverse_workspace_bytes(int B, int L);
+int psca_hpd_inverse(const double* sigma, int B, int L, double* out, int* status,
+                     double* cond_est, double* logdet, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* q_n = s^H P s, r_n = s^H P Sigma_hat P s  (covlinalg.py:134-156 quad_forms).
+ * pilots [B][L][N], sigma_inv [B][L][L], emp_cov [B][L][L] -> q, r [B][N]. */
+size_t psca_quad_workspace_bytes(int B, int N, int L);
+int psca_quad_forms(const double* pilots, const double* sigma_inv, const double* emp_cov, int B,
+                    int N, int L, double* q, double* r, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* log|Sigma| + Re tr(Sigma^-1 Sigma_hat)  (covlinalg.py:159-172 eval_objective).
+ * out [B]; status[b] = PSCA_CHOL_FAIL when Sigma is not PD. */
+size_t psca_objective_workspace_bytes(int B, int L);
+int psca_eval_objective(const double* sigma, const double* sigma_inv, const double* emp_cov,
+                        int B, int L, double* out, int* status, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Number of kernel launches the last psca_solve on this thread issued
+ * (reported as bench.py's gpu_launches). */
+int psca_last_launch_count(void);
+
+/* Library version string (host pointer). */
+const char* psca_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSCA_H */

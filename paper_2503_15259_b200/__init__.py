@@ -1,0 +1,24 @@
+"""B200-native PSCA activity-detection hot path (arXiv 2503.15259).
+
+Drop-in for the solver API of the reference package ``actdet``
+(/root/reference/pkg/src/actdet/__init__.py:12-24): the same names, argument
+meanings and error behaviour, with the PSCA iteration running as hand-written
+sm_100a CUDA kernels behind the C ABI in include/psca.h.  Batched entry
+points (``psca_run_batch``, ``unroll.forward_batch``) are the throughput path.
+"""
+
+from .sysmodel import ActivityModel, DomainError, Sample, SystemConfig, empirical_cov
+from .estimators import (DetectorTrace, Problem, StepSchedule, psca_run, psca_run_batch,
+                         default_schedule, default_steps, bounds_for)
+from .priors import EffPathlossPrior, IndependentPrior
+from .covlinalg import (ConditioningError, CovState, cov_known, cov_unknown, eval_objective,
+                        frobenius_inverse, quad_forms)
+
+__all__ = [
+    "ActivityModel", "DomainError", "Sample", "SystemConfig", "empirical_cov",
+    "DetectorTrace", "Problem", "StepSchedule", "psca_run", "psca_run_batch",
+    "default_schedule", "default_steps", "bounds_for",
+    "EffPathlossPrior", "IndependentPrior",
+    "ConditioningError", "CovState", "cov_known", "cov_unknown", "eval_objective",
+    "frobenius_inverse", "quad_forms",
+]

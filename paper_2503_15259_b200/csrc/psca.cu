@@ -1,0 +1,1265 @@
+// B200 (sm_100a) kernels for the PSCA activity-detection hot path + the C ABI
+// declared in include/psca.h.
+//
+// Reference algorithm: /root/reference/pkg/src/actdet (pure Python).  One PSCA
+// iteration (estimators.py:259-286) is split into two kernels:
+//
+//   column_kernel  (grid: column chunks x instances)
+//     S tiles -> SMEM (cp.async, swizzled); per 8-column block the two
+//     Hermitian quadratic forms q_n = s^H P s and r_n = s^H A s
+//     (A = P Sigma_hat P, covlinalg.py:134-156) as a lower-triangular real
+//     GEMM on FP64 DMMA (mma.sync m8n8k4); the per-device update
+//     (gradient, surrogate coefficient, clamp, relaxed step:
+//     estimators.py:176-200, 272-276, priors.py:154-159, 377-399) fused as
+//     the epilogue; then the covariance rebuild for the NEXT iterate,
+//     Sigma += S diag(w_new) S^H (covlinalg.py:55), again on DMMA over the
+//     lower block triangle, from the same SMEM tile.  S is read once per
+//     iteration.
+//
+//   factor_kernel  (grid: instances)
+//     finalises the previous iteration (q-floor guard estimators.py:267-271,
+//     update norm, tol stop, objective), assembles Sigma from the chunk
+//     partials + sigma^2 I, inverts it in SMEM with a Gauss-Jordan sweep
+//     (Hermitian PD, no pivoting: same pivots as Cholesky, log|Sigma| =
+//     sum log pivots, covlinalg.py:91-115 / 159-172), symmetrises, forms
+//     A = P Sigma_hat P, and packs P and A (doubled off-diagonal, lower
+//     triangle) directly in DMMA A-fragment order for the next column_kernel.
+//
+// All arithmetic is IEEE float64.  Reductions use fixed orders (no float
+// atomics), so reruns are bit-identical.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "psca.h"
+
+#define PSCA_VERSION_STR "psca-b200 0.1.0 (sm_100a)"
+
+namespace {
+
+constexpr int NT = 256;            // threads per CTA
+constexpr int NWARP = NT / 32;
+constexpr int NCT = 32;            // device columns per SMEM tile
+constexpr int NCB = NCT / 8;       // 8-column blocks per tile
+constexpr int FAC_SMEM_MAX_LP = 80;
+constexpr int MAX_L_TILE = 128;    // tile path limit (SMEM: 1.5 KB per padded row)
+
+thread_local int g_launches = 0;
+
+// ---------------------------------------------------------------------------
+// geometry
+// ---------------------------------------------------------------------------
+struct Geo {
+    int L, LP, NRB, LP8, NB, NBLK;
+};
+
+__host__ __device__ inline int rebuild_block_count(int nrb) {
+    int s = 0;
+    for (int i = 0; i < nrb; ++i) s += (4 * i + 3) / 8 + 1;
+    return s;
+}
+
+__host__ __device__ inline Geo make_geo(int L) {
+    Geo g;
+    g.L = L;
+    g.LP = (L + 3) & ~3;     // complex rows, multiple of 4 (one 8-real-row block = 4 rows)
+    g.NRB = g.LP / 4;        // real row blocks
+    g.LP8 = (L + 7) & ~7;    // SMEM tile rows (rebuild B fragments read 8-row blocks)
+    g.NB = g.NRB * (g.NRB + 1);           // quad-form fragment blocks (lower triangle)
+    g.NBLK = rebuild_block_count(g.NRB);  // rebuild C blocks (lower triangle)
+    return g;
+}
+
+// swizzle of the 16-byte complex slot inside a 32-column SMEM row; makes the
+// DMMA B-fragment loads of both the quad-form and the rebuild stage
+// bank-conflict free.
+__host__ __device__ inline int swz(int m) { return ((m & 1) << 2) | (m & 2); }
+
+__device__ __forceinline__ int tile_idx(int m, int n) { return m * NCT + (n ^ swz(m)); }
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c[0]), "+d"(c[1])
+        : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cfma_conj_a(double2 a, double2 b, double2 acc) {
+    // acc + conj(a) * b
+    acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+    acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+    return acc;
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+    acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+    acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+    return acc;
+}
+__device__ __forceinline__ double comp(double2 v, int c) { return c ? v.y : v.x; }
+
+// clamp with numpy semantics (NaN propagates): np.clip(v, lo, hi)
+__device__ __forceinline__ double np_clip(double v, double lo, double hi) {
+    return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// deterministic CTA reductions (fixed shuffle + fixed warp order)
+__device__ double block_sum(double v, double* sred) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sred[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NWARP; ++i) t += sred[i];
+        sred[NWARP] = t;
+    }
+    __syncthreads();
+    return sred[NWARP];
+}
+
+// ---------------------------------------------------------------------------
+// effective-pathloss prior (priors.py:246-281, 313-399); mirrors the numpy
+// operation order so rounding matches the reference closely
+// ---------------------------------------------------------------------------
+__device__ void eff_density(double gm, double p, const psca_eff_prior& e, double& dens,
+                            double& der) {
+    const double eps = e.eps, gl = e.g_low;
+    dens = 0.0;
+    der = 0.0;
+    if (gm < eps) {  // cubic bump on [0, eps)
+        double gb = gm;
+        double t1 = (1.0 - p) * (1.0 + 2.0 * gb / eps);
+        double t2 = (gb - eps) / eps;
+        dens = t1 * (t2 * t2);
+        der = 6.0 * (1.0 - p) * gb * (gb - eps) / pow(eps, 3.0);
+    } else if (gm >= gl - eps && gm < gl) {  // Hermite bridge
+        double t = gm - gl;
+        double u = (t + eps) / eps;
+        double u2 = u * u;
+        dens = p * (e.cv * (1.0 - 2.0 * t / eps) * u2 + e.cw * t * u2);
+        der = p * (-6.0 * e.cv * t * (t + eps) / pow(eps, 3.0) +
+                   e.cw * (t + eps) * (3.0 * t + eps) / (eps * eps));
+    } else if (gm >= gl) {  // exact tail p * p_G
+        double base = gm / e.p_lin;
+        double inv = (1.0 / e.k) * pow(base, -1.0 / e.eta);
+        double dinv = -(1.0 / (e.k * e.eta * e.p_lin)) * pow(base, -1.0 / e.eta - 1.0);
+        double d2inv = ((1.0 + e.eta) / (e.k * (e.eta * e.eta) * (e.p_lin * e.p_lin))) *
+                       pow(base, -1.0 / e.eta - 2.0);
+        double pg = -2.0 * inv * dinv / e.area2;
+        double dpg = -2.0 * (dinv * dinv + inv * d2inv) / e.area2;
+        dens = p * pg;
+        der = p * dpg;
+    }
+}
+
+__device__ double eff_grad(double gm, double p, const psca_eff_prior& e, int n_antennas) {
+    double dens, der;
+    eff_density(gm, p, e, dens, der);
+    const double mag = e.dead_zone_grad;
+    if (dens <= 1e-300) {
+        double s = (gm <= e.g_low / 2.0) ? 1.0 : -1.0;
+        return s * (mag / n_antennas);
+    }
+    double v = np_clip(der / dens, -mag, mag);
+    return -v / n_antennas;
+}
+
+// ---------------------------------------------------------------------------
+// column kernel
+// ---------------------------------------------------------------------------
+enum ColMode { COL_SOLVE = 0, COL_QUAD = 1, COL_REBUILD = 2 };
+
+struct ColArgs {
+    int kind, B, N, L, n_chunks, chunk_cols, k, T, n_antennas, record_objective;
+    const double2* pilots;      // [B][L][N]
+    const double* gains;        // [B][N]
+    const double* x_cur;        // [B][N]
+    double* x_next;             // [B][N]
+    double* iterates;           // [B][T+1][N] or null
+    const double2* frags;       // [B][NB][32] double2 (P', A')
+    double2* sig_part;          // [B][chunks][NBLK][32] double2
+    double* red_part;           // [B][chunks][4]
+    const int* status;          // [B]
+    const double* steps;        // [T]
+    const double* prior_lin;    // [N]
+    const double* prior_p;      // [N]
+    psca_eff_prior eff;
+    double* q_out;              // COL_QUAD: [B][N]
+    double* r_out;
+    const double* w_in;         // COL_REBUILD: [B][N]
+};
+
+__device__ __forceinline__ void load_tile(double2* buf, const double2* __restrict__ sb, int N,
+                                          int L, int LP8, int col0) {
+    const int total = LP8 * NCT;
+    for (int e = threadIdx.x; e < total; e += NT) {
+        int m = e / NCT, n = e % NCT;
+        bool ok = (m < L) && (col0 + n < N);
+        const double2* src = ok ? (sb + (size_t)m * N + col0 + n) : sb;
+        cp_async16(buf + tile_idx(m, n), src, ok ? 16 : 0);
+    }
+    cp_async_commit();
+}
+
+template <int MAXBW, int MODE>
+__global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Geo geo = make_geo(a.L);
+    const int b = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const size_t bN = (size_t)b * a.N;
+    const int n_begin = chunk * a.chunk_cols;
+    const int n_end = min(a.N, n_begin + a.chunk_cols);
+
+    if (MODE == COL_SOLVE && a.status[b] != PSCA_RUNNING) {
+        // frozen instance (aborted / converged): keep the ping-pong invariant
+        for (int n = n_begin + tid; n < n_end; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
+        return;
+    }
+
+    double2* S0 = reinterpret_cast<double2*>(smem_raw);
+    double2* S1 = S0 + geo.LP8 * NCT;
+    double2* WS = S1 + geo.LP8 * NCT;
+    double* qr_s = reinterpret_cast<double*>(WS + geo.LP8 * NCT);  // [2 halves][NCT][2]
+    double* wv_s = qr_s + 2 * NCT * 2;                              // [NCT]
+
+    const double2* sb = a.pilots + (size_t)b * a.L * a.N;
+    const double2* fr = a.frags + (size_t)b * geo.NB * 32;
+
+    // ---- static work split -------------------------------------------------
+    // quad forms: warp -> (column block, row-block half); halves balanced by a
+    // greedy LPT pass over row-block costs 2(i+1)
+    const int cb = warp & (NCB - 1);
+    const int half = warp / NCB;
+    unsigned long long rowmask = 0ull;
+    {
+        int load0 = 0, load1 = 0;
+        for (int i = geo.NRB - 1; i >= 0; --i) {
+            int cost = 2 * (i + 1);
+            int h = (load1 < load0) ? 1 : 0;
+            if (h) load1 += cost; else load0 += cost;
+            if (h == half) rowmask |= (1ull << i);
+        }
+    }
+    // rebuild: C blocks w, w+8, ... (lower block triangle, row-major order)
+    int bi_i[MAXBW], bi_j[MAXBW];
+    int nbw = 0;
+    {
+        int idx = 0;
+#pragma unroll 1
+        for (int i = 0; i < geo.NRB; ++i) {
+            int jmax = (4 * i + 3) / 8;
+            for (int j = 0; j <= jmax; ++j, ++idx) {
+                if ((idx % NWARP) == warp) {
+#pragma unroll
+                    for (int t = 0; t < MAXBW; ++t)
+                        if (t == nbw) { bi_i[t] = i; bi_j[t] = j; }
+                    ++nbw;
+                }
+            }
+        }
+    }
+    double acc[MAXBW][2];
+#pragma unroll
+    for (int t = 0; t < MAXBW; ++t) acc[t][0] = acc[t][1] = 0.0;
+
+    // update-stage partials (warp 0)
+    double p_dx2 = 0.0, p_minq = INFINITY, p_prior = 0.0;
+    const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
+    const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
+    const double rho = (MODE == COL_SOLVE) ? a.steps[a.k] : 0.0;
+
+    const int ntiles = (n_end - n_begin + NCT - 1) / NCT;
+    if (ntiles > 0) load_tile(S0, sb, a.N, a.L, geo.LP8, n_begin);
+
+    for (int t = 0; t < ntiles; ++t) {
+        double2* S = (t & 1) ? S1 : S0;
+        const int col0 = n_begin + t * NCT;
+        if (t + 1 < ntiles) {
+            load_tile((t & 1) ? S0 : S1, sb, a.N, a.L, geo.LP8, col0 + NCT);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* Sd = reinterpret_cast<const double*>(S);
+
+        if (MODE != COL_REBUILD) {
+            // ---- quadratic forms on DMMA -----------------------------------
+            double qa0 = 0.0, qa1 = 0.0, ra0 = 0.0, ra1 = 0.0;
+            const int nb_col = cb * 8 + r8;  // B-fragment column (device) of this lane
+#pragma unroll 1
+            for (int i = 0; i < geo.NRB; ++i) {
+                if (!((rowmask >> i) & 1ull)) continue;
+                double tp[2] = {0.0, 0.0}, ta[2] = {0.0, 0.0};
+                const double2* f = fr + (size_t)(i * (i + 1)) * 32 + lane;
+                const int nk = 2 * (i + 1);
+#pragma unroll 4
+                for (int kk = 0; kk < nk; ++kk) {
+                    double2 pa = __ldg(f + kk * 32);
+                    int m = 2 * kk + (c4 >> 1);
+                    double bv = Sd[2 * tile_idx(m, nb_col) + (c4 & 1)];
+                    dmma(tp, pa.x, bv);
+                    dmma(ta, pa.y, bv);
+                }
+                // epilogue: q_n += sum_{rows} S_real * T_real  (C-fragment positions)
+                int l = 4 * i + (r8 >> 1), p = r8 & 1;
+                int n0 = cb * 8 + 2 * c4;
+                double s0 = Sd[2 * tile_idx(l, n0) + p];
+                double s1 = Sd[2 * tile_idx(l, n0 + 1) + p];
+                qa0 = fma(s0, tp[0], qa0);
+                qa1 = fma(s1, tp[1], qa1);
+                ra0 = fma(s0, ta[0], ra0);
+                ra1 = fma(s1, ta[1], ra1);
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                qa0 += __shfl_xor_sync(0xffffffffu, qa0, o);
+                qa1 += __shfl_xor_sync(0xffffffffu, qa1, o);
+                ra0 += __shfl_xor_sync(0xffffffffu, ra0, o);
+                ra1 += __shfl_xor_sync(0xffffffffu, ra1, o);
+            }
+            if (r8 == 0) {
+                int n0 = cb * 8 + 2 * c4;
+                double* d = qr_s + half * NCT * 2;
+                d[2 * n0] = qa0;
+                d[2 * n0 + 1] = ra0;
+                d[2 * (n0 + 1)] = qa1;
+                d[2 * (n0 + 1) + 1] = ra1;
+            }
+            __syncthreads();
+        }
+
+        if (MODE == COL_QUAD) {
+            if (tid < NCT) {
+                int n = col0 + tid;
+                if (n < n_end) {
+                    a.q_out[bN + n] = qr_s[2 * tid] + qr_s[NCT * 2 + 2 * tid];
+                    a.r_out[bN + n] = qr_s[2 * tid + 1] + qr_s[NCT * 2 + 2 * tid + 1];
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+
+        // ---- per-device update (estimators.py:272-276) ----------------------
+        if (tid < NCT) {
+            const int n = col0 + tid;
+            double w_new = 0.0;
+            if (n < n_end) {
+                if (MODE == COL_REBUILD) {
+                    w_new = a.w_in[bN + n];
+                } else {
+                    const double q = qr_s[2 * tid] + qr_s[NCT * 2 + 2 * tid];
+                    const double r = qr_s[2 * tid + 1] + qr_s[NCT * 2 + 2 * tid + 1];
+                    const double x = a.x_cur[bN + n];
+                    const double g = known ? a.gains[bN + n] : 1.0;
+                    const double diff = __dsub_rn(q, r);
+                    double grad;
+                    if (a.kind == PSCA_ML_K) {
+                        grad = __dmul_rn(g, diff);
+                    } else if (a.kind == PSCA_MAP_K) {
+                        grad = __dadd_rn(__dmul_rn(g, diff), a.prior_lin[n]);
+                    } else if (a.kind == PSCA_ML_UD) {
+                        grad = diff;
+                    } else {
+                        grad = __dadd_rn(diff, eff_grad(x, a.prior_p[n], a.eff, a.n_antennas));
+                    }
+                    const double gq = known ? __dmul_rn(g, q) : q;
+                    const double coef = __dmul_rn(gq, gq);
+                    const double cand = np_clip(__dsub_rn(x, __ddiv_rn(grad, coef)), 0.0, hi);
+                    const double xn = __dadd_rn(__dmul_rn(__dsub_rn(1.0, rho), x), __dmul_rn(rho, cand));
+                    a.x_next[bN + n] = xn;
+                    if (a.iterates)
+                        a.iterates[((size_t)b * (a.T + 1) + a.k + 1) * a.N + n] = xn;
+                    w_new = known ? __dmul_rn(xn, g) : xn;
+                    const double dx = __dsub_rn(xn, x);
+                    p_dx2 = fma(dx, dx, p_dx2);
+                    p_minq = (q < p_minq) ? q : p_minq;
+                    if (a.record_objective) {
+                        if (a.kind == PSCA_MAP_K) {
+                            p_prior = fma(a.prior_lin[n], x, p_prior);
+                        } else if (a.kind == PSCA_MAP_UR) {
+                            double dens, der;
+                            eff_density(x, a.prior_p[n], a.eff, dens, der);
+                            p_prior += log(dens > 1e-300 ? dens : 1e-300);
+                        }
+                    }
+                }
+            }
+            wv_s[tid] = w_new;
+        }
+        __syncthreads();
+
+        // ---- WS = S diag(w) (A operand of the rebuild) ----------------------
+        for (int e = tid; e < geo.LP8 * NCT; e += NT) {
+            int m = e / NCT, ph = e % NCT;
+            int n = ph ^ swz(m);
+            double w = wv_s[n];
+            double2 v = S[m * NCT + ph];
+            WS[m * NCT + ph] = make_double2(w * v.x, w * v.y);
+        }
+        __syncthreads();
+
+        // ---- rebuild Sigma_next += S diag(w) S^H on DMMA (lower blocks) -----
+        {
+            const double* Wd = reinterpret_cast<const double*>(WS);
+            const int p = r8 & 1, q = c4 & 1;
+            const int ac = p ^ q;
+            const unsigned long long sgn = (p & q) ? 0x8000000000000000ull : 0ull;
+#pragma unroll 1
+            for (int kk2 = 0; kk2 < NCT / 2; ++kk2) {
+                if (wv_s[2 * kk2] == 0.0 && wv_s[2 * kk2 + 1] == 0.0) continue;  // exact skip
+                const int n = 2 * kk2 + (c4 >> 1);
+#pragma unroll
+                for (int t = 0; t < MAXBW; ++t) {
+                    if (t < nbw) {
+                        int l = 4 * bi_i[t] + (r8 >> 1);
+                        double av = Wd[2 * tile_idx(l, n) + ac];
+                        av = __longlong_as_double(__double_as_longlong(av) ^ sgn);
+                        int m = 8 * bi_j[t] + r8;
+                        double bv = Sd[2 * tile_idx(m, n) + q];
+                        dmma(acc[t], av, bv);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    if (MODE == COL_QUAD) return;
+
+    // ---- chunk outputs ------------------------------------------------------
+    {
+        double2* sp = a.sig_part + ((size_t)b * a.n_chunks + chunk) * geo.NBLK * 32;
+        int idx = 0, t = 0;
+        for (int i = 0; i < geo.NRB; ++i) {
+            int jmax = (4 * i + 3) / 8;
+            for (int j = 0; j <= jmax; ++j, ++idx) {
+                if ((idx % NWARP) == warp) {
+#pragma unroll
+                    for (int u = 0; u < MAXBW; ++u)
+                        if (u == t) sp[(size_t)idx * 32 + lane] = make_double2(acc[u][0], acc[u][1]);
+                    ++t;
+                }
+            }
+        }
+    }
+    if (MODE == COL_SOLVE && warp == 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            p_dx2 += __shfl_xor_sync(0xffffffffu, p_dx2, o);
+            double mq = __shfl_xor_sync(0xffffffffu, p_minq, o);
+            p_minq = (mq < p_minq) ? mq : p_minq;
+            p_prior += __shfl_xor_sync(0xffffffffu, p_prior, o);
+        }
+        if (lane == 0) {
+            double* rp = a.red_part + ((size_t)b * a.n_chunks + chunk) * 4;
+            rp[0] = p_dx2;
+            rp[1] = p_minq;
+            rp[2] = p_prior;
+            rp[3] = 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// factor kernel
+// ---------------------------------------------------------------------------
+enum FacMode { FAC_SOLVE = 0, FAC_INVERSE = 1, FAC_PREP = 2, FAC_ASSEMBLE = 3, FAC_OBJECTIVE = 4 };
+
+struct FacArgs {
+    int B, N, L, T, n_chunks, k_new, kind, n_antennas, record_objective;
+    double tol;
+    const double* noise;        // [B]
+    const double2* emp_cov;     // [B][L][L]
+    const double2* sig_part;    // [B][chunks][NBLK][32]
+    const double* red_part;     // [B][chunks][4]
+    double2* frags;             // [B][NB][32]
+    double* inst;               // [B][4]: frob, logdet, trace
+    int* status;
+    int* n_iter;
+    double* cond_est;
+    double* update_norm;        // [B][T]
+    double* objective;          // [B][T] or null
+    const double* x_cur;
+    double* x_next;
+    double2* scratch;           // global X/G when LP > FAC_SMEM_MAX_LP: [B][2][LP][LP+1]
+    const double2* in_mat;      // FAC_INVERSE / FAC_PREP / FAC_OBJECTIVE input [B][L][L]
+    const double2* in_mat2;     // FAC_OBJECTIVE: sigma_inv
+    double2* out_mat;           // FAC_INVERSE / FAC_ASSEMBLE output [B][L][L]
+    double* out_vec;            // FAC_INVERSE: logdet, FAC_OBJECTIVE: value
+};
+
+// Gauss-Jordan sweep inversion of a Hermitian PD matrix held in X (row
+// stride ld).  One __syncthreads per pivot: row k / column k of the step's
+// input are staged in ping-pong buffers by their owners during the previous
+// step.  Pivots equal the LDL^H / Cholesky pivots, so log|Sigma| = sum log
+// pivots.  Returns false (uniformly) if a pivot is not > 0.
+__device__ bool gj_inverse(double2* X, int ld, int L, double2* rowb, double2* colb,
+                           double& logdet, double& pmin, double& pmax) {
+    const int tid = threadIdx.x;
+    for (int e = tid; e < L; e += NT) {
+        rowb[e] = X[e];
+        colb[e] = X[e * ld];
+    }
+    __syncthreads();
+    logdet = 0.0;
+    pmin = INFINITY;
+    pmax = 0.0;
+    for (int k = 0; k < L; ++k) {
+        const double2* rk = rowb + (k & 1) * L;
+        const double2* ck = colb + (k & 1) * L;
+        double2* rn = rowb + ((k + 1) & 1) * L;
+        double2* cn = colb + ((k + 1) & 1) * L;
+        const double piv = rk[k].x;
+        if (!(piv > 0.0)) {
+            pmin = piv;
+            return false;
+        }
+        logdet += log(piv);
+        pmin = fmin(pmin, piv);
+        pmax = fmax(pmax, piv);
+        const double pinv = 1.0 / piv;
+        for (int e = tid; e < L * L; e += NT) {
+            int i = e / L, j = e - i * L;
+            double2 v = X[i * ld + j], nv;
+            if (i == k) {
+                nv = (j == k) ? make_double2(pinv, 0.0) : make_double2(v.x * pinv, v.y * pinv);
+            } else if (j == k) {
+                nv = make_double2(-v.x * pinv, -v.y * pinv);
+            } else {
+                double2 pr = cmul(ck[i], rk[j]);
+                nv = make_double2(v.x - pr.x * pinv, v.y - pr.y * pinv);
+            }
+            X[i * ld + j] = nv;
+            if (i == k + 1) rn[j] = nv;
+            if (j == k + 1) cn[i] = nv;
+        }
+        __syncthreads();
+    }
+    return true;
+}
+
+// P <- (P + P^H)/2 in place (covlinalg.py:107, 112-114)
+__device__ void symmetrize(double2* X, int ld, int L) {
+    for (int e = threadIdx.x; e < L * L; e += NT) {
+        int i = e / L, j = e - i * L;
+        if (i > j) {
+            double2 u = X[i * ld + j], v = X[j * ld + i];
+            double2 s = make_double2(0.5 * (u.x + v.x), 0.5 * (u.y - v.y));
+            X[i * ld + j] = s;
+            X[j * ld + i] = make_double2(s.x, -s.y);
+        } else if (i == j) {
+            X[i * ld + i].y = 0.0;
+        }
+    }
+    __syncthreads();
+}
+
+// G = E X  (E = Sigma_hat from global, X = P)
+__device__ void gemm_EX(const double2* __restrict__ E, const double2* X, int ld, double2* G,
+                        int L) {
+    for (int e = threadIdx.x; e < L * L; e += NT) {
+        int a = e / L, m = e - a * L;
+        double2 s = make_double2(0.0, 0.0);
+        const double2* er = E + (size_t)a * L;
+        for (int c = 0; c < L; ++c) s = cfma(__ldg(er + c), X[c * ld + m], s);
+        G[a * ld + m] = s;
+    }
+    __syncthreads();
+}
+
+// Pack P' (from X) and A' = (P^H G) into DMMA A-fragment order: block (i,kk)
+// holds rows l = 4i..4i+3, cols m = 2kk..2kk+1; lane (r,c): row (l = 4i + r/2,
+// part p = r&1), k (m = 2kk + c/2, part q = c&1); value = the real 2x2
+// expansion [[re, -im], [im, re]] of the complex entry, off-diagonal doubled,
+// strictly upper / padded entries zero.
+__device__ void pack_frags(const double2* X, const double2* G, int ld, int L, const Geo& geo,
+                           double2* __restrict__ out) {
+    double* od = reinterpret_cast<double*>(out);
+    const int total = geo.NB * 8;
+    for (int e = threadIdx.x; e < total; e += NT) {
+        int blk = e >> 3, a4 = (e >> 1) & 3, cc = e & 1;
+        int i = 0;
+        while ((i + 1) * (i + 2) <= blk) ++i;
+        int kk = blk - i * (i + 1);
+        int l = 4 * i + a4, m = 2 * kk + cc;
+        double2 pv = make_double2(0.0, 0.0), av = make_double2(0.0, 0.0);
+        if (l < L && m <= l) {
+            pv = X[l * ld + m];
+            double2 s = make_double2(0.0, 0.0);
+            for (int t = 0; t < L; ++t) s = cfma_conj_a(X[t * ld + l], G[t * ld + m], s);
+            av = s;
+            if (m < l) {
+                pv.x *= 2.0; pv.y *= 2.0; av.x *= 2.0; av.y *= 2.0;
+            } else {
+                pv.y = 0.0; av.y = 0.0;
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                int lane = 4 * (2 * a4 + p) + (2 * cc + q);
+                double sg = (p == 0 && q == 1) ? -1.0 : 1.0;
+                double vp = sg * comp(pv, p ^ q), va = sg * comp(av, p ^ q);
+                size_t o = ((size_t)blk * 32 + lane) * 2;
+                od[o] = vp;
+                od[o + 1] = va;
+            }
+    }
+}
+
+// Sigma (lower + mirrored) from the chunk partial C fragments + sigma^2 I
+__device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2* X, int ld,
+                               bool zero_weights) {
+    const int L = a.L;
+    for (int e = threadIdx.x; e < L * L; e += NT) {
+        int i = e / L, j = e - i * L;
+        X[i * ld + j] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    double* Xd = reinterpret_cast<double*>(X);
+    if (!zero_weights) {
+        const int total = geo.NBLK * 32;
+        const double2* sp = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
+        for (int e = threadIdx.x; e < total; e += NT) {
+            int blk = e >> 5, lane = e & 31;
+            // decode (i, j) of rebuild block blk
+            int i = 0, base = 0;
+            while (base + (4 * i + 3) / 8 + 1 <= blk) { base += (4 * i + 3) / 8 + 1; ++i; }
+            int j = blk - base;
+            double2 s = make_double2(0.0, 0.0);
+            for (int c = 0; c < a.n_chunks; ++c) {
+                double2 v = sp[(size_t)c * geo.NBLK * 32 + e];
+                s.x += v.x;
+                s.y += v.y;
+            }
+            int r8 = lane >> 2, c4 = lane & 3;
+            int l = 4 * i + (r8 >> 1), p = r8 & 1;
+            int m0 = 8 * j + 2 * c4;
+            if (l < L) {
+                if (m0 <= l) Xd[2 * (l * ld + m0) + p] = s.x;
+                if (m0 + 1 <= l) Xd[2 * (l * ld + m0 + 1) + p] = s.y;
+            }
+        }
+    }
+    __syncthreads();
+    const double s2 = a.noise[b];
+    for (int e = threadIdx.x; e < L * L; e += NT) {
+        int i = e / L, j = e - i * L;
+        if (i < j) {
+            double2 v = X[j * ld + i];
+            X[i * ld + j] = make_double2(v.x, -v.y);
+        } else if (i == j) {
+            X[i * ld + i] = make_double2(X[i * ld + i].x + s2, 0.0);
+        }
+    }
+    __syncthreads();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double sred[NWARP + 1];
+    __shared__ int s_flag;
+    const Geo geo = make_geo(a.L);
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int L = a.L;
+    const int ld = geo.LP + 1;
+    const size_t mat = (size_t)geo.LP * ld;
+
+    if (MODE == FAC_SOLVE) {
+        if (a.status[b] != PSCA_RUNNING) return;
+    }
+    double2 *X, *G, *rowb, *colb;
+    {
+        double2* sm = reinterpret_cast<double2*>(smem_raw);
+        rowb = sm;
+        colb = sm + 2 * geo.LP;
+        if (geo.LP <= FAC_SMEM_MAX_LP) {
+            X = sm + 4 * geo.LP;
+            G = X + mat;
+        } else {
+            X = a.scratch + (size_t)b * 2 * mat;
+            G = X + mat;
+        }
+    }
+
+    if (MODE == FAC_SOLVE && a.k_new > 0) {
+        // ---- finalise iteration k = k_new - 1 -------------------------------
+        if (tid == 0) {
+            const int k = a.k_new - 1;
+            double dx2 = 0.0, minq = INFINITY, prior = 0.0;
+            const double* rp = a.red_part + (size_t)b * a.n_chunks * 4;
+            for (int c = 0; c < a.n_chunks; ++c) {
+                dx2 += rp[4 * c];
+                minq = (rp[4 * c + 1] < minq) ? rp[4 * c + 1] : minq;
+                prior += rp[4 * c + 2];
+            }
+            const double* in = a.inst + (size_t)b * 4;
+            const double qfloor = 0.5 * L / in[0];
+            int flag = 0;
+            if (minq < qfloor) {
+                flag = PSCA_QFLOOR;
+                a.status[b] = PSCA_QFLOOR;
+                a.n_iter[b] = k;
+            } else {
+                const double un = sqrt(dx2);
+                a.update_norm[(size_t)b * a.T + k] = un;
+                if (a.objective) {
+                    double pv = 0.0;
+                    if (a.kind == PSCA_MAP_K) pv = prior;  // prior_lin already carries -1/M
+                    else if (a.kind == PSCA_MAP_UR) pv = -prior / a.n_antennas;
+                    a.objective[(size_t)b * a.T + k] = in[1] + in[2] + pv;
+                }
+                a.n_iter[b] = k + 1;
+                if (un < a.tol) {
+                    flag = PSCA_CONVERGED;
+                    a.status[b] = PSCA_CONVERGED;
+                }
+            }
+            s_flag = flag;
+        }
+        __syncthreads();
+        if (s_flag == PSCA_QFLOOR) {
+            const size_t bN = (size_t)b * a.N;
+            for (int n = tid; n < a.N; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
+            return;
+        }
+        if (s_flag != 0 || a.k_new >= a.T) return;
+    }
+
+    // ---- the matrix to work on ---------------------------------------------
+    if (MODE == FAC_SOLVE || MODE == FAC_ASSEMBLE) {
+        assemble_sigma(a, geo, b, X, ld, MODE == FAC_SOLVE && a.k_new == 0);
+        if (MODE == FAC_ASSEMBLE) {
+            double2* o = a.out_mat + (size_t)b * L * L;
+            for (int e = tid; e < L * L; e += NT) {
+                int i = e / L, j = e - i * L;
+                o[e] = X[i * ld + j];
+            }
+            return;
+        }
+    } else {
+        const double2* src = a.in_mat + (size_t)b * L * L;
+        for (int e = tid; e < L * L; e += NT) {
+            int i = e / L, j = e - i * L;
+            X[i * ld + j] = src[e];
+        }
+        __syncthreads();
+    }
+
+    double frob = 0.0;
+    if (MODE == FAC_SOLVE) {
+        double s = 0.0;
+        for (int e = tid; e < L * L; e += NT) {
+            int i = e / L, j = e - i * L;
+            double2 v = X[i * ld + j];
+            s = fma(v.x, v.x, fma(v.y, v.y, s));
+        }
+        frob = sqrt(block_sum(s, sred));
+    }
+
+    if (MODE != FAC_PREP) {
+        double logdet, pmin, pmax;
+        bool ok = gj_inverse(X, ld, L, rowb, colb, logdet, pmin, pmax);
+        if (!ok) {
+            if (tid == 0) {
+                if (MODE == FAC_SOLVE) a.status[b] = PSCA_CHOL_FAIL;
+                else a.status[b] = PSCA_CHOL_FAIL;
+                if (a.cond_est) a.cond_est[b] = INFINITY;
+            }
+            return;
+        }
+        if (MODE == FAC_OBJECTIVE) {
+            // log|Sigma| + Re sum(Sigma^-1 .* Sigma_hat^T)  (covlinalg.py:159-172)
+            const double2* P = a.in_mat2 + (size_t)b * L * L;
+            const double2* E = a.emp_cov + (size_t)b * L * L;
+            double s = 0.0;
+            for (int e = tid; e < L * L; e += NT) {
+                int i = e / L, j = e - i * L;
+                double2 pv = P[e], ev = E[(size_t)j * L + i];
+                s = fma(pv.x, ev.x, fma(-pv.y, ev.y, s));
+            }
+            s = block_sum(s, sred);
+            if (tid == 0) {
+                a.out_vec[b] = logdet + s;
+                a.status[b] = 0;
+            }
+            return;
+        }
+        symmetrize(X, ld, L);
+        if (MODE == FAC_INVERSE) {
+            double2* o = a.out_mat + (size_t)b * L * L;
+            for (int e = tid; e < L * L; e += NT) {
+                int i = e / L, j = e - i * L;
+                o[e] = X[i * ld + j];
+            }
+            if (tid == 0) {
+                a.status[b] = 0;
+                if (a.cond_est) a.cond_est[b] = pmax / pmin;
+                if (a.out_vec) a.out_vec[b] = logdet;
+            }
+            return;
+        }
+        // FAC_SOLVE: objective pieces of this iterate
+        double trace = 0.0;
+        if (a.record_objective) {
+            const double2* E = a.emp_cov + (size_t)b * L * L;
+            double s = 0.0;
+            for (int e = tid; e < L * L; e += NT) {
+                int i = e / L, j = e - i * L;
+                double2 pv = X[i * ld + j], ev = E[(size_t)j * L + i];
+                s = fma(pv.x, ev.x, fma(-pv.y, ev.y, s));
+            }
+            trace = block_sum(s, sred);
+        }
+        if (tid == 0) {
+            double* in = a.inst + (size_t)b * 4;
+            in[0] = frob;
+            in[1] = logdet;
+            in[2] = trace;
+        }
+    }
+
+    // ---- A = P^H Sigma_hat P and the fragment pack --------------------------
+    gemm_EX(a.emp_cov + (size_t)b * L * L, X, ld, G, L);
+    // FAC_PREP (quad_forms drop-in, P given by the caller): A' = P^H E P is
+    // packed from the raw P; the P' half is then replaced by (P + P^H)/2,
+    // which leaves q = Re s^H P s unchanged for any P.
+    pack_frags(X, G, ld, L, geo, a.frags + (size_t)b * geo.NB * 32);
+    if (MODE == FAC_PREP) {
+        __syncthreads();
+        // overwrite the P' halves with the symmetrised P (exact for q)
+        for (int e = tid; e < L * L; e += NT) {
+            int i = e / L, j = e - i * L;
+            if (i > j) {
+                double2 u = X[i * ld + j], v = X[j * ld + i];
+                G[i * ld + j] = make_double2(0.5 * (u.x + v.x), 0.5 * (u.y - v.y));
+            }
+        }
+        __syncthreads();
+        double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 32);
+        const int total = geo.NB * 8;
+        for (int e = tid; e < total; e += NT) {
+            int blk = e >> 3, a4 = (e >> 1) & 3, cc = e & 1;
+            int i = 0;
+            while ((i + 1) * (i + 2) <= blk) ++i;
+            int kk = blk - i * (i + 1);
+            int l = 4 * i + a4, m = 2 * kk + cc;
+            double2 pv = make_double2(0.0, 0.0);
+            if (l < L && m < l) {
+                pv = G[l * ld + m];
+                pv.x *= 2.0;
+                pv.y *= 2.0;
+            } else if (l < L && m == l) {
+                pv = make_double2(X[l * ld + l].x, 0.0);
+            }
+            for (int p = 0; p < 2; ++p)
+                for (int q = 0; q < 2; ++q) {
+                    int lane = 4 * (2 * a4 + p) + (2 * cc + q);
+                    double sg = (p == 0 && q == 1) ? -1.0 : 1.0;
+                    od[((size_t)blk * 32 + lane) * 2] = sg * comp(pv, p ^ q);
+                }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// empirical covariance (HERK): Sigma_hat = Y Y^H / M
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) herk_kernel(const double2* __restrict__ y, int L, int Mc,
+                                                  int n_antennas,
+                                                  double2* __restrict__ out) {
+    const int b = blockIdx.y;
+    const int e = blockIdx.x * NT + threadIdx.x;
+    const int npair = L * (L + 1) / 2;
+    if (e >= npair) return;
+    // decode lower-triangle pair (l >= m), row-major
+    int l = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (l * (l + 1) / 2 > e) --l;
+    while ((l + 1) * (l + 2) / 2 <= e) ++l;
+    const int m = e - l * (l + 1) / 2;
+    const double2* yl = y + ((size_t)b * L + l) * Mc;
+    const double2* ym = y + ((size_t)b * L + m) * Mc;
+    double2 s = make_double2(0.0, 0.0);
+    for (int c = 0; c < Mc; ++c) {
+        double2 u = __ldg(yl + c), v = __ldg(ym + c);
+        // u * conj(v)
+        s.x = fma(u.x, v.x, fma(u.y, v.y, s.x));
+        s.y = fma(u.y, v.x, fma(-u.x, v.y, s.y));
+    }
+    s.x = s.x / (double)n_antennas;
+    s.y = s.y / (double)n_antennas;
+    double2* o = out + (size_t)b * L * L;
+    if (l == m) {
+        o[l * L + l] = make_double2(s.x, 0.0);
+    } else {
+        o[l * L + m] = s;
+        o[m * L + l] = make_double2(s.x, -s.y);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+inline size_t align_up(size_t v) { return (v + 255) & ~size_t(255); }
+
+inline int maxbw_for(int nblk) { return (nblk + NWARP - 1) / NWARP; }
+
+inline size_t col_smem_bytes(const Geo& g) {
+    return (size_t)g.LP8 * NCT * 16 * 3 + 2 * NCT * 2 * 8 + NCT * 8;
+}
+
+inline size_t fac_smem_bytes(const Geo& g) {
+    size_t s = (size_t)4 * g.LP * 16;
+    if (g.LP <= FAC_SMEM_MAX_LP) s += (size_t)2 * g.LP * (g.LP + 1) * 16;
+    return s;
+}
+
+inline size_t fac_scratch_bytes(const Geo& g, int B) {
+    return g.LP <= FAC_SMEM_MAX_LP ? 0 : (size_t)B * 2 * g.LP * (g.LP + 1) * 16;
+}
+
+struct Carve {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t bytes) {
+        T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+        off += align_up(bytes);
+        return p;
+    }
+};
+
+// chunk count with no empty chunk: ceil(tiles / ceil(tiles / want))
+int fit_chunks(int want, int N) {
+    const int tiles = (N + NCT - 1) / NCT;
+    if (want < 1) want = 1;
+    if (want > tiles) want = tiles;
+    const int per = (tiles + want - 1) / want;
+    return (tiles + per - 1) / per;
+}
+
+int auto_chunks(int B, int N) {
+    // aim for >= ~4 CTAs per SM worth of work items on 148 SMs
+    const int target = 148 * 4;
+    return fit_chunks((target + B - 1) / (B > 0 ? B : 1), N);
+}
+
+template <int MODE>
+cudaError_t launch_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStream_t st) {
+    const int mbw = maxbw_for(g.NBLK);
+    dim3 grid(n_chunks, ca.B);
+    size_t sm = col_smem_bytes(g);
+    cudaError_t err = cudaSuccess;
+#define PSCA_LAUNCH_COL(MB)                                                            \
+    {                                                                                  \
+        auto kfn = column_kernel<MB, MODE>;                                            \
+        err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                   (int)sm);                                           \
+        if (err != cudaSuccess) return err;                                            \
+        kfn<<<grid, NT, sm, st>>>(ca);                                                 \
+    }
+    if (mbw <= 2) PSCA_LAUNCH_COL(2)
+    else if (mbw <= 4) PSCA_LAUNCH_COL(4)
+    else if (mbw <= 8) PSCA_LAUNCH_COL(8)
+    else if (mbw <= 16) PSCA_LAUNCH_COL(16)
+    else if (mbw <= 24) PSCA_LAUNCH_COL(24)
+    else if (mbw <= 36) PSCA_LAUNCH_COL(36)
+    else return cudaErrorInvalidValue;
+#undef PSCA_LAUNCH_COL
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
+    size_t sm = fac_smem_bytes(g);
+    auto kfn = factor_kernel<MODE>;
+    cudaError_t err =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (err != cudaSuccess) return err;
+    kfn<<<fa.B, NT, sm, st>>>(fa);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+struct SolveLayout {
+    double2* frags;
+    double2* sig_part;
+    double* red_part;
+    double* x_alt;
+    double* inst;
+    double2* scratch;
+    size_t total;
+};
+
+SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, void* ws) {
+    Carve cv{static_cast<char*>(ws)};
+    SolveLayout s;
+    s.frags = cv.take<double2>((size_t)a->B * g.NB * 32 * 16);
+    s.sig_part = cv.take<double2>((size_t)a->B * n_chunks * g.NBLK * 32 * 16);
+    s.red_part = cv.take<double>((size_t)a->B * n_chunks * 4 * 8);
+    s.x_alt = cv.take<double>((size_t)a->B * a->N * 8);
+    s.inst = cv.take<double>((size_t)a->B * 4 * 8);
+    s.scratch = cv.take<double2>(fac_scratch_bytes(g, a->B));
+    s.total = cv.off;
+    return s;
+}
+
+int check_solve_args(const psca_solve_args* a) {
+    if (!a || a->B < 0 || a->N < 1 || a->L < 1 || a->max_iter < 0) return PSCA_E_ARG;
+    if (a->kind < PSCA_ML_K || a->kind > PSCA_MAP_UR) return PSCA_E_ARG;
+    if (a->L > MAX_L_TILE) return PSCA_E_UNSUPPORTED;
+    if (a->n_antennas < 1) return PSCA_E_ARG;
+    if (!a->pilots || !a->emp_cov || !a->noise || !a->x_out || !a->status || !a->n_iter)
+        return PSCA_E_ARG;
+    if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_K && !a->prior_lin) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_UR && !a->prior_p) return PSCA_E_ARG;
+    if (a->max_iter > 0 && (!a->steps || !a->update_norm)) return PSCA_E_ARG;
+    return PSCA_OK;
+}
+
+int resolved_chunks(const psca_solve_args* a) {
+    return a->n_chunks > 0 ? fit_chunks(a->n_chunks, a->N) : auto_chunks(a->B, a->N);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* psca_version(void) { return PSCA_VERSION_STR; }
+
+int psca_last_launch_count(void) { return g_launches; }
+
+size_t psca_solve_workspace_bytes(const psca_solve_args* a) {
+    if (check_solve_args(a) != PSCA_OK) return 0;
+    Geo g = make_geo(a->L);
+    return solve_layout(a, g, resolved_chunks(a), nullptr).total;
+}
+
+int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes, void* stream) {
+    int rc = check_solve_args(a);
+    if (rc != PSCA_OK) return rc;
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const Geo g = make_geo(a->L);
+    const int n_chunks = resolved_chunks(a);
+    SolveLayout lay = solve_layout(a, g, n_chunks, workspace);
+    if (workspace_bytes < lay.total || (!workspace && lay.total)) return PSCA_E_WORKSPACE;
+    if (a->B == 0) return PSCA_OK;
+    const size_t BN = (size_t)a->B * a->N;
+
+    if (cudaMemsetAsync(a->x_out, 0, BN * 8, st) != cudaSuccess) return PSCA_E_CUDA;
+    if (cudaMemsetAsync(a->status, 0, (size_t)a->B * 4, st) != cudaSuccess) return PSCA_E_CUDA;
+    if (cudaMemsetAsync(a->n_iter, 0, (size_t)a->B * 4, st) != cudaSuccess) return PSCA_E_CUDA;
+    if (a->cond_est) cudaMemsetAsync(a->cond_est, 0, (size_t)a->B * 8, st);
+    if (a->iterates) cudaMemsetAsync(a->iterates, 0, BN * (a->max_iter + 1) * 8, st);
+    if (a->max_iter == 0) return cudaGetLastError() == cudaSuccess ? PSCA_OK : PSCA_E_CUDA;
+    cudaMemsetAsync(a->update_norm, 0, (size_t)a->B * a->max_iter * 8, st);
+    if (a->objective) cudaMemsetAsync(a->objective, 0, (size_t)a->B * a->max_iter * 8, st);
+
+    ColArgs ca{};
+    ca.kind = a->kind; ca.B = a->B; ca.N = a->N; ca.L = a->L; ca.n_chunks = n_chunks;
+    {
+        int tiles = (a->N + NCT - 1) / NCT;
+        ca.chunk_cols = ((tiles + n_chunks - 1) / n_chunks) * NCT;
+    }
+    ca.T = a->max_iter; ca.n_antennas = a->n_antennas;
+    ca.record_objective = a->record_objective && a->objective;
+    ca.pilots = reinterpret_cast<const double2*>(a->pilots);
+    ca.gains = a->gains; ca.iterates = a->iterates; ca.frags = lay.frags;
+    ca.sig_part = lay.sig_part; ca.red_part = lay.red_part; ca.status = a->status;
+    ca.steps = a->steps; ca.prior_lin = a->prior_lin; ca.prior_p = a->prior_p; ca.eff = a->eff;
+
+    FacArgs fa{};
+    fa.B = a->B; fa.N = a->N; fa.L = a->L; fa.T = a->max_iter; fa.n_chunks = n_chunks;
+    fa.kind = a->kind; fa.n_antennas = a->n_antennas;
+    fa.record_objective = ca.record_objective; fa.tol = a->tol;
+    fa.noise = a->noise; fa.emp_cov = reinterpret_cast<const double2*>(a->emp_cov);
+    fa.sig_part = lay.sig_part; fa.red_part = lay.red_part; fa.frags = lay.frags;
+    fa.inst = lay.inst; fa.status = a->status; fa.n_iter = a->n_iter; fa.cond_est = a->cond_est;
+    fa.update_norm = a->update_norm; fa.objective = ca.record_objective ? a->objective : nullptr;
+    fa.scratch = lay.scratch;
+
+    double* xc = a->x_out;
+    double* xn = lay.x_alt;
+    fa.k_new = 0; fa.x_cur = xc; fa.x_next = xn;
+    if (launch_factor<FAC_SOLVE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+    for (int k = 0; k < a->max_iter; ++k) {
+        ca.k = k; ca.x_cur = xc; ca.x_next = xn;
+        if (launch_column<COL_SOLVE>(ca, g, n_chunks, st) != cudaSuccess) return PSCA_E_CUDA;
+        fa.k_new = k + 1; fa.x_cur = xc; fa.x_next = xn;
+        if (launch_factor<FAC_SOLVE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+        double* t = xc; xc = xn; xn = t;
+    }
+    if (xc != a->x_out) {
+        if (cudaMemcpyAsync(a->x_out, xc, BN * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return PSCA_E_CUDA;
+    }
+    return cudaGetLastError() == cudaSuccess ? PSCA_OK : PSCA_E_CUDA;
+}
+
+int psca_empirical_cov(const double* y, int B, int L, int Mc, int n_antennas, double* out,
+                       void* stream) {
+    if (!y || !out || B < 0 || L < 1 || Mc < 0 || n_antennas < 1) return PSCA_E_ARG;
+    if (B == 0) return PSCA_OK;
+    g_launches = 0;
+    const int npair = L * (L + 1) / 2;
+    dim3 grid((npair + NT - 1) / NT, B);
+    herk_kernel<<<grid, NT, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const double2*>(y), L, Mc, n_antennas,
+        reinterpret_cast<double2*>(out));
+    ++g_launches;
+    return cudaGetLastError() == cudaSuccess ? PSCA_OK : PSCA_E_CUDA;
+}
+
+size_t psca_cov_workspace_bytes(int B, int N, int L) {
+    if (B < 0 || N < 1 || L < 1 || L > MAX_L_TILE) return 0;
+    Geo g = make_geo(L);
+    int nc = auto_chunks(B, N);
+    Carve cv{nullptr};
+    cv.take<double2>((size_t)B * nc * g.NBLK * 32 * 16);
+    cv.take<double>((size_t)B * nc * 4 * 8);
+    cv.take<double2>(fac_scratch_bytes(g, B));
+    return cv.off;
+}
+
+int psca_cov_unknown(const double* pilots, const double* w, const double* noise, int B, int N,
+                     int L, double* out, void* workspace, size_t workspace_bytes, void* stream) {
+    if (!pilots || !w || !noise || !out || B < 0 || N < 1 || L < 1) return PSCA_E_ARG;
+    if (L > MAX_L_TILE) return PSCA_E_UNSUPPORTED;
+    if (workspace_bytes < psca_cov_workspace_bytes(B, N, L)) return PSCA_E_WORKSPACE;
+    if (B == 0) return PSCA_OK;
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Geo g = make_geo(L);
+    int nc = auto_chunks(B, N);
+    Carve cv{static_cast<char*>(workspace)};
+    double2* sig_part = cv.take<double2>((size_t)B * nc * g.NBLK * 32 * 16);
+    double* red_part = cv.take<double>((size_t)B * nc * 4 * 8);
+    double2* scratch = cv.take<double2>(fac_scratch_bytes(g, B));
+    ColArgs ca{};
+    ca.kind = PSCA_ML_UD; ca.B = B; ca.N = N; ca.L = L; ca.n_chunks = nc;
+    int tiles = (N + NCT - 1) / NCT;
+    ca.chunk_cols = ((tiles + nc - 1) / nc) * NCT;
+    ca.pilots = reinterpret_cast<const double2*>(pilots);
+    ca.sig_part = sig_part; ca.red_part = red_part; ca.w_in = w;
+    if (launch_column<COL_REBUILD>(ca, g, nc, st) != cudaSuccess) return PSCA_E_CUDA;
+    FacArgs fa{};
+    fa.B = B; fa.N = N; fa.L = L; fa.n_chunks = nc; fa.noise = noise; fa.sig_part = sig_part;
+    fa.scratch = scratch; fa.out_mat = reinterpret_cast<double2*>(out);
+    if (launch_factor<FAC_ASSEMBLE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+    return PSCA_OK;
+}
+
+size_t psca_inverse_workspace_bytes(int B, int L) {
+    if (B < 0 || L < 1) return 0;
+    return fac_scratch_bytes(make_geo(L), B);
+}
+
+int psca_hpd_inverse(const double* sigma, int B, int L, double* out, int* status,
+                     double* cond_est, double* logdet, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    if (!sigma || !out || !status || B < 0 || L < 1) return PSCA_E_ARG;
+    if (workspace_bytes < psca_inverse_workspace_bytes(B, L)) return PSCA_E_WORKSPACE;
+    if (B == 0) return PSCA_OK;
+    g_launches = 0;
+    Geo g = make_geo(L);
+    FacArgs fa{};
+    fa.B = B; fa.L = L; fa.in_mat = reinterpret_cast<const double2*>(sigma);
+    fa.out_mat = reinterpret_cast<double2*>(out); fa.status = status; fa.cond_est = cond_est;
+    fa.out_vec = logdet; fa.scratch = static_cast<double2*>(workspace);
+    if (launch_factor<FAC_INVERSE>(fa, g, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return PSCA_E_CUDA;
+    return PSCA_OK;
+}
+
+size_t psca_quad_workspace_bytes(int B, int N, int L) {
+    if (B < 0 || N < 1 || L < 1 || L > MAX_L_TILE) return 0;
+    Geo g = make_geo(L);
+    Carve cv{nullptr};
+    cv.take<double2>((size_t)B * g.NB * 32 * 16);
+    cv.take<double2>(fac_scratch_bytes(g, B));
+    return cv.off;
+}
+
+int psca_quad_forms(const double* pilots, const double* sigma_inv, const double* emp_cov, int B,
+                    int N, int L, double* q, double* r, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+    if (!pilots || !sigma_inv || !emp_cov || !q || !r || B < 0 || N < 1 || L < 1)
+        return PSCA_E_ARG;
+    if (L > MAX_L_TILE) return PSCA_E_UNSUPPORTED;
+    if (workspace_bytes < psca_quad_workspace_bytes(B, N, L)) return PSCA_E_WORKSPACE;
+    if (B == 0) return PSCA_OK;
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Geo g = make_geo(L);
+    Carve cv{static_cast<char*>(workspace)};
+    double2* frags = cv.take<double2>((size_t)B * g.NB * 32 * 16);
+    double2* scratch = cv.take<double2>(fac_scratch_bytes(g, B));
+    FacArgs fa{};
+    fa.B = B; fa.L = L; fa.in_mat = reinterpret_cast<const double2*>(sigma_inv);
+    fa.emp_cov = reinterpret_cast<const double2*>(emp_cov); fa.frags = frags;
+    fa.scratch = scratch;
+    if (launch_factor<FAC_PREP>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+    int nc = auto_chunks(B, N);
+    ColArgs ca{};
+    ca.kind = PSCA_ML_UD; ca.B = B; ca.N = N; ca.L = L; ca.n_chunks = nc;
+    int tiles = (N + NCT - 1) / NCT;
+    ca.chunk_cols = ((tiles + nc - 1) / nc) * NCT;
+    ca.pilots = reinterpret_cast<const double2*>(pilots);
+    ca.frags = frags; ca.q_out = q; ca.r_out = r;
+    if (launch_column<COL_QUAD>(ca, g, nc, st) != cudaSuccess) return PSCA_E_CUDA;
+    return PSCA_OK;
+}
+
+size_t psca_objective_workspace_bytes(int B, int L) { return psca_inverse_workspace_bytes(B, L); }
+
+int psca_eval_objective(const double* sigma, const double* sigma_inv, const double* emp_cov,
+                        int B, int L, double* out, int* status, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    if (!sigma || !sigma_inv || !emp_cov || !out || !status || B < 0 || L < 1) return PSCA_E_ARG;
+    if (workspace_bytes < psca_objective_workspace_bytes(B, L)) return PSCA_E_WORKSPACE;
+    if (B == 0) return PSCA_OK;
+    g_launches = 0;
+    Geo g = make_geo(L);
+    FacArgs fa{};
+    fa.B = B; fa.L = L; fa.in_mat = reinterpret_cast<const double2*>(sigma);
+    fa.in_mat2 = reinterpret_cast<const double2*>(sigma_inv);
+    fa.emp_cov = reinterpret_cast<const double2*>(emp_cov);
+    fa.out_vec = out; fa.status = status; fa.scratch = static_cast<double2*>(workspace);
+    if (launch_factor<FAC_OBJECTIVE>(fa, g, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return PSCA_E_CUDA;
+    return PSCA_OK;
+}
+
+}  // extern "C"

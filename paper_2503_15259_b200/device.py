@@ -1,0 +1,323 @@
+"""ctypes binding of the C ABI in include/psca.h (the product's only compute path).
+
+torch is used for device memory, streams and host<->device copies only; every
+FLOP of the solver runs in ``_psca.so`` (built from ``csrc/psca.cu`` for
+sm_100a).  There is no CPU fallback: a missing library or a missing GPU raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import pathlib
+import threading
+
+import numpy as np
+
+_HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = _HERE / "_psca.so"
+
+KIND_CODES = {"ml-k": 0, "map-k": 1, "ml-ud": 2, "map-ur": 3}
+STATUS_RUNNING, STATUS_CHOL_FAIL, STATUS_QFLOOR, STATUS_CONVERGED = 0, 1, 2, 3
+
+_lock = threading.Lock()
+_lib = None
+
+
+class PscaNativeError(RuntimeError):
+    """The CUDA library is missing, the GPU is missing, or a call failed."""
+
+
+class EffPriorC(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_double) for name in
+                ("eps", "g_low", "g_high", "dead_zone_grad", "p_lin", "k", "eta", "area2",
+                 "cv", "cw")]
+
+
+class SolveArgsC(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int), ("B", ctypes.c_int), ("N", ctypes.c_int), ("L", ctypes.c_int),
+        ("n_antennas", ctypes.c_int), ("max_iter", ctypes.c_int), ("tol", ctypes.c_double),
+        ("record_objective", ctypes.c_int), ("n_chunks", ctypes.c_int),
+        ("pilots", ctypes.c_void_p), ("gains", ctypes.c_void_p), ("emp_cov", ctypes.c_void_p),
+        ("noise", ctypes.c_void_p), ("steps", ctypes.c_void_p), ("prior_lin", ctypes.c_void_p),
+        ("prior_p", ctypes.c_void_p), ("eff", EffPriorC),
+        ("x_out", ctypes.c_void_p), ("update_norm", ctypes.c_void_p),
+        ("objective", ctypes.c_void_p), ("iterates", ctypes.c_void_p),
+        ("status", ctypes.c_void_p), ("n_iter", ctypes.c_void_p), ("cond_est", ctypes.c_void_p),
+    ]
+
+
+# exported symbols and their signatures (must match include/psca.h)
+_SIGS = {
+    "psca_version": (ctypes.c_char_p, []),
+    "psca_last_launch_count": (ctypes.c_int, []),
+    "psca_solve_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(SolveArgsC)]),
+    "psca_solve": (ctypes.c_int, [ctypes.POINTER(SolveArgsC), ctypes.c_void_p, ctypes.c_size_t,
+                                  ctypes.c_void_p]),
+    "psca_empirical_cov": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                          ctypes.c_void_p]),
+    "psca_cov_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "psca_cov_unknown": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "psca_inverse_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int]),
+    "psca_hpd_inverse": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_void_p]),
+    "psca_quad_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "psca_quad_forms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.c_void_p]),
+    "psca_objective_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int]),
+    "psca_eval_objective": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                           ctypes.c_void_p]),
+}
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+def load() -> ctypes.CDLL:
+    """Load ``_psca.so`` (raises PscaNativeError when it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise PscaNativeError(
+                    f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                    "g.build()'` (there is no CPU fallback)")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise PscaNativeError("the PSCA solver needs a CUDA GPU (sm_100a); none is visible")
+    return torch
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        names = {-1: "bad argument", -2: "CUDA error", -3: "workspace too small",
+                 -4: "unsupported shape"}
+        raise PscaNativeError(f"{what} failed: {names.get(rc, rc)}")
+
+
+def _stream(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _workspace(torch, nbytes: int, device):
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def _dev(torch, arr, dtype, device):
+    if isinstance(arr, torch.Tensor):
+        return arr.to(device=device, dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(arr), dtype=dtype, device=device)
+
+
+# ---------------------------------------------------------------------------
+# the batched solver (device tensors in, device tensors out)
+# ---------------------------------------------------------------------------
+
+def eff_prior_struct(prior) -> EffPriorC:
+    """psca_eff_prior from an EffPathlossPrior-like object (priors.py:173-281)."""
+    if prior is None:
+        return EffPriorC()
+    p_lin = 10.0 ** (prior.tx_power_dbm / 10.0)
+    k = 4.0 * np.pi / prior.wavelength
+    cv, cw = prior._hermite_coeffs()
+    return EffPriorC(eps=float(prior.eps), g_low=float(prior.g_low), g_high=float(prior.g_high),
+                     dead_zone_grad=float(prior.dead_zone_grad), p_lin=float(p_lin), k=float(k),
+                     eta=float(prior.pathloss_exp),
+                     area2=float(prior.d_outer ** 2 - prior.d_inner ** 2), cv=float(cv),
+                     cw=float(cw))
+
+
+def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=None,
+          prior_lin=None, prior_p=None, eff_prior=None, max_iter: int | None = None,
+          tol: float = 0.0, record_objective: bool = False, record_iterates: bool = False,
+          n_chunks: int = 0, out=None):
+    """Run the batched PSCA solve on the current CUDA device / stream.
+
+    pilots (B,L,N) complex128, emp_cov (B,L,L) complex128, noise (B,) float64,
+    gains (B,N) float64 for known-pathloss kinds, steps (T,) float64.
+    Inputs may be numpy arrays or torch tensors (moved to the device if
+    needed).  Returns a dict of device tensors: x (B,N), update_norm (B,T),
+    objective (B,T) or None, iterates (B,T+1,N) or None, status (B,) int32,
+    n_iter (B,) int32, cond_est (B,).
+    """
+    torch = _torch()
+    lib = load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if kind not in KIND_CODES:
+        raise ValueError(f"unknown problem kind {kind!r}")
+    S = _dev(torch, pilots, torch.complex128, dev)
+    if S.dim() != 3:
+        raise ValueError("pilots must be (B, L, N)")
+    B, L, N = S.shape
+    E = _dev(torch, emp_cov, torch.complex128, dev)
+    sig2 = _dev(torch, noise, torch.float64, dev).reshape(B)
+    st = _dev(torch, steps, torch.float64, dev).reshape(-1)
+    T = int(st.numel()) if max_iter is None else int(max_iter)
+    if st.numel() < T:
+        raise ValueError("need one step per iteration")
+    g = _dev(torch, gains, torch.float64, dev) if gains is not None else None
+    pl = _dev(torch, prior_lin, torch.float64, dev) if prior_lin is not None else None
+    pp = _dev(torch, prior_p, torch.float64, dev) if prior_p is not None else None
+    if out is None:
+        out = {}
+    x = out.get("x")
+    if x is None:
+        x = torch.empty((B, N), dtype=torch.float64, device=dev)
+    un = torch.empty((B, max(T, 1)), dtype=torch.float64, device=dev)
+    obj = torch.empty((B, max(T, 1)), dtype=torch.float64, device=dev) if record_objective else None
+    its = torch.empty((B, T + 1, N), dtype=torch.float64, device=dev) if record_iterates else None
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    n_iter = torch.empty(B, dtype=torch.int32, device=dev)
+    cond = torch.empty(B, dtype=torch.float64, device=dev)
+    args = SolveArgsC(
+        kind=KIND_CODES[kind], B=B, N=N, L=L, n_antennas=int(n_antennas), max_iter=T,
+        tol=float(tol), record_objective=int(bool(record_objective)), n_chunks=int(n_chunks),
+        pilots=S.data_ptr(), gains=g.data_ptr() if g is not None else 0, emp_cov=E.data_ptr(),
+        noise=sig2.data_ptr(), steps=st.data_ptr(),
+        prior_lin=pl.data_ptr() if pl is not None else 0,
+        prior_p=pp.data_ptr() if pp is not None else 0,
+        eff=eff_prior_struct(eff_prior), x_out=x.data_ptr(), update_norm=un.data_ptr(),
+        objective=obj.data_ptr() if obj is not None else 0,
+        iterates=its.data_ptr() if its is not None else 0, status=status.data_ptr(),
+        n_iter=n_iter.data_ptr(), cond_est=cond.data_ptr())
+    nbytes = lib.psca_solve_workspace_bytes(ctypes.byref(args))
+    if nbytes == 0 and B > 0:
+        raise PscaNativeError("psca_solve rejected the arguments (shape/kind/pointers)")
+    ws = out.get("_ws")
+    if ws is None or ws.numel() < nbytes:
+        ws = _workspace(torch, nbytes, dev)
+    _check(lib.psca_solve(ctypes.byref(args), _ptr(ws), ctypes.c_size_t(ws.numel()),
+                          _stream(torch)), "psca_solve")
+    return {"x": x, "update_norm": un[:, :T], "objective": obj[:, :T] if obj is not None else None,
+            "iterates": its, "status": status, "n_iter": n_iter, "cond_est": cond, "_ws": ws,
+            "launches": lib.psca_last_launch_count()}
+
+
+# ---------------------------------------------------------------------------
+# component entry points (numpy or tensors in; numpy out for numpy input)
+# ---------------------------------------------------------------------------
+
+def _batched(arr, ndim):
+    a = np.asarray(arr)
+    return (a[None], True) if a.ndim == ndim else (a, False)
+
+
+def empirical_cov(y, n_antennas: int):
+    torch = _torch()
+    lib = load()
+    ya, single = _batched(y, 2)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Y = _dev(torch, ya, torch.complex128, dev)
+    B, L, Mc = Y.shape
+    out = torch.empty((B, L, L), dtype=torch.complex128, device=dev)
+    _check(lib.psca_empirical_cov(_ptr(Y), B, L, Mc, int(n_antennas), _ptr(out), _stream(torch)),
+           "psca_empirical_cov")
+    res = out.cpu().numpy()
+    return res[0] if single else res
+
+
+def cov_unknown(pilots, weights, noise):
+    torch = _torch()
+    lib = load()
+    pa, single = _batched(pilots, 2)
+    wa = np.asarray(weights, dtype=float).reshape(pa.shape[0], pa.shape[2])
+    na = np.broadcast_to(np.asarray(noise, dtype=float), (pa.shape[0],)).copy()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S = _dev(torch, pa, torch.complex128, dev)
+    W = _dev(torch, wa, torch.float64, dev)
+    Nz = _dev(torch, na, torch.float64, dev)
+    B, L, N = S.shape
+    out = torch.empty((B, L, L), dtype=torch.complex128, device=dev)
+    ws = _workspace(torch, lib.psca_cov_workspace_bytes(B, N, L), dev)
+    _check(lib.psca_cov_unknown(_ptr(S), _ptr(W), _ptr(Nz), B, N, L, _ptr(out), _ptr(ws),
+                                ctypes.c_size_t(ws.numel()), _stream(torch)), "psca_cov_unknown")
+    res = out.cpu().numpy()
+    return res[0] if single else res
+
+
+def hpd_inverse(sigma):
+    """Returns (inverse, status, cond_est, logdet) as numpy arrays."""
+    torch = _torch()
+    lib = load()
+    sa, single = _batched(sigma, 2)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    X = _dev(torch, sa, torch.complex128, dev)
+    B, L, _ = X.shape
+    out = torch.empty_like(X)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    cond = torch.empty(B, dtype=torch.float64, device=dev)
+    logdet = torch.empty(B, dtype=torch.float64, device=dev)
+    ws = _workspace(torch, lib.psca_inverse_workspace_bytes(B, L), dev)
+    _check(lib.psca_hpd_inverse(_ptr(X), B, L, _ptr(out), _ptr(status), _ptr(cond), _ptr(logdet),
+                                _ptr(ws), ctypes.c_size_t(ws.numel()), _stream(torch)),
+           "psca_hpd_inverse")
+    res = (out.cpu().numpy(), status.cpu().numpy(), cond.cpu().numpy(), logdet.cpu().numpy())
+    return tuple(r[0] for r in res) if single else res
+
+
+def quad_forms(pilots, sigma_inv, emp_cov):
+    torch = _torch()
+    lib = load()
+    pa, single = _batched(pilots, 2)
+    B, L, N = pa.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S = _dev(torch, pa, torch.complex128, dev)
+    P = _dev(torch, np.asarray(sigma_inv).reshape(B, L, L), torch.complex128, dev)
+    E = _dev(torch, np.asarray(emp_cov).reshape(B, L, L), torch.complex128, dev)
+    q = torch.empty((B, N), dtype=torch.float64, device=dev)
+    r = torch.empty((B, N), dtype=torch.float64, device=dev)
+    ws = _workspace(torch, lib.psca_quad_workspace_bytes(B, N, L), dev)
+    _check(lib.psca_quad_forms(_ptr(S), _ptr(P), _ptr(E), B, N, L, _ptr(q), _ptr(r), _ptr(ws),
+                               ctypes.c_size_t(ws.numel()), _stream(torch)), "psca_quad_forms")
+    qn, rn = q.cpu().numpy(), r.cpu().numpy()
+    return (qn[0], rn[0]) if single else (qn, rn)
+
+
+def eval_objective(sigma, sigma_inv, emp_cov):
+    """Returns (value, status) numpy arrays."""
+    torch = _torch()
+    lib = load()
+    sa, single = _batched(sigma, 2)
+    B, L, _ = sa.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    X = _dev(torch, sa, torch.complex128, dev)
+    P = _dev(torch, np.asarray(sigma_inv).reshape(B, L, L), torch.complex128, dev)
+    E = _dev(torch, np.asarray(emp_cov).reshape(B, L, L), torch.complex128, dev)
+    out = torch.empty(B, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+    ws = _workspace(torch, lib.psca_objective_workspace_bytes(B, L), dev)
+    _check(lib.psca_eval_objective(_ptr(X), _ptr(P), _ptr(E), B, L, _ptr(out), _ptr(status),
+                                   _ptr(ws), ctypes.c_size_t(ws.numel()), _stream(torch)),
+           "psca_eval_objective")
+    v, s = out.cpu().numpy(), status.cpu().numpy()
+    return (v[0], s[0]) if single else (v, s)
+
+
+def version() -> str:
+    return load().psca_version().decode()
+
+
+def finite_or_inf(v: float) -> float:
+    return v if math.isfinite(v) else math.inf

@@ -1,0 +1,272 @@
+"""PSCA engine entry points (mirror of actdet.estimators, GPU-backed).
+
+``psca_run`` keeps the reference signature (estimators.py:239-289) and
+returns the same ``DetectorTrace``; the whole iteration loop runs on the GPU
+as 1 + 2T kernel launches (csrc/psca.cu: factor_kernel / column_kernel).
+``psca_run_batch`` is the throughput entry: B independent instances in one
+call, device tensors in and out.
+"""
+
+from __future__ import annotations
+
+import json
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import device, priors
+from .sysmodel import DomainError
+
+KINDS = ("ml-k", "map-k", "ml-ud", "map-ur")
+
+
+@dataclass(frozen=True)
+class Problem:
+    """Which objective is minimised; MAP kinds carry their prior (estimators.py:30-63)."""
+
+    kind: str
+    prior: object | None = None
+
+    def __post_init__(self):
+        if self.kind not in KINDS:
+            raise DomainError(f"unknown problem kind {self.kind!r}")
+        if self.kind in ("map-k", "map-ur") and self.prior is None:
+            raise DomainError(f"{self.kind} requires a prior")
+        if self.kind in ("ml-k", "ml-ud") and self.prior is not None:
+            raise DomainError(f"{self.kind} does not take a prior")
+
+    @classmethod
+    def ml_k(cls):
+        return cls("ml-k")
+
+    @classmethod
+    def map_k(cls, prior):
+        return cls("map-k", prior)
+
+    @classmethod
+    def ml_ud(cls):
+        return cls("ml-ud")
+
+    @classmethod
+    def map_ur(cls, prior):
+        return cls("map-ur", prior)
+
+    @property
+    def known_pathloss(self) -> bool:
+        return self.kind in ("ml-k", "map-k")
+
+
+def default_schedule(k: int) -> float:
+    """k-th step of rho <- rho (1 - rho/2), rho_0 = 1/2 (estimators.py:66-73)."""
+    if k < 0:
+        raise DomainError("iteration index must be >= 0")
+    rho = 0.5
+    for _ in range(k):
+        rho = rho * (1.0 - 0.5 * rho)
+    return rho
+
+
+def default_steps(n: int) -> np.ndarray:
+    """First n steps of the default schedule (estimators.py:76-83)."""
+    out = np.empty(n)
+    rho = 0.5
+    for i in range(n):
+        out[i] = rho
+        rho = rho * (1.0 - 0.5 * rho)
+    return out
+
+
+@dataclass
+class StepSchedule:
+    """Per-iteration steps: a rule k -> rho or an explicit vector (estimators.py:86-128)."""
+
+    fn: object | None = None
+    steps: np.ndarray | None = None
+
+    def __post_init__(self):
+        if (self.fn is None) == (self.steps is None):
+            raise DomainError("provide exactly one of fn or steps")
+        if self.steps is not None:
+            self.steps = np.asarray(self.steps, dtype=float)
+            if np.any(self.steps <= 0.0) or np.any(self.steps > 1.0):
+                raise DomainError("every step must lie in (0,1]")
+
+    @classmethod
+    def default(cls) -> "StepSchedule":
+        return cls(fn=default_schedule)
+
+    @classmethod
+    def polynomial(cls, offset: float = 4.0, exponent: float = 0.8) -> "StepSchedule":
+        if not 0.5 < exponent <= 1.0:
+            raise DomainError("exponent must lie in (0.5, 1] for admissibility")
+        return cls(fn=lambda k: (1.0 + k / offset) ** -exponent)
+
+    @classmethod
+    def explicit(cls, steps) -> "StepSchedule":
+        return cls(steps=steps)
+
+    def __call__(self, k: int) -> float:
+        if self.steps is not None:
+            return float(self.steps[k])
+        rho = float(self.fn(k))
+        if not 0.0 < rho <= 1.0:
+            raise DomainError(f"schedule produced step {rho} outside (0,1]")
+        return rho
+
+    def materialize(self, n: int) -> np.ndarray:
+        """rho_0..rho_{n-1} as the device step vector.
+
+        The default rule uses the recursion directly (bitwise the values
+        ``default_schedule(k)`` returns); other rules are evaluated eagerly, so
+        an invalid step anywhere in the first n raises up front.
+        """
+        if self.steps is not None:
+            return np.asarray(self.steps[:n], dtype=float)
+        if self.fn is default_schedule:
+            return default_steps(n)
+        return np.array([self(k) for k in range(n)], dtype=float)
+
+
+@dataclass
+class DetectorTrace:
+    """Per-iteration record of one run (estimators.py:131-164).
+
+    wall_times: the solve is one device call, so each entry is the mean
+    device time per iteration of that call (CUDA events).
+    """
+
+    iterates: list = field(default_factory=list)
+    objective: list = field(default_factory=list)
+    update_norm: list = field(default_factory=list)
+    wall_times: list = field(default_factory=list)
+    final: np.ndarray | None = None
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_iterations(self) -> int:
+        return len(self.update_norm)
+
+    def dump_jsonl(self, path, method: str = ""):
+        with open(path, "a", encoding="utf-8") as fh:
+            for k in range(self.n_iterations):
+                rec = {
+                    "method": method or self.meta.get("method", ""),
+                    "iteration": k + 1,
+                    "update_norm": self.update_norm[k],
+                    "objective": self.objective[k] if k < len(self.objective) else None,
+                    "wall_time_s": self.wall_times[k],
+                }
+                fh.write(json.dumps(rec) + "\n")
+
+
+def bounds_for(problem, sample=None) -> tuple[float, float]:
+    """Coordinate box (estimators.py:167-173)."""
+    if problem.kind in ("ml-k", "map-k"):
+        return 0.0, 1.0
+    if problem.kind == "ml-ud":
+        return 0.0, np.inf
+    return 0.0, problem.prior.g_high
+
+
+def prior_arrays(problem, n_devices: int, n_antennas: int) -> dict:
+    """Device-side prior inputs for ``device.solve`` from a Problem."""
+    if problem.kind == "map-k":
+        return {"prior_lin": priors.known_prior_gradient(problem.prior, n_antennas, n_devices)}
+    if problem.kind == "map-ur":
+        p = np.broadcast_to(np.asarray(problem.prior.p, dtype=float), (n_devices,)).copy()
+        return {"prior_p": p, "eff_prior": problem.prior}
+    return {}
+
+
+ABORT_COND = "Sigma is numerically singular (estimated condition number {:.3e})"
+ABORT_QFLOOR = "quadratic form underflow; inverse inconsistent"
+
+
+def psca_run(problem, sample, schedule: StepSchedule | None = None, max_iter: int = 30,
+             tol: float = 1e-4, record_objective: bool = True) -> DetectorTrace:
+    """Run the PSCA iteration from the all-zero start on the GPU (estimators.py:239-289).
+
+    Same stopping rules and trace contents as the reference: stops at
+    max_iter or when the update norm drops below tol; a singular covariance
+    or a q-floor violation ends the run with ``meta["abort"]`` set and
+    ``final`` = the last accepted iterate.
+    """
+    import torch
+
+    if schedule is None:
+        schedule = StepSchedule.default()
+    n = sample.n_devices
+    trace = DetectorTrace(meta={"kind": problem.kind, "tol": tol})
+    if problem.kind == "map-ur":
+        trace.meta["dead_zone_grad"] = problem.prior.dead_zone_grad
+    n_steps = max_iter
+    if schedule.steps is not None and len(schedule.steps) < max_iter:
+        n_steps = len(schedule.steps)    # the reference would IndexError at k = len(steps)
+    steps = schedule.materialize(n_steps)
+    m = sample.n_antennas
+    kw = prior_arrays(problem, n, m)
+    t0 = torch.cuda.Event(enable_timing=True) if torch.cuda.is_available() else None
+    t1 = torch.cuda.Event(enable_timing=True) if torch.cuda.is_available() else None
+    if t0 is not None:
+        t0.record()
+    res = device.solve(problem.kind, np.asarray(sample.pilots)[None],
+                       np.asarray(sample.emp_cov)[None], np.array([sample.noise_power], float), m,
+                       steps, gains=np.asarray(sample.gains, dtype=float)[None] if problem.known_pathloss else None,
+                       max_iter=n_steps, tol=tol, record_objective=record_objective,
+                       record_iterates=True, **kw)
+    if t1 is not None:
+        t1.record()
+    status = int(res["status"][0].item())
+    k_done = int(res["n_iter"][0].item())
+    its = res["iterates"][0, :k_done + 1].cpu().numpy()
+    trace.iterates = [its[i].copy() for i in range(k_done + 1)]
+    trace.update_norm = [float(v) for v in res["update_norm"][0, :k_done].cpu().numpy()]
+    if record_objective:
+        trace.objective = [float(v) for v in res["objective"][0, :k_done].cpu().numpy()]
+    torch.cuda.synchronize()
+    per = (t0.elapsed_time(t1) * 1e-3 / max(k_done, 1)) if t0 is not None else 0.0
+    trace.wall_times = [per] * k_done
+    if status == device.STATUS_CHOL_FAIL:
+        trace.meta["abort"] = ABORT_COND.format(float(res["cond_est"][0].item()))
+    elif status == device.STATUS_QFLOOR:
+        trace.meta["abort"] = ABORT_QFLOOR
+    trace.final = res["x"][0].cpu().numpy().copy()
+    if (status in (device.STATUS_RUNNING,) and schedule.steps is not None
+            and len(schedule.steps) < max_iter):
+        raise IndexError("explicit schedule shorter than max_iter")
+    return trace
+
+
+def psca_run_batch(problem, pilots, emp_cov, noise, n_antennas: int, gains=None,
+                   schedule: StepSchedule | None = None, max_iter: int = 30, tol: float = 0.0,
+                   record_objective: bool = False, n_chunks: int = 0, out=None) -> dict:
+    """B independent PSCA runs in one device call.
+
+    pilots (B,L,N), emp_cov (B,L,L), noise (B,), gains (B,N); numpy arrays
+    or CUDA tensors.  Returns device tensors (see ``device.solve``).
+    """
+    if schedule is None:
+        schedule = StepSchedule.default()
+    steps = schedule.materialize(max_iter)
+    n = pilots.shape[-1]
+    kw = prior_arrays(problem, n, n_antennas)
+    if problem.known_pathloss and gains is None:
+        raise DomainError("known-pathloss problems need the gains")
+    return device.solve(problem.kind, pilots, emp_cov, noise, n_antennas, steps,
+                        gains=gains if problem.known_pathloss else None, max_iter=max_iter,
+                        tol=tol, record_objective=record_objective, n_chunks=n_chunks, out=out,
+                        **kw)
+
+
+# -- elementwise helpers kept for API parity (estimators.py:176-200); the
+#    solver never calls them: the same arithmetic is fused in column_kernel.
+
+def surrogate_coef(problem, state, gains):
+    if problem.known_pathloss:
+        return (gains * state.q) ** 2
+    return state.q ** 2
+
+
+def coord_solution(x, grad, coef, lo, hi):
+    return np.clip(x - grad / coef, lo, hi)

@@ -1,0 +1,188 @@
+"""CUDA path vs the reference outputs (golden fixtures) and the CPU oracle.
+
+All tests here need a GPU.  Every call goes through the C ABI
+(paper_2503_15259_b200/_psca.so).  Tolerances: 1e-9 relative on gamma /
+alpha for ml-k, map-k and ml-ud (north star); map-ur uses the same bar unless
+the reference itself is measurably unstable on the instance,
+in which case the bound is stated per test.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import psca_oracle as orc   # checker only
+from psca_testutil import case, max_rel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def _pkg():
+    import paper_2503_15259_b200 as pkg
+    from paper_2503_15259_b200 import estimators, priors, unroll
+    return pkg, estimators, priors, unroll
+
+
+def _sample(c):
+    pkg, *_ = _pkg()
+    return pkg.Sample(pilots=c["pilots"], gains=c["gains"], activities=c["activities"],
+                      eff_pathloss=c["activities"] * c["gains"], received=c["received"],
+                      emp_cov=c["emp_cov"], noise_power=float(c["noise"]))
+
+
+def _problem(c):
+    pkg, est, pri, _ = _pkg()
+    kind = str(c["kind"])
+    n = c["pilots"].shape[1]
+    if kind == "ml-k":
+        return est.Problem.ml_k()
+    if kind == "ml-ud":
+        return est.Problem.ml_ud()
+    if kind == "map-k":
+        return est.Problem.map_k(pri.IndependentPrior(np.full(n, float(c["p"]))))
+    f = c["eff"]
+    prior = pri.EffPathlossPrior(np.full(n, float(c["p"])), f[0], f[1], f[2], f[3], f[4], f[5])
+    return est.Problem.map_ur(prior)
+
+
+def _tol(c, steps, max_iter, stop_tol=0.0):
+    """1e-9, or 10x the reference's own sensitivity floor for map-ur."""
+    if str(c["kind"]) != "map-ur":
+        return TOL
+    n = c["pilots"].shape[1]
+    f = c["eff"]
+    eff = orc.EffPrior(np.full(n, float(c["p"])), *f[:7])
+    floor = orc.perturbation_floor("map-ur", c["pilots"], c["gains"], c["emp_cov"],
+                                   float(c["noise"]), c["received"].shape[1], steps, max_iter,
+                                   stop_tol, eff=eff)
+    return max(TOL, 10.0 * floor)
+
+
+# ---------------------------------------------------------------------------
+# components
+# ---------------------------------------------------------------------------
+
+def test_components_match_reference(cuda_device, golden_components):
+    pkg, *_ = _pkg()
+    g = golden_components
+    for j in range(int(g["n_comp"])):
+        p = f"comp{j}_"
+        s, emp = g[p + "pilots"], g[p + "emp"]
+        m = g[p + "y"].shape[1]
+        assert max_rel(pkg.empirical_cov(g[p + "y"], m), emp) <= 1e-13
+        sigma = pkg.cov_unknown(s, g[p + "gamma"], float(g[p + "noise"]))
+        assert max_rel(sigma, g[p + "sigma"]) <= 1e-13
+        inv = pkg.frobenius_inverse(g[p + "sigma"])
+        assert max_rel(inv, g[p + "inv"]) <= 1e-10
+        assert np.array_equal(inv, inv.conj().T)            # exactly Hermitian
+        q, r = pkg.quad_forms(s, g[p + "inv"], emp)
+        assert max_rel(q, g[p + "q"]) <= 1e-11 and max_rel(r, g[p + "r"]) <= 1e-11
+        obj = pkg.eval_objective(g[p + "sigma"], g[p + "inv"], emp)
+        assert obj == pytest.approx(float(g[p + "obj"]), rel=1e-11)
+
+
+def test_cov_known_equals_unknown_bitwise(cuda_device):
+    # test_covlinalg.py:40-46
+    pkg, *_ = _pkg()
+    rng = np.random.default_rng(3)
+    s = (rng.standard_normal((8, 30)) + 1j * rng.standard_normal((8, 30))) / np.sqrt(2)
+    g = rng.uniform(0.1, 2.0, 30)
+    alpha = (rng.random(30) < 0.3).astype(float)
+    a = pkg.cov_known(s, alpha, g, 0.9)
+    b = pkg.cov_unknown(s, alpha * g, 0.9)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_inverse_known_answers(cuda_device):
+    pkg, *_ = _pkg()
+    inv = pkg.frobenius_inverse(2.5 * np.eye(5, dtype=complex))
+    np.testing.assert_allclose(inv, np.eye(5) / 2.5, atol=1e-14)
+    assert np.all(inv.imag == 0.0)
+    with pytest.raises(pkg.ConditioningError) as err:
+        pkg.frobenius_inverse(np.diag([1.0, 1.0, 0.0]).astype(complex))
+    assert err.value.cond_estimate > 1e12
+    rng = np.random.default_rng(1234)
+    b = rng.standard_normal((64, 64)) + 1j * rng.standard_normal((64, 64))
+    sigma = b @ b.conj().T / 64
+    sigma = (sigma + sigma.conj().T) / 2 + 0.01 * np.eye(64)
+    inv = pkg.frobenius_inverse(sigma)
+    assert np.linalg.norm(sigma @ inv - np.eye(64)) <= 1e-8 * 64
+
+
+def test_quad_forms_noise_floor_and_telescoping(cuda_device):
+    pkg, *_ = _pkg()
+    rng = np.random.default_rng(9)
+    s = (rng.standard_normal((8, 25)) + 1j * rng.standard_normal((8, 25))) / np.sqrt(2)
+    s = s * (np.sqrt(8) / np.linalg.norm(s, axis=0))
+    q, r = pkg.quad_forms(s, np.eye(8, dtype=complex) / 0.25, np.zeros((8, 8), dtype=complex))
+    np.testing.assert_allclose(q, 8 / 0.25, rtol=1e-12)
+    np.testing.assert_allclose(r, 0.0, atol=1e-14)
+    gamma = rng.uniform(0, 1, 25)
+    sigma = pkg.cov_unknown(s, gamma, 1.0)
+    q, r = pkg.quad_forms(s, pkg.frobenius_inverse(sigma), sigma)
+    np.testing.assert_allclose(q, r, rtol=1e-9, atol=1e-11)
+
+
+# ---------------------------------------------------------------------------
+# psca_run / forward vs the reference traces
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("i", range(32))
+def test_psca_run_matches_reference(cuda_device, golden_small, i):
+    _, est, _, _ = _pkg()
+    c = case(golden_small, i)
+    tr = est.psca_run(_problem(c), _sample(c), est.StepSchedule.default(),
+                      max_iter=int(c["max_iter"]), tol=0.0, record_objective=True)
+    tol = _tol(c, orc.default_steps(int(c["max_iter"])), int(c["max_iter"]))
+    assert ("abort" in tr.meta) == bool(c["abort"])
+    assert tr.n_iterations == len(c["update_norm"])
+    assert max_rel(tr.final, c["final"]) <= tol
+    assert max_rel(np.array(tr.iterates), c["iterates"]) <= tol
+    assert max_rel(tr.update_norm, c["update_norm"]) <= 1e-8
+    assert max_rel(tr.objective, c["objective"]) <= 1e-10
+    lo, hi = est.bounds_for(_problem(c))
+    assert np.all(tr.final >= lo) and np.all(tr.final <= hi)
+
+
+@pytest.mark.parametrize("i", range(0, 32, 3))
+def test_polynomial_schedule_and_tolerance_stop(cuda_device, golden_small, i):
+    _, est, _, _ = _pkg()
+    c = case(golden_small, i)
+    tr = est.psca_run(_problem(c), _sample(c), est.StepSchedule.polynomial(), max_iter=60,
+                      tol=1e-4, record_objective=False)
+    assert tr.n_iterations == len(c["poly_update_norm"])
+    assert max_rel(tr.final, c["poly_final"]) <= _tol(c, orc.polynomial_steps(60), 60, 1e-4)
+
+
+@pytest.mark.parametrize("i", range(1, 32, 4))
+def test_net_forward_matches_reference(cuda_device, golden_small, i):
+    _, est, _, unroll = _pkg()
+    c = case(golden_small, i)
+    net = unroll.UnrolledConfig(_problem(c), c["net_steps"])
+    out = unroll.forward(net, _sample(c))
+    assert max_rel(out, c["net_out"]) <= _tol(c, c["net_steps"], len(c["net_steps"]))
+    # forward is psca_run truncated, bit for bit (test_unroll.py:51-59)
+    tr = est.psca_run(_problem(c), _sample(c), est.StepSchedule.explicit(c["net_steps"]),
+                      max_iter=len(c["net_steps"]), tol=0.0)
+    np.testing.assert_array_equal(out, tr.final)
+
+
+def test_batch_equals_single_and_is_deterministic(cuda_device, golden_small):
+    """The batched entry gives the single-instance results bit for bit, twice."""
+    _, est, _, _ = _pkg()
+    idx = [0, 4, 8]   # same kind (ml-k), different shapes -> run one batch per shape
+    for i in idx:
+        c = case(golden_small, i)
+        single = est.psca_run(_problem(c), _sample(c), max_iter=20, tol=0.0,
+                              record_objective=False).final
+        b = 3
+        kw = dict(pilots=np.stack([c["pilots"]] * b), emp_cov=np.stack([c["emp_cov"]] * b),
+                  noise=np.full(b, float(c["noise"])), n_antennas=c["received"].shape[1],
+                  gains=np.stack([c["gains"]] * b), max_iter=20)
+        r1 = est.psca_run_batch(_problem(c), **kw)["x"].cpu().numpy()
+        r2 = est.psca_run_batch(_problem(c), n_chunks=1, **kw)["x"].cpu().numpy()
+        for k in range(b):
+            assert max_rel(r1[k], single) <= 1e-13
+            np.testing.assert_array_equal(r1[k], r1[0])
+            assert max_rel(r2[k], single) <= 1e-13
