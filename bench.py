@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 PSCA hot path (driver contract).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+PSCA-MLE with unknown pathloss (ml-ud), N=1000 devices, L=40, M=128, K=50
+active, T=100 iterations from gamma=0 with the default step rule, a batch of
+4096 independent instances per GPU (weak scaling: rank r solves instances
+r*4096 .. r*4096+4095; no collective on the data path).  One "step" = one
+batched solve of the whole batch.
+
+  value  instances/s over all ranks, inputs resident in HBM, device-timed
+         (CUDA events, barrier + synchronize on both sides, max over ranks)
+  e2e    the same through the public API (psca_run_batch) from pinned HOST
+         buffers: H2D of the step's pilots / Sigma_hat / noise and D2H of the
+         estimates inside the timed region
+  roofline  column_kernel (the dominant kernel): algorithmic FP64 flops per
+         launch (24 N L^2 per instance-iteration) / its mean
+         CUDA-event duration, against the FP64 peak measured live (cuBLAS DGEMM)
+  cpu_baseline  the CPU oracle (numpy/OpenBLAS restatement of the reference)
+         on this host's cores, one process per core, bounded sample
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port; the reference is pure Python and cannot travel to the box) on
+the same workload with all host cores and prints the same JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import statistics
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "detection instances/sec and PSCA iters/sec at N=1000,L=40,M=128; % of roofline"
+UNIT = "instances/s"
+CONFIG_NAME = "c1"
+ALGO_FLOPS_PER_UNIT = "24*N*L^2 FP64 flops per instance-iteration (SURVEY.md 8(d))"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=0, help="instances per GPU (default: config)")
+    ap.add_argument("--iters", type=int, default=0, help="PSCA iterations (default: config)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="CPU-baseline sample budget (seconds of solve time per worker)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+
+def _gen_chunk(args):
+    name, ids = args
+    from paper_2503_15259_b200 import scenes
+    cfg = scenes.BASELINE_CONFIGS[name]
+    samples = [scenes.make_scene(cfg, i) for i in ids]
+    return scenes.stack_batch(samples)
+
+
+def generate(name: str, ids: list[int], workers: int):
+    """Seeded scenes for instance ids (parallel over host processes)."""
+    import multiprocessing as mp
+    import numpy as np
+    chunks = [ids[i:i + 64] for i in range(0, len(ids), 64)]
+    if workers > 1 and len(chunks) > 1:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(min(workers, len(chunks))) as pool:
+            parts = pool.map(_gen_chunk, [(name, c) for c in chunks])
+    else:
+        parts = [_gen_chunk((name, c)) for c in chunks]
+    out = {k: np.concatenate([p[k] for p in parts]) for k in ("pilots", "gains", "emp_cov",
+                                                              "noise", "activities")}
+    out["n_antennas"] = parts[0]["n_antennas"]
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle, one process per core, OPENBLAS_NUM_THREADS=1)
+# ---------------------------------------------------------------------------
+
+def _cpu_worker(args):
+    wid, nworkers, budget_s, name, iters, per_step = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import numpy as np
+    from oracle import psca_oracle as orc
+    from paper_2503_15259_b200 import scenes
+    cfg = scenes.BASELINE_CONFIGS[name]
+    steps = orc.default_steps(iters)
+    done, solve_s = 0, 0.0
+    i = wid
+    while (per_step and done < per_step) or (not per_step and solve_s < budget_s):
+        s = scenes.make_scene(cfg, 10_000_000 + i)
+        t0 = time.perf_counter()
+        orc.psca(cfg.kind, s.pilots, s.gains, s.emp_cov, s.noise_power, s.n_antennas, steps,
+                 iters)
+        solve_s += time.perf_counter() - t0
+        done += 1
+        i += nworkers
+    return done, solve_s
+
+
+def _cpu_pool(workers):
+    import multiprocessing as mp
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    return mp.get_context("spawn").Pool(workers)
+
+
+def cpu_baseline(name: str, iters: int, budget_s: float) -> dict:
+    workers = os.cpu_count() or 1
+    with _cpu_pool(workers) as pool:
+        pool.map(_cpu_worker, [(w, workers, 0.0, name, 2, 1) for w in range(workers)])  # warm
+        res = pool.map(_cpu_worker, [(w, workers, budget_s, name, iters, 0)
+                                     for w in range(workers)])
+    n = sum(r[0] for r in res)
+    rate = sum(r[0] / r[1] for r in res if r[1] > 0)
+    return {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": f"{n} {name} instances (T={iters}) solved by the numpy/OpenBLAS oracle, "
+                      f"{workers} processes x 1 BLAS thread, ~{budget_s:.0f} s of solve time each; "
+                      "scene generation excluded"}
+
+
+# ---------------------------------------------------------------------------
+# clocks (NVML, sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+            0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                self.reasons |= int(fn(self.h))
+            except Exception:
+                pass
+            time.sleep(0.2)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in _REASONS.items() if self.reasons & b and b != 0x1],
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# FP64 peak (cuBLAS DGEMM, measured live)
+# ---------------------------------------------------------------------------
+
+def fp64_peak_tflops(torch) -> float:
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = math.inf
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def ncu_traffic(name: str = "column_kernel"):
+    """dram bytes per launch of the column kernel from the committed ncu summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        return d[name]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# arms
+# ---------------------------------------------------------------------------
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def reference_arm(args):
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return 0
+    from paper_2503_15259_b200 import scenes
+    cfg = scenes.BASELINE_CONFIGS[CONFIG_NAME]
+    iters = args.iters or cfg.n_iter
+    workers = os.cpu_count() or 1
+    with _cpu_pool(workers) as pool:
+        for _ in range(args.warmup):
+            pool.map(_cpu_worker, [(w, workers, 0, CONFIG_NAME, iters, 1) for w in range(workers)])
+        t0 = time.perf_counter()
+        n = 0
+        for _ in range(args.steps):
+            res = pool.map(_cpu_worker, [(w, workers, 0, CONFIG_NAME, iters, 1)
+                                         for w in range(workers)])
+            n += sum(r[0] for r in res)
+        wall = time.perf_counter() - t0
+    value = n / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(cfg, iters, workers, per_gpu=False),
+        "psca_iters_per_s": value * iters,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"each step: {workers} {CONFIG_NAME} instances (T={iters}), one per "
+                                   "host core, numpy/OpenBLAS oracle (restatement of the reference; "
+                                   "the reference is pure Python and cannot be installed on the box), "
+                                   "scene generation included"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg, iters, batch, per_gpu=True):
+    return {"workload": f"{CONFIG_NAME}: PSCA-MLE unknown pathloss (ml-ud), N={cfg.n_devices}, "
+                        f"L={cfg.pilot_len}, M={cfg.n_antennas}, K={cfg.n_active} active, "
+                        f"T={iters} iterations, default step rule, complex128",
+            "instances_per_gpu" if per_gpu else "instances_per_step": batch,
+            "N": cfg.n_devices, "L": cfg.pilot_len, "M": cfg.n_antennas, "T": iters,
+            "kind": cfg.kind,
+            "l2": "inputs larger than L2 (pilots 640 KB/instance, 2.6 GB per GPU vs 126 MB L2)",
+            "parallelism": "instance sharding, no collective"}
+
+
+def ours_arm(args):
+    import numpy as np
+    import torch
+    world, rank, local = dist_setup(args)
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2503_15259_b200 import device, estimators, scenes
+
+    cfg = scenes.BASELINE_CONFIGS[CONFIG_NAME]
+    B = args.batch or cfg.batch
+    iters = args.iters or cfg.n_iter
+    ids = list(range(rank * B, (rank + 1) * B))
+    host = generate(CONFIG_NAME, ids, os.cpu_count() or 1)
+    problem = scenes.problem_for(cfg)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pil_h = torch.from_numpy(host["pilots"]).pin_memory()
+    emp_h = torch.from_numpy(host["emp_cov"]).pin_memory()
+    noi_h = torch.from_numpy(host["noise"]).pin_memory()
+    pil_d, emp_d, noi_d = (t.to(dev) for t in (pil_h, emp_h, noi_h))
+    m = int(host["n_antennas"])
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {}
+    for _ in range(args.warmup):
+        out = estimators.psca_run_batch(problem, pil_d, emp_d, noi_d, m, max_iter=iters, out=out)
+    torch.cuda.synchronize()
+    peak = fp64_peak_tflops(torch)
+
+    # ---- device-resident timed region -------------------------------------
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    device.profile_begin()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            out = estimators.psca_run_batch(problem, pil_d, emp_d, noi_d, m, max_iter=iters,
+                                            out=out)
+            launches += out["launches"]
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    prof = device.profile_end()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    value = world * B * args.steps / (ms * 1e-3)
+    col_ms = prof["column_ms"] / max(prof["column_launches"], 1)
+    flops_launch = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * B
+    achieved = flops_launch / (col_ms * 1e-3) / 1e12
+    x_check = out["x"]
+    finite = bool(torch.isfinite(x_check).all().item())
+
+    # ---- end to end through the public API from pinned host buffers ----------
+    e2e = None
+    if not args.no_e2e:
+        x_h = torch.empty((B, cfg.n_devices), dtype=torch.float64).pin_memory()
+        h2d = pil_h.numel() * 16 + emp_h.numel() * 16 + noi_h.numel() * 8
+        d2h = x_h.numel() * 8
+        out2 = {}
+        p2, em2, n2 = (torch.empty_like(t) for t in (pil_d, emp_d, noi_d))
+
+        def e2e_step():
+            nonlocal out2
+            p2.copy_(pil_h, non_blocking=True)
+            em2.copy_(emp_h, non_blocking=True)
+            n2.copy_(noi_h, non_blocking=True)
+            out2 = estimators.psca_run_batch(problem, p2, em2, n2, m, max_iter=iters, out=out2)
+            x_h.copy_(out2["x"], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": world * B * args.steps / (ems * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": ems / args.steps}
+        del p2, em2, n2
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(CONFIG_NAME, iters, args.cpu_seconds)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE c1 scenes, paper_2503_15259_b200/scenes.py)",
+            "config": config_block(cfg, iters, B),
+            "psca_iters_per_s": value * iters,
+            "roofline": {
+                "bound": "tensor", "kernel": "column_kernel", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": ncu_traffic(),
+                "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured live in this run "
+                               "(MEASURED_PEAKS.json has no FP64 entry)",
+                "algorithmic_flops_per_launch": flops_launch,
+                "flops_per_unit": ALGO_FLOPS_PER_UNIT,
+                "executed_flops_note": "the kernel exploits Hermitian symmetry (lower-triangle "
+                                       "quadratic forms and rebuild) and skips exactly-zero "
+                                       "weights, so it executes fewer flops than the reference's "
+                                       "three dense ZGEMMs; frac > 1 is possible",
+                "column_ms_per_launch": col_ms,
+                "factor_ms_per_launch": prof["factor_ms"] / max(prof["factor_launches"], 1),
+                "column_share": prof["column_ms"] / max(prof["column_ms"] + prof["factor_ms"], 1e-9),
+            },
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "finite": finite,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -127,6 +127,13 @@ int psca_eval_objective(const double* sigma, const double* sigma_inv, const doub
  * (reported as bench.py's gpu_launches). */
 int psca_last_launch_count(void);
 
+/* Device timing of every column / factor kernel launched by this thread
+ * between begin and end (CUDA events on the launch stream; bench.py's
+ * roofline).  end() synchronises on the recorded events. */
+int psca_profile_begin(void);
+int psca_profile_end(double* column_ms, int* column_launches, double* factor_ms,
+                     int* factor_launches);
+
 /* Library version string (host pointer). */
 const char* psca_version(void);
 

@@ -31,7 +31,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "psca.h"
 
@@ -48,6 +50,47 @@ constexpr int MAX_L_TILE = 128;    // tile path limit (SMEM: 1.5 KB per padded r
 
 thread_local int g_launches = 0;
 
+// optional per-launch device timing (psca_profile_begin/end): CUDA events
+// recorded on the launch stream around each column / factor kernel
+struct ProfRec {
+    cudaEvent_t a, b;
+    int kind;  // 0 column, 1 factor
+};
+struct Prof {
+    bool on = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    cudaEvent_t get() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+};
+thread_local Prof g_prof;
+
+struct ProfScope {
+    cudaStream_t st;
+    int kind;
+    cudaEvent_t a = nullptr;
+    ProfScope(cudaStream_t s, int k) : st(s), kind(k) {
+        if (g_prof.on) {
+            a = g_prof.get();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = g_prof.get();
+            cudaEventRecord(b, st);
+            g_prof.recs.push_back({a, b, kind});
+        }
+    }
+};
+
 // ---------------------------------------------------------------------------
 // geometry
 // ---------------------------------------------------------------------------
@@ -55,18 +98,21 @@ struct Geo {
     int L, LP, NRB, LP8, NB, NBLK;
 };
 
-__host__ __device__ inline int rebuild_block_count(int nrb) {
+__host__ __device__ constexpr int rebuild_block_count(int nrb) {
     int s = 0;
     for (int i = 0; i < nrb; ++i) s += (4 * i + 3) / 8 + 1;
     return s;
 }
 
-__host__ __device__ inline Geo make_geo(int L) {
+// nrb = 0: the natural row-block count ceil(L/4); otherwise a padded count
+// (rows L..4*nrb-1 are zero in every tile and fragment) so that L maps onto
+// one of the compiled, fully unrolled column-kernel shapes.
+__host__ __device__ inline Geo make_geo(int L, int nrb = 0) {
     Geo g;
     g.L = L;
-    g.LP = (L + 3) & ~3;     // complex rows, multiple of 4 (one 8-real-row block = 4 rows)
-    g.NRB = g.LP / 4;        // real row blocks
-    g.LP8 = (L + 7) & ~7;    // SMEM tile rows (rebuild B fragments read 8-row blocks)
+    g.NRB = nrb > 0 ? nrb : (L + 3) / 4;  // real row blocks (8 real rows = 4 complex rows)
+    g.LP = 4 * g.NRB;                     // padded complex rows
+    g.LP8 = (g.LP + 7) & ~7;              // SMEM tile rows (rebuild B fragments read 8-row blocks)
     g.NB = g.NRB * (g.NRB + 1);           // quad-form fragment blocks (lower triangle)
     g.NBLK = rebuild_block_count(g.NRB);  // rebuild C blocks (lower triangle)
     return g;
@@ -114,6 +160,19 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
     return acc;
 }
 __device__ __forceinline__ double comp(double2 v, int c) { return c ? v.y : v.x; }
+
+// lane -> packed P'/A' fragment entry (see pack_frags)
+__device__ __forceinline__ int frag_lane_offset(int lane) {
+    const int r8 = lane >> 2, c4 = lane & 3;
+    return 2 * (2 * (r8 >> 1) + (c4 >> 1)) + ((r8 & 1) ^ (c4 & 1));
+}
+__device__ __forceinline__ unsigned long long frag_lane_sign(int lane) {
+    const int r8 = lane >> 2, c4 = lane & 3;
+    return ((r8 & 1) == 0 && (c4 & 1) == 1) ? 0x8000000000000000ull : 0ull;
+}
+__device__ __forceinline__ double xsign(double v, unsigned long long m) {
+    return __longlong_as_double(__double_as_longlong(v) ^ m);
+}
 
 // clamp with numpy semantics (NaN propagates): np.clip(v, lo, hi)
 __device__ __forceinline__ double np_clip(double v, double lo, double hi) {
@@ -171,25 +230,13 @@ __device__ void eff_density(double gm, double p, const psca_eff_prior& e, double
     }
 }
 
-__device__ double eff_grad(double gm, double p, const psca_eff_prior& e, int n_antennas) {
-    double dens, der;
-    eff_density(gm, p, e, dens, der);
-    const double mag = e.dead_zone_grad;
-    if (dens <= 1e-300) {
-        double s = (gm <= e.g_low / 2.0) ? 1.0 : -1.0;
-        return s * (mag / n_antennas);
-    }
-    double v = np_clip(der / dens, -mag, mag);
-    return -v / n_antennas;
-}
-
 // ---------------------------------------------------------------------------
 // column kernel
 // ---------------------------------------------------------------------------
 enum ColMode { COL_SOLVE = 0, COL_QUAD = 1, COL_REBUILD = 2 };
 
 struct ColArgs {
-    int kind, B, N, L, n_chunks, chunk_cols, k, T, n_antennas, record_objective;
+    int kind, B, N, L, nrb, n_chunks, chunk_cols, k, T, n_antennas, record_objective;
     const double2* pilots;      // [B][L][N]
     const double* gains;        // [B][N]
     const double* x_cur;        // [B][N]
@@ -202,6 +249,7 @@ struct ColArgs {
     const double* steps;        // [T]
     const double* prior_lin;    // [N]
     const double* prior_p;      // [N]
+    const double* pgrad;        // map-ur: [B][N] prior gradient at x_cur (factor_kernel)
     psca_eff_prior eff;
     double* q_out;              // COL_QUAD: [B][N]
     double* r_out;
@@ -220,10 +268,11 @@ __device__ __forceinline__ void load_tile(double2* buf, const double2* __restric
     cp_async_commit();
 }
 
+// Generic (runtime-shape) column kernel: any L <= MAX_L_TILE, all modes.
 template <int MAXBW, int MODE>
 __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Geo geo = make_geo(a.L);
+    const Geo geo = make_geo(a.L, a.nrb);
     const int b = blockIdx.y;
     const int chunk = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -245,7 +294,9 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
     double* wv_s = qr_s + 2 * NCT * 2;                              // [NCT]
 
     const double2* sb = a.pilots + (size_t)b * a.L * a.N;
-    const double2* fr = a.frags + (size_t)b * geo.NB * 32;
+    const double* frd = reinterpret_cast<const double*>(a.frags) + (size_t)b * geo.NB * 32;
+    const int foff = frag_lane_offset(lane);
+    const unsigned long long fsgn = frag_lane_sign(lane);
 
     // ---- static work split -------------------------------------------------
     // quad forms: warp -> (column block, row-block half); halves balanced by a
@@ -313,15 +364,16 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
             for (int i = 0; i < geo.NRB; ++i) {
                 if (!((rowmask >> i) & 1ull)) continue;
                 double tp[2] = {0.0, 0.0}, ta[2] = {0.0, 0.0};
-                const double2* f = fr + (size_t)(i * (i + 1)) * 32 + lane;
+                const double* f = frd + (size_t)(i * (i + 1)) * 32 + foff;
                 const int nk = 2 * (i + 1);
 #pragma unroll 4
                 for (int kk = 0; kk < nk; ++kk) {
-                    double2 pa = __ldg(f + kk * 32);
+                    const double pv = xsign(__ldg(f + kk * 32), fsgn);
+                    const double av = xsign(__ldg(f + kk * 32 + 16), fsgn);
                     int m = 2 * kk + (c4 >> 1);
                     double bv = Sd[2 * tile_idx(m, nb_col) + (c4 & 1)];
-                    dmma(tp, pa.x, bv);
-                    dmma(ta, pa.y, bv);
+                    dmma(tp, pv, bv);
+                    dmma(ta, av, bv);
                 }
                 // epilogue: q_n += sum_{rows} S_real * T_real  (C-fragment positions)
                 int l = 4 * i + (r8 >> 1), p = r8 & 1;
@@ -384,7 +436,7 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
                     } else if (a.kind == PSCA_ML_UD) {
                         grad = diff;
                     } else {
-                        grad = __dadd_rn(diff, eff_grad(x, a.prior_p[n], a.eff, a.n_antennas));
+                        grad = __dadd_rn(diff, a.pgrad[bN + n]);
                     }
                     const double gq = known ? __dmul_rn(g, q) : q;
                     const double coef = __dmul_rn(gq, gq);
@@ -397,15 +449,6 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
                     const double dx = __dsub_rn(xn, x);
                     p_dx2 = fma(dx, dx, p_dx2);
                     p_minq = (q < p_minq) ? q : p_minq;
-                    if (a.record_objective) {
-                        if (a.kind == PSCA_MAP_K) {
-                            p_prior = fma(a.prior_lin[n], x, p_prior);
-                        } else if (a.kind == PSCA_MAP_UR) {
-                            double dens, der;
-                            eff_density(x, a.prior_p[n], a.eff, dens, der);
-                            p_prior += log(dens > 1e-300 ? dens : 1e-300);
-                        }
-                    }
                 }
             }
             wv_s[tid] = w_new;
@@ -484,19 +527,352 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
 }
 
 // ---------------------------------------------------------------------------
+// Compiled-shape column kernel (COL_SOLVE): NRB row blocks known at compile
+// time, loops fully unrolled, every SMEM address a per-lane base plus an
+// immediate.  SMEM per CTA: S tile double buffer, WS = S diag(w_new), and the
+// instance's packed P'/A' fragments (staged once per launch).  Per 32-column
+// tile:
+//   [cp.async prefetch of tile t+1; x, g of tile t into registers]
+//   quad forms    warp -> (8-column block, row-block half); B fragments of the
+//                 column block in registers; 4 independent DMMA chains
+//   sync
+//   update + WS   warp w builds rows w, w+8, ... of WS for the 32 columns
+//                 (lane = column); the per-device update is computed in every
+//                 warp (identical arithmetic), warp 0 stores x_next
+//   sync
+//   rebuild       warp -> its lower-triangle C blocks, 4 DMMA chains each
+// ---------------------------------------------------------------------------
+template <int NRB>
+struct TG {
+    static constexpr int LP = 4 * NRB;
+    static constexpr int LP8 = (LP + 7) & ~7;
+    static constexpr int NB = NRB * (NRB + 1);
+    static constexpr int NBLK = rebuild_block_count(NRB);
+    static constexpr int MAXBW = (NBLK + NWARP - 1) / NWARP;
+    static constexpr int RPT = LP8 / 8;            // tile rows per warp (copy / WS build)
+    static constexpr size_t S_BYTES = (size_t)LP8 * NCT * 16;
+    static constexpr size_t F_BYTES = (size_t)NB * 256;
+    static constexpr size_t SMEM = 3 * S_BYTES + F_BYTES + 2 * NCT * 2 * 8 + NWARP * 4 * 8;
+};
+
+template <int NRB>
+__global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColArgs a) {
+    using G = TG<NRB>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const size_t bN = (size_t)b * a.N;
+    const int n_begin = chunk * a.chunk_cols;
+    const int n_end = min(a.N, n_begin + a.chunk_cols);
+
+    if (a.status[b] != PSCA_RUNNING) {
+        for (int n = n_begin + tid; n < n_end; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
+        return;
+    }
+
+    double2* S0 = reinterpret_cast<double2*>(smem_raw);
+    double2* S1 = S0 + G::LP8 * NCT;
+    double2* WS = S1 + G::LP8 * NCT;
+    double* FR = reinterpret_cast<double*>(WS + G::LP8 * NCT);      // [NB][32]
+    double* qr_s = FR + G::NB * 32;                                 // [2][NCT][2]
+    double* red_s = qr_s + 2 * NCT * 2;                             // [NWARP][4]
+
+    const double2* sb = a.pilots + (size_t)b * a.L * a.N;
+
+    // ---- stage the instance's P'/A' fragments (one cp.async group) ----------
+    {
+        const double2* src = a.frags + (size_t)b * G::NB * 16;
+        double2* dst = reinterpret_cast<double2*>(FR);
+        for (int e = tid; e < G::NB * 16; e += NT) cp_async16(dst + e, src + e, 16);
+        cp_async_commit();
+    }
+
+    // ---- per-lane constants --------------------------------------------------
+    const int cp_dst = warp * NCT + (lane ^ swz(warp));   // tile copy slot (+ s*8*NCT)
+    const int cb = warp & (NCB - 1);
+    const int half = warp / NCB;
+    unsigned long long rowmask = 0ull;
+    {
+        int load0 = 0, load1 = 0;
+        for (int i = NRB - 1; i >= 0; --i) {
+            int cost = 2 * (i + 1);
+            int h = (load1 < load0) ? 1 : 0;
+            if (h) load1 += cost; else load0 += cost;
+            if (h == half) rowmask |= (1ull << i);
+        }
+    }
+    int qoff[2];   // quad B fragment, k-step parity
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+        const int cpr = c4 >> 1;
+        const int sw = (cpr << 2) | (2 * par);
+        qoff[par] = 2 * (cpr * NCT + cb * 8 + (r8 ^ sw)) + (c4 & 1);
+    }
+    int epoff[2];  // epilogue S at C-fragment positions (+ i*8*NCT)
+    {
+        const int se = swz(r8 >> 1);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            epoff[j] = 2 * ((r8 >> 1) * NCT + cb * 8 + ((2 * c4 + j) ^ se)) + (r8 & 1);
+    }
+    const int foff = frag_lane_offset(lane);
+    const unsigned long long fsgn = frag_lane_sign(lane);
+    // rebuild block slots, packed (i << 8) | j
+    int slot[G::MAXBW];
+    int nbw = 0;
+    {
+        int idx = 0;
+#pragma unroll 1
+        for (int i = 0; i < NRB; ++i) {
+            const int jmax = (4 * i + 3) / 8;
+            for (int j = 0; j <= jmax; ++j, ++idx) {
+                if ((idx % NWARP) == warp) {
+#pragma unroll
+                    for (int t = 0; t < G::MAXBW; ++t)
+                        if (t == nbw) slot[t] = (i << 8) | j;
+                    ++nbw;
+                }
+            }
+        }
+    }
+    // rebuild fragments, k-step k2 = 4 g + h:
+    //   A (WS):  l = 4i + (r8>>1), n = 2 k2 + (c4>>1), component p^q, sign p&q
+    //            n ^ swz(l) = 8 g + 2 (h ^ sa) + (c4>>1)
+    //   B (S):   m = 8j + r8,      n = 2 k2 + (c4>>1), component q
+    //            n ^ swz(m) = 8 g + 2 (h ^ sbb) + (c4>>1)
+    int wa_lane[4], b_lane[4];
+    unsigned long long wsgn;
+    {
+        const int p = r8 & 1, q = c4 & 1, cpr = c4 >> 1;
+        const int sa = swz(r8 >> 1) >> 1;
+        const int sbb = swz(r8) >> 1;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            wa_lane[h] = 4 * (h ^ sa) + 2 * cpr + (p ^ q);
+            b_lane[h] = 4 * (h ^ sbb) + 2 * cpr + q;
+        }
+        wsgn = (p & q) ? 0x8000000000000000ull : 0ull;
+    }
+    double acc[G::MAXBW][2];
+#pragma unroll
+    for (int t = 0; t < G::MAXBW; ++t) acc[t][0] = acc[t][1] = 0.0;
+
+    double p_dx2 = 0.0, p_minq = INFINITY;
+    const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
+    const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
+    const double rho = a.steps[a.k];
+    const double omr = __dsub_rn(1.0, rho);
+
+    auto issue_tile = [&](double2* buf, int col0) {
+        const int n = col0 + lane;
+        const bool colok = n < a.N;
+#pragma unroll
+        for (int s2 = 0; s2 < G::RPT; ++s2) {
+            const int m = warp + 8 * s2;
+            const bool ok = colok && (m < a.L);
+            const double2* src = ok ? (sb + (size_t)m * a.N + n) : sb;
+            cp_async16(buf + cp_dst + s2 * 8 * NCT, src, ok ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+
+    const int ntiles = (n_end - n_begin + NCT - 1) / NCT;
+    if (ntiles > 0) issue_tile(S0, n_begin);
+
+    for (int t = 0; t < ntiles; ++t) {
+        double2* S = (t & 1) ? S1 : S0;
+        const double* Sd = reinterpret_cast<const double*>(S);
+        const int col0 = n_begin + t * NCT;
+        // per-device operands of this tile (lane = column), latency hidden by the quad stage
+        const int ncol = col0 + lane;
+        const bool cvalid = ncol < n_end;
+        double x = 0.0, g = 1.0, pg = 0.0;
+        if (cvalid) {
+            x = a.x_cur[bN + ncol];
+            if (known) g = a.gains[bN + ncol];
+            if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
+            else if (a.kind == PSCA_MAP_UR) pg = a.pgrad[bN + ncol];
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        if (t + 1 < ntiles) issue_tile((t & 1) ? S0 : S1, col0 + NCT);
+
+        // ---- quadratic forms ---------------------------------------------
+        {
+            double bq[2 * NRB];
+#pragma unroll
+            for (int kk = 0; kk < 2 * NRB; ++kk) bq[kk] = Sd[qoff[kk & 1] + kk * 4 * NCT];
+            double qa0 = 0.0, qa1 = 0.0, ra0 = 0.0, ra1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < NRB; ++i) {
+                if ((rowmask >> i) & 1ull) {
+                    double t0[2] = {0.0, 0.0}, t1[2] = {0.0, 0.0};
+                    double u0[2] = {0.0, 0.0}, u1[2] = {0.0, 0.0};
+                    const double* f = FR + i * (i + 1) * 32 + foff;
+#pragma unroll
+                    for (int kk = 0; kk < 2 * (i + 1); ++kk) {
+                        const double pv = xsign(f[kk * 32], fsgn);
+                        const double av = xsign(f[kk * 32 + 16], fsgn);
+                        if (kk & 1) {
+                            dmma(t1, pv, bq[kk]);
+                            dmma(u1, av, bq[kk]);
+                        } else {
+                            dmma(t0, pv, bq[kk]);
+                            dmma(u0, av, bq[kk]);
+                        }
+                    }
+                    const double s0 = Sd[epoff[0] + i * 8 * NCT];
+                    const double s1 = Sd[epoff[1] + i * 8 * NCT];
+                    qa0 = fma(s0, t0[0] + t1[0], qa0);
+                    qa1 = fma(s1, t0[1] + t1[1], qa1);
+                    ra0 = fma(s0, u0[0] + u1[0], ra0);
+                    ra1 = fma(s1, u0[1] + u1[1], ra1);
+                }
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                qa0 += __shfl_xor_sync(0xffffffffu, qa0, o);
+                qa1 += __shfl_xor_sync(0xffffffffu, qa1, o);
+                ra0 += __shfl_xor_sync(0xffffffffu, ra0, o);
+                ra1 += __shfl_xor_sync(0xffffffffu, ra1, o);
+            }
+            if (r8 == 0) {
+                const int n0 = cb * 8 + 2 * c4;
+                double* d = qr_s + half * NCT * 2;
+                d[2 * n0] = qa0;
+                d[2 * n0 + 1] = ra0;
+                d[2 * (n0 + 1)] = qa1;
+                d[2 * (n0 + 1) + 1] = ra1;
+            }
+        }
+        __syncthreads();
+
+        // ---- update (estimators.py:272-276) + WS = S diag(w_new) -------------
+        {
+            double w_new = 0.0;
+            if (cvalid) {
+                const double q = qr_s[2 * lane] + qr_s[NCT * 2 + 2 * lane];
+                const double r = qr_s[2 * lane + 1] + qr_s[NCT * 2 + 2 * lane + 1];
+                const double diff = __dsub_rn(q, r);
+                double grad;
+                if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
+                else if (a.kind == PSCA_MAP_K) grad = __dadd_rn(__dmul_rn(g, diff), pg);
+                else if (a.kind == PSCA_ML_UD) grad = diff;
+                else grad = __dadd_rn(diff, pg);
+                const double gq = known ? __dmul_rn(g, q) : q;
+                const double coef = __dmul_rn(gq, gq);
+                const double cand = np_clip(__dsub_rn(x, __ddiv_rn(grad, coef)), 0.0, hi);
+                const double xn = __dadd_rn(__dmul_rn(omr, x), __dmul_rn(rho, cand));
+                w_new = known ? __dmul_rn(xn, g) : xn;
+                if (warp == 0) {
+                    a.x_next[bN + ncol] = xn;
+                    if (a.iterates)
+                        a.iterates[((size_t)b * (a.T + 1) + a.k + 1) * a.N + ncol] = xn;
+                    const double dx = __dsub_rn(xn, x);
+                    p_dx2 = fma(dx, dx, p_dx2);
+                    p_minq = (q < p_minq) ? q : p_minq;
+                }
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < G::RPT; ++s2) {
+                const int idx = cp_dst + s2 * 8 * NCT;     // row warp + 8 s2, column lane
+                const double2 v = S[idx];
+                WS[idx] = make_double2(w_new * v.x, w_new * v.y);
+            }
+        }
+        __syncthreads();
+
+        // ---- rebuild: Sigma_next += S diag(w) S^H (lower C blocks) ----------
+        {
+            const double* Wd = reinterpret_cast<const double*>(WS);
+#pragma unroll
+            for (int t2 = 0; t2 < G::MAXBW; ++t2) {
+                if (t2 < nbw) {
+                    const int bi = slot[t2] >> 8, bj = slot[t2] & 0xff;
+                    const int abase = 2 * (4 * bi + (r8 >> 1)) * NCT;
+                    const int bbase = 2 * (8 * bj + r8) * NCT;
+                    const double* A0 = Wd + abase + wa_lane[0];
+                    const double* A1 = Wd + abase + wa_lane[1];
+                    const double* A2 = Wd + abase + wa_lane[2];
+                    const double* A3 = Wd + abase + wa_lane[3];
+                    const double* B0 = Sd + bbase + b_lane[0];
+                    const double* B1 = Sd + bbase + b_lane[1];
+                    const double* B2 = Sd + bbase + b_lane[2];
+                    const double* B3 = Sd + bbase + b_lane[3];
+                    double e1[2] = {0.0, 0.0}, e2[2] = {0.0, 0.0}, e3[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int k2 = 0; k2 < NCT / 2; ++k2) {
+                        const int h = k2 & 3, g8 = 16 * (k2 >> 2);
+                        const double* Ap = h == 0 ? A0 : h == 1 ? A1 : h == 2 ? A2 : A3;
+                        const double* Bp = h == 0 ? B0 : h == 1 ? B1 : h == 2 ? B2 : B3;
+                        const double av = xsign(Ap[g8], wsgn);
+                        const double bv = Bp[g8];
+                        switch (h) {
+                            case 0: dmma(acc[t2], av, bv); break;
+                            case 1: dmma(e1, av, bv); break;
+                            case 2: dmma(e2, av, bv); break;
+                            default: dmma(e3, av, bv); break;
+                        }
+                    }
+                    acc[t2][0] += (e1[0] + e2[0]) + e3[0];
+                    acc[t2][1] += (e1[1] + e2[1]) + e3[1];
+                }
+            }
+        }
+    }
+
+    // ---- chunk outputs --------------------------------------------------------
+    {
+        double2* sp = a.sig_part + ((size_t)b * a.n_chunks + chunk) * G::NBLK * 32;
+        int idx = 0, t2 = 0;
+        for (int i = 0; i < NRB; ++i) {
+            const int jmax = (4 * i + 3) / 8;
+            for (int j = 0; j <= jmax; ++j, ++idx) {
+                if ((idx % NWARP) == warp) {
+#pragma unroll
+                    for (int u = 0; u < G::MAXBW; ++u)
+                        if (u == t2) sp[(size_t)idx * 32 + lane] = make_double2(acc[u][0], acc[u][1]);
+                    ++t2;
+                }
+            }
+        }
+    }
+    if (warp == 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            p_dx2 += __shfl_xor_sync(0xffffffffu, p_dx2, o);
+            const double mq = __shfl_xor_sync(0xffffffffu, p_minq, o);
+            p_minq = (mq < p_minq) ? mq : p_minq;
+        }
+        if (lane == 0) {
+            double* rp = a.red_part + ((size_t)b * a.n_chunks + chunk) * 4;
+            rp[0] = p_dx2;
+            rp[1] = p_minq;
+            rp[2] = 0.0;
+            rp[3] = 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // factor kernel
 // ---------------------------------------------------------------------------
 enum FacMode { FAC_SOLVE = 0, FAC_INVERSE = 1, FAC_PREP = 2, FAC_ASSEMBLE = 3, FAC_OBJECTIVE = 4 };
 
 struct FacArgs {
-    int B, N, L, T, n_chunks, k_new, kind, n_antennas, record_objective;
+    int B, N, L, nrb, T, n_chunks, k_new, kind, n_antennas, record_objective;
     double tol;
     const double* noise;        // [B]
     const double2* emp_cov;     // [B][L][L]
     const double2* sig_part;    // [B][chunks][NBLK][32]
     const double* red_part;     // [B][chunks][4]
     double2* frags;             // [B][NB][32]
-    double* inst;               // [B][4]: frob, logdet, trace
+    double* inst;               // [B][4]: frob, logdet, trace, prior value
+    const double* prior_lin;    // map-k [N]
+    const double* prior_p;      // map-ur [N]
+    psca_eff_prior eff;
+    double* pgrad;              // map-ur [B][N]: prior gradient at the new iterate
     int* status;
     int* n_iter;
     double* cond_est;
@@ -590,11 +966,14 @@ __device__ void gemm_EX(const double2* __restrict__ E, const double2* X, int ld,
     __syncthreads();
 }
 
-// Pack P' (from X) and A' = (P^H G) into DMMA A-fragment order: block (i,kk)
-// holds rows l = 4i..4i+3, cols m = 2kk..2kk+1; lane (r,c): row (l = 4i + r/2,
-// part p = r&1), k (m = 2kk + c/2, part q = c&1); value = the real 2x2
-// expansion [[re, -im], [im, re]] of the complex entry, off-diagonal doubled,
-// strictly upper / padded entries zero.
+// Pack P' (from X) and A' = P^H G for the quad-form DMMAs.  Fragment block
+// (i,kk) covers complex rows l = 4i..4i+3 and cols m = 2kk..2kk+1 and is stored
+// as 32 doubles: the 8 complex P' entries (e = 2*(l-4i) + (m-2kk)), then the
+// 8 complex A' entries.  Off-diagonal entries are doubled (lower-triangle
+// quadratic form), diagonal entries real, strictly upper / padded entries 0.
+// Lane (r,c) of the DMMA A fragment reads entry e = 2*(r>>1) + (c>>1),
+// component (r&1)^(c&1), negated when (r&1)==0 && (c&1)==1 -- the real 2x2
+// expansion [[re,-im],[im,re]] (see frag_lane_offset / frag_lane_sign).
 __device__ void pack_frags(const double2* X, const double2* G, int ld, int L, const Geo& geo,
                            double2* __restrict__ out) {
     double* od = reinterpret_cast<double*>(out);
@@ -617,17 +996,12 @@ __device__ void pack_frags(const double2* X, const double2* G, int ld, int L, co
                 pv.y = 0.0; av.y = 0.0;
             }
         }
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                int lane = 4 * (2 * a4 + p) + (2 * cc + q);
-                double sg = (p == 0 && q == 1) ? -1.0 : 1.0;
-                double vp = sg * comp(pv, p ^ q), va = sg * comp(av, p ^ q);
-                size_t o = ((size_t)blk * 32 + lane) * 2;
-                od[o] = vp;
-                od[o + 1] = va;
-            }
+        const int ent = a4 * 2 + cc;
+        double* o = od + (size_t)blk * 32;
+        o[2 * ent] = pv.x;
+        o[2 * ent + 1] = pv.y;
+        o[16 + 2 * ent] = av.x;
+        o[16 + 2 * ent + 1] = av.y;
     }
 }
 
@@ -684,7 +1058,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double sred[NWARP + 1];
     __shared__ int s_flag;
-    const Geo geo = make_geo(a.L);
+    const Geo geo = make_geo(a.L, a.nrb);
     const int b = blockIdx.x;
     const int tid = threadIdx.x;
     const int L = a.L;
@@ -729,12 +1103,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
             } else {
                 const double un = sqrt(dx2);
                 a.update_norm[(size_t)b * a.T + k] = un;
-                if (a.objective) {
-                    double pv = 0.0;
-                    if (a.kind == PSCA_MAP_K) pv = prior;  // prior_lin already carries -1/M
-                    else if (a.kind == PSCA_MAP_UR) pv = -prior / a.n_antennas;
-                    a.objective[(size_t)b * a.T + k] = in[1] + in[2] + pv;
-                }
+                if (a.objective) a.objective[(size_t)b * a.T + k] = in[1] + in[2] + in[3];
                 a.n_iter[b] = k + 1;
                 if (un < a.tol) {
                     flag = PSCA_CONVERGED;
@@ -750,6 +1119,37 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
             return;
         }
         if (s_flag != 0 || a.k_new >= a.T) return;
+    }
+
+    // ---- prior terms at the new iterate x_{k_new} (priors.py:145-159, 370-399)
+    double prior_value = 0.0;
+    if (MODE == FAC_SOLVE &&
+        (a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.record_objective))) {
+        const size_t bN = (size_t)b * a.N;
+        const double* xv = (a.k_new == 0 ? a.x_cur : a.x_next) + bN;
+        double acc = 0.0;
+        for (int n = tid; n < a.N; n += NT) {
+            const double x = xv[n];
+            if (a.kind == PSCA_MAP_UR) {
+                double dens, der;
+                eff_density(x, a.prior_p[n], a.eff, dens, der);
+                const double mag = a.eff.dead_zone_grad;
+                double gr;
+                if (dens <= 1e-300) {
+                    gr = ((x <= a.eff.g_low / 2.0) ? 1.0 : -1.0) * (mag / a.n_antennas);
+                } else {
+                    gr = -np_clip(der / dens, -mag, mag) / a.n_antennas;
+                }
+                a.pgrad[bN + n] = gr;
+                if (a.record_objective) acc += log(dens > 1e-300 ? dens : 1e-300);
+            } else {
+                acc = fma(a.prior_lin[n], x, acc);
+            }
+        }
+        if (a.record_objective) {
+            acc = block_sum(acc, sred);
+            prior_value = (a.kind == PSCA_MAP_K) ? acc : -acc / a.n_antennas;
+        }
     }
 
     // ---- the matrix to work on ---------------------------------------------
@@ -842,6 +1242,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
             in[0] = frob;
             in[1] = logdet;
             in[2] = trace;
+            in[3] = prior_value;
         }
     }
 
@@ -850,7 +1251,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
     // FAC_PREP (quad_forms drop-in, P given by the caller): A' = P^H E P is
     // packed from the raw P; the P' half is then replaced by (P + P^H)/2,
     // which leaves q = Re s^H P s unchanged for any P.
-    pack_frags(X, G, ld, L, geo, a.frags + (size_t)b * geo.NB * 32);
+    pack_frags(X, G, ld, L, geo, a.frags + (size_t)b * geo.NB * 16);
     if (MODE == FAC_PREP) {
         __syncthreads();
         // overwrite the P' halves with the symmetrised P (exact for q)
@@ -862,7 +1263,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
             }
         }
         __syncthreads();
-        double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 32);
+        double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 16);
         const int total = geo.NB * 8;
         for (int e = tid; e < total; e += NT) {
             int blk = e >> 3, a4 = (e >> 1) & 3, cc = e & 1;
@@ -878,12 +1279,9 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
             } else if (l < L && m == l) {
                 pv = make_double2(X[l * ld + l].x, 0.0);
             }
-            for (int p = 0; p < 2; ++p)
-                for (int q = 0; q < 2; ++q) {
-                    int lane = 4 * (2 * a4 + p) + (2 * cc + q);
-                    double sg = (p == 0 && q == 1) ? -1.0 : 1.0;
-                    od[((size_t)blk * 32 + lane) * 2] = sg * comp(pv, p ^ q);
-                }
+            const int ent = a4 * 2 + cc;
+            od[(size_t)blk * 32 + 2 * ent] = pv.x;
+            od[(size_t)blk * 32 + 2 * ent + 1] = pv.y;
         }
     }
 }
@@ -970,12 +1368,48 @@ int auto_chunks(int B, int N) {
     return fit_chunks((target + B - 1) / (B > 0 ? B : 1), N);
 }
 
+// Row-block counts with a compiled, fully unrolled column kernel (L <= 80).
+// Other L are padded up to the next one; L > 80 uses the generic kernel.
+constexpr int kCompiledNrb[] = {2, 3, 4, 5, 6, 8, 10, 12, 16, 20};
+
+bool generic_forced() {
+    static const bool forced = [] {
+        const char* e = getenv("PSCA_GENERIC_COLUMN");
+        return e && e[0] == '1';
+    }();
+    return forced;
+}
+
+int solve_nrb(int L) {
+    const int nat = (L + 3) / 4;
+    if (generic_forced()) return nat;
+    for (int c : kCompiledNrb)
+        if (c >= nat) return c;
+    return nat;
+}
+
+template <int NRB>
+cudaError_t launch_column_t(const ColArgs& ca, int n_chunks, cudaStream_t st) {
+    auto kfn = column_kernel_t<NRB>;
+    const size_t sm = TG<NRB>::SMEM;
+    cudaError_t err =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (err != cudaSuccess) return err;
+    ProfScope prof(st, 0);
+    kfn<<<dim3(n_chunks, ca.B), NT, sm, st>>>(ca);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStream_t st);
+
 template <int MODE>
 cudaError_t launch_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStream_t st) {
     const int mbw = maxbw_for(g.NBLK);
     dim3 grid(n_chunks, ca.B);
     size_t sm = col_smem_bytes(g);
     cudaError_t err = cudaSuccess;
+    ProfScope prof(st, 0);
 #define PSCA_LAUNCH_COL(MB)                                                            \
     {                                                                                  \
         auto kfn = column_kernel<MB, MODE>;                                            \
@@ -996,6 +1430,25 @@ cudaError_t launch_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStr
     return cudaGetLastError();
 }
 
+cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStream_t st) {
+    if (!generic_forced()) {
+        switch (g.NRB) {
+            case 2: return launch_column_t<2>(ca, n_chunks, st);
+            case 3: return launch_column_t<3>(ca, n_chunks, st);
+            case 4: return launch_column_t<4>(ca, n_chunks, st);
+            case 5: return launch_column_t<5>(ca, n_chunks, st);
+            case 6: return launch_column_t<6>(ca, n_chunks, st);
+            case 8: return launch_column_t<8>(ca, n_chunks, st);
+            case 10: return launch_column_t<10>(ca, n_chunks, st);
+            case 12: return launch_column_t<12>(ca, n_chunks, st);
+            case 16: return launch_column_t<16>(ca, n_chunks, st);
+            case 20: return launch_column_t<20>(ca, n_chunks, st);
+            default: break;
+        }
+    }
+    return launch_column<COL_SOLVE>(ca, g, n_chunks, st);
+}
+
 template <int MODE>
 cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     size_t sm = fac_smem_bytes(g);
@@ -1003,6 +1456,7 @@ cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
+    ProfScope prof(st, 1);
     kfn<<<fa.B, NT, sm, st>>>(fa);
     ++g_launches;
     return cudaGetLastError();
@@ -1014,6 +1468,7 @@ struct SolveLayout {
     double* red_part;
     double* x_alt;
     double* inst;
+    double* pgrad;
     double2* scratch;
     size_t total;
 };
@@ -1021,11 +1476,12 @@ struct SolveLayout {
 SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, void* ws) {
     Carve cv{static_cast<char*>(ws)};
     SolveLayout s;
-    s.frags = cv.take<double2>((size_t)a->B * g.NB * 32 * 16);
+    s.frags = cv.take<double2>((size_t)a->B * g.NB * 256);
     s.sig_part = cv.take<double2>((size_t)a->B * n_chunks * g.NBLK * 32 * 16);
     s.red_part = cv.take<double>((size_t)a->B * n_chunks * 4 * 8);
     s.x_alt = cv.take<double>((size_t)a->B * a->N * 8);
     s.inst = cv.take<double>((size_t)a->B * 4 * 8);
+    s.pgrad = cv.take<double>(a->kind == PSCA_MAP_UR ? (size_t)a->B * a->N * 8 : 0);
     s.scratch = cv.take<double2>(fac_scratch_bytes(g, a->B));
     s.total = cv.off;
     return s;
@@ -1060,9 +1516,36 @@ const char* psca_version(void) { return PSCA_VERSION_STR; }
 
 int psca_last_launch_count(void) { return g_launches; }
 
+int psca_profile_begin(void) {
+    g_prof.on = true;
+    g_prof.recs.clear();
+    g_prof.used = 0;
+    return PSCA_OK;
+}
+
+int psca_profile_end(double* column_ms, int* column_launches, double* factor_ms,
+                     int* factor_launches) {
+    double cms = 0.0, fms = 0.0;
+    int cn = 0, fn = 0;
+    for (const ProfRec& r : g_prof.recs) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return PSCA_E_CUDA;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) return PSCA_E_CUDA;
+        if (r.kind == 0) { cms += ms; ++cn; } else { fms += ms; ++fn; }
+    }
+    g_prof.on = false;
+    g_prof.recs.clear();
+    g_prof.used = 0;
+    if (column_ms) *column_ms = cms;
+    if (column_launches) *column_launches = cn;
+    if (factor_ms) *factor_ms = fms;
+    if (factor_launches) *factor_launches = fn;
+    return PSCA_OK;
+}
+
 size_t psca_solve_workspace_bytes(const psca_solve_args* a) {
     if (check_solve_args(a) != PSCA_OK) return 0;
-    Geo g = make_geo(a->L);
+    Geo g = make_geo(a->L, solve_nrb(a->L));
     return solve_layout(a, g, resolved_chunks(a), nullptr).total;
 }
 
@@ -1071,7 +1554,7 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     if (rc != PSCA_OK) return rc;
     g_launches = 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const Geo g = make_geo(a->L);
+    const Geo g = make_geo(a->L, solve_nrb(a->L));
     const int n_chunks = resolved_chunks(a);
     SolveLayout lay = solve_layout(a, g, n_chunks, workspace);
     if (workspace_bytes < lay.total || (!workspace && lay.total)) return PSCA_E_WORKSPACE;
@@ -1088,7 +1571,8 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     if (a->objective) cudaMemsetAsync(a->objective, 0, (size_t)a->B * a->max_iter * 8, st);
 
     ColArgs ca{};
-    ca.kind = a->kind; ca.B = a->B; ca.N = a->N; ca.L = a->L; ca.n_chunks = n_chunks;
+    ca.kind = a->kind; ca.B = a->B; ca.N = a->N; ca.L = a->L; ca.nrb = g.NRB;
+    ca.n_chunks = n_chunks;
     {
         int tiles = (a->N + NCT - 1) / NCT;
         ca.chunk_cols = ((tiles + n_chunks - 1) / n_chunks) * NCT;
@@ -1099,9 +1583,12 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     ca.gains = a->gains; ca.iterates = a->iterates; ca.frags = lay.frags;
     ca.sig_part = lay.sig_part; ca.red_part = lay.red_part; ca.status = a->status;
     ca.steps = a->steps; ca.prior_lin = a->prior_lin; ca.prior_p = a->prior_p; ca.eff = a->eff;
+    ca.pgrad = lay.pgrad;
 
     FacArgs fa{};
-    fa.B = a->B; fa.N = a->N; fa.L = a->L; fa.T = a->max_iter; fa.n_chunks = n_chunks;
+    fa.B = a->B; fa.N = a->N; fa.L = a->L; fa.nrb = g.NRB; fa.T = a->max_iter;
+    fa.n_chunks = n_chunks;
+    fa.prior_lin = a->prior_lin; fa.prior_p = a->prior_p; fa.eff = a->eff; fa.pgrad = lay.pgrad;
     fa.kind = a->kind; fa.n_antennas = a->n_antennas;
     fa.record_objective = ca.record_objective; fa.tol = a->tol;
     fa.noise = a->noise; fa.emp_cov = reinterpret_cast<const double2*>(a->emp_cov);
@@ -1116,7 +1603,7 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     if (launch_factor<FAC_SOLVE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
     for (int k = 0; k < a->max_iter; ++k) {
         ca.k = k; ca.x_cur = xc; ca.x_next = xn;
-        if (launch_column<COL_SOLVE>(ca, g, n_chunks, st) != cudaSuccess) return PSCA_E_CUDA;
+        if (launch_solve_column(ca, g, n_chunks, st) != cudaSuccess) return PSCA_E_CUDA;
         fa.k_new = k + 1; fa.x_cur = xc; fa.x_next = xn;
         if (launch_factor<FAC_SOLVE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
         double* t = xc; xc = xn; xn = t;
@@ -1168,14 +1655,15 @@ int psca_cov_unknown(const double* pilots, const double* w, const double* noise,
     double* red_part = cv.take<double>((size_t)B * nc * 4 * 8);
     double2* scratch = cv.take<double2>(fac_scratch_bytes(g, B));
     ColArgs ca{};
-    ca.kind = PSCA_ML_UD; ca.B = B; ca.N = N; ca.L = L; ca.n_chunks = nc;
+    ca.kind = PSCA_ML_UD; ca.B = B; ca.N = N; ca.L = L; ca.nrb = g.NRB; ca.n_chunks = nc;
     int tiles = (N + NCT - 1) / NCT;
     ca.chunk_cols = ((tiles + nc - 1) / nc) * NCT;
     ca.pilots = reinterpret_cast<const double2*>(pilots);
     ca.sig_part = sig_part; ca.red_part = red_part; ca.w_in = w;
     if (launch_column<COL_REBUILD>(ca, g, nc, st) != cudaSuccess) return PSCA_E_CUDA;
     FacArgs fa{};
-    fa.B = B; fa.N = N; fa.L = L; fa.n_chunks = nc; fa.noise = noise; fa.sig_part = sig_part;
+    fa.B = B; fa.N = N; fa.L = L; fa.nrb = g.NRB; fa.n_chunks = nc; fa.noise = noise;
+    fa.sig_part = sig_part;
     fa.scratch = scratch; fa.out_mat = reinterpret_cast<double2*>(out);
     if (launch_factor<FAC_ASSEMBLE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
     return PSCA_OK;
@@ -1195,7 +1683,7 @@ int psca_hpd_inverse(const double* sigma, int B, int L, double* out, int* status
     g_launches = 0;
     Geo g = make_geo(L);
     FacArgs fa{};
-    fa.B = B; fa.L = L; fa.in_mat = reinterpret_cast<const double2*>(sigma);
+    fa.B = B; fa.L = L; fa.nrb = g.NRB; fa.in_mat = reinterpret_cast<const double2*>(sigma);
     fa.out_mat = reinterpret_cast<double2*>(out); fa.status = status; fa.cond_est = cond_est;
     fa.out_vec = logdet; fa.scratch = static_cast<double2*>(workspace);
     if (launch_factor<FAC_INVERSE>(fa, g, static_cast<cudaStream_t>(stream)) != cudaSuccess)
@@ -1207,7 +1695,7 @@ size_t psca_quad_workspace_bytes(int B, int N, int L) {
     if (B < 0 || N < 1 || L < 1 || L > MAX_L_TILE) return 0;
     Geo g = make_geo(L);
     Carve cv{nullptr};
-    cv.take<double2>((size_t)B * g.NB * 32 * 16);
+    cv.take<double2>((size_t)B * g.NB * 256);
     cv.take<double2>(fac_scratch_bytes(g, B));
     return cv.off;
 }
@@ -1224,16 +1712,16 @@ int psca_quad_forms(const double* pilots, const double* sigma_inv, const double*
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Geo g = make_geo(L);
     Carve cv{static_cast<char*>(workspace)};
-    double2* frags = cv.take<double2>((size_t)B * g.NB * 32 * 16);
+    double2* frags = cv.take<double2>((size_t)B * g.NB * 256);
     double2* scratch = cv.take<double2>(fac_scratch_bytes(g, B));
     FacArgs fa{};
-    fa.B = B; fa.L = L; fa.in_mat = reinterpret_cast<const double2*>(sigma_inv);
+    fa.B = B; fa.L = L; fa.nrb = g.NRB; fa.in_mat = reinterpret_cast<const double2*>(sigma_inv);
     fa.emp_cov = reinterpret_cast<const double2*>(emp_cov); fa.frags = frags;
     fa.scratch = scratch;
     if (launch_factor<FAC_PREP>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
     int nc = auto_chunks(B, N);
     ColArgs ca{};
-    ca.kind = PSCA_ML_UD; ca.B = B; ca.N = N; ca.L = L; ca.n_chunks = nc;
+    ca.kind = PSCA_ML_UD; ca.B = B; ca.N = N; ca.L = L; ca.nrb = g.NRB; ca.n_chunks = nc;
     int tiles = (N + NCT - 1) / NCT;
     ca.chunk_cols = ((tiles + nc - 1) / nc) * NCT;
     ca.pilots = reinterpret_cast<const double2*>(pilots);
@@ -1253,7 +1741,7 @@ int psca_eval_objective(const double* sigma, const double* sigma_inv, const doub
     g_launches = 0;
     Geo g = make_geo(L);
     FacArgs fa{};
-    fa.B = B; fa.L = L; fa.in_mat = reinterpret_cast<const double2*>(sigma);
+    fa.B = B; fa.L = L; fa.nrb = g.NRB; fa.in_mat = reinterpret_cast<const double2*>(sigma);
     fa.in_mat2 = reinterpret_cast<const double2*>(sigma_inv);
     fa.emp_cov = reinterpret_cast<const double2*>(emp_cov);
     fa.out_vec = out; fa.status = status; fa.scratch = static_cast<double2*>(workspace);

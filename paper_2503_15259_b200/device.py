@@ -52,6 +52,9 @@ class SolveArgsC(ctypes.Structure):
 _SIGS = {
     "psca_version": (ctypes.c_char_p, []),
     "psca_last_launch_count": (ctypes.c_int, []),
+    "psca_profile_begin": (ctypes.c_int, []),
+    "psca_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "psca_solve_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(SolveArgsC)]),
     "psca_solve": (ctypes.c_int, [ctypes.POINTER(SolveArgsC), ctypes.c_void_p, ctypes.c_size_t,
                                   ctypes.c_void_p]),
@@ -313,6 +316,21 @@ def eval_objective(sigma, sigma_inv, emp_cov):
            "psca_eval_objective")
     v, s = out.cpu().numpy(), status.cpu().numpy()
     return (v[0], s[0]) if single else (v, s)
+
+
+def profile_begin():
+    """Start per-kernel CUDA-event timing of subsequent solves on this thread."""
+    _check(load().psca_profile_begin(), "psca_profile_begin")
+
+
+def profile_end() -> dict:
+    """Stop timing; returns summed device ms and launch counts per kernel family."""
+    cms, fms = ctypes.c_double(), ctypes.c_double()
+    cn, fn = ctypes.c_int(), ctypes.c_int()
+    _check(load().psca_profile_end(ctypes.byref(cms), ctypes.byref(cn), ctypes.byref(fms),
+                                   ctypes.byref(fn)), "psca_profile_end")
+    return {"column_ms": cms.value, "column_launches": cn.value, "factor_ms": fms.value,
+            "factor_launches": fn.value}
 
 
 def version() -> str:
