@@ -1053,6 +1053,85 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
     __syncthreads();
 }
 
+// Finalise iteration k = k_new - 1 of instance b (estimators.py:267-286): the
+// q-floor guard on that iteration's q (chunk minima), its update norm, the
+// objective value and the tol stop.  Returns true when the CTA must stop
+// (instance frozen or no further factorisation needed).
+__device__ bool fac_finalize(const FacArgs& a, int b, int* s_flag) {
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        const int k = a.k_new - 1;
+        double dx2 = 0.0, minq = INFINITY;
+        const double* rp = a.red_part + (size_t)b * a.n_chunks * 4;
+        for (int c = 0; c < a.n_chunks; ++c) {
+            dx2 += rp[4 * c];
+            minq = (rp[4 * c + 1] < minq) ? rp[4 * c + 1] : minq;
+        }
+        const double* in = a.inst + (size_t)b * 4;
+        const double qfloor = 0.5 * a.L / in[0];
+        int flag = 0;
+        if (minq < qfloor) {
+            flag = PSCA_QFLOOR;
+            a.status[b] = PSCA_QFLOOR;
+            a.n_iter[b] = k;
+        } else {
+            const double un = sqrt(dx2);
+            a.update_norm[(size_t)b * a.T + k] = un;
+            if (a.objective) a.objective[(size_t)b * a.T + k] = in[1] + in[2] + in[3];
+            a.n_iter[b] = k + 1;
+            if (un < a.tol) {
+                flag = PSCA_CONVERGED;
+                a.status[b] = PSCA_CONVERGED;
+            }
+        }
+        *s_flag = flag;
+    }
+    __syncthreads();
+    if (*s_flag == PSCA_QFLOOR) {
+        const size_t bN = (size_t)b * a.N;
+        for (int n = tid; n < a.N; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
+        return true;
+    }
+    return *s_flag != 0 || a.k_new >= a.T;
+}
+
+// Prior terms at the new iterate x_{k_new} (priors.py:145-159, 370-399): the
+// map-ur gradient for the next column pass (into a.pgrad) and, when the
+// objective is recorded, the prior penalty value.
+__device__ double fac_prior_terms(const FacArgs& a, int b, double* sred) {
+    const int tid = threadIdx.x;
+    double prior_value = 0.0;
+    if ((a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.record_objective))) {
+        const size_t bN = (size_t)b * a.N;
+        const double* xv = (a.k_new == 0 ? a.x_cur : a.x_next) + bN;
+        double acc = 0.0;
+        for (int n = tid; n < a.N; n += NT) {
+            const double x = xv[n];
+            if (a.kind == PSCA_MAP_UR) {
+                double dens, der;
+                eff_density(x, a.prior_p[n], a.eff, dens, der);
+                const double mag = a.eff.dead_zone_grad;
+                double gr;
+                if (dens <= 1e-300) {
+                    gr = ((x <= a.eff.g_low / 2.0) ? 1.0 : -1.0) * (mag / a.n_antennas);
+                } else {
+                    gr = -np_clip(der / dens, -mag, mag) / a.n_antennas;
+                }
+                a.pgrad[bN + n] = gr;
+                if (a.record_objective) acc += log(dens > 1e-300 ? dens : 1e-300);
+            } else {
+                acc = fma(a.prior_lin[n], x, acc);
+            }
+        }
+        if (a.record_objective) {
+            acc = block_sum(acc, sred);
+            prior_value = (a.kind == PSCA_MAP_K) ? acc : -acc / a.n_antennas;
+        }
+    }
+
+    return prior_value;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1083,74 +1162,10 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
     }
 
     if (MODE == FAC_SOLVE && a.k_new > 0) {
-        // ---- finalise iteration k = k_new - 1 -------------------------------
-        if (tid == 0) {
-            const int k = a.k_new - 1;
-            double dx2 = 0.0, minq = INFINITY, prior = 0.0;
-            const double* rp = a.red_part + (size_t)b * a.n_chunks * 4;
-            for (int c = 0; c < a.n_chunks; ++c) {
-                dx2 += rp[4 * c];
-                minq = (rp[4 * c + 1] < minq) ? rp[4 * c + 1] : minq;
-                prior += rp[4 * c + 2];
-            }
-            const double* in = a.inst + (size_t)b * 4;
-            const double qfloor = 0.5 * L / in[0];
-            int flag = 0;
-            if (minq < qfloor) {
-                flag = PSCA_QFLOOR;
-                a.status[b] = PSCA_QFLOOR;
-                a.n_iter[b] = k;
-            } else {
-                const double un = sqrt(dx2);
-                a.update_norm[(size_t)b * a.T + k] = un;
-                if (a.objective) a.objective[(size_t)b * a.T + k] = in[1] + in[2] + in[3];
-                a.n_iter[b] = k + 1;
-                if (un < a.tol) {
-                    flag = PSCA_CONVERGED;
-                    a.status[b] = PSCA_CONVERGED;
-                }
-            }
-            s_flag = flag;
-        }
-        __syncthreads();
-        if (s_flag == PSCA_QFLOOR) {
-            const size_t bN = (size_t)b * a.N;
-            for (int n = tid; n < a.N; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
-            return;
-        }
-        if (s_flag != 0 || a.k_new >= a.T) return;
+        if (fac_finalize(a, b, &s_flag)) return;
     }
-
-    // ---- prior terms at the new iterate x_{k_new} (priors.py:145-159, 370-399)
     double prior_value = 0.0;
-    if (MODE == FAC_SOLVE &&
-        (a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.record_objective))) {
-        const size_t bN = (size_t)b * a.N;
-        const double* xv = (a.k_new == 0 ? a.x_cur : a.x_next) + bN;
-        double acc = 0.0;
-        for (int n = tid; n < a.N; n += NT) {
-            const double x = xv[n];
-            if (a.kind == PSCA_MAP_UR) {
-                double dens, der;
-                eff_density(x, a.prior_p[n], a.eff, dens, der);
-                const double mag = a.eff.dead_zone_grad;
-                double gr;
-                if (dens <= 1e-300) {
-                    gr = ((x <= a.eff.g_low / 2.0) ? 1.0 : -1.0) * (mag / a.n_antennas);
-                } else {
-                    gr = -np_clip(der / dens, -mag, mag) / a.n_antennas;
-                }
-                a.pgrad[bN + n] = gr;
-                if (a.record_objective) acc += log(dens > 1e-300 ? dens : 1e-300);
-            } else {
-                acc = fma(a.prior_lin[n], x, acc);
-            }
-        }
-        if (a.record_objective) {
-            acc = block_sum(acc, sred);
-            prior_value = (a.kind == PSCA_MAP_K) ? acc : -acc / a.n_antennas;
-        }
-    }
+    if (MODE == FAC_SOLVE) prior_value = fac_prior_terms(a, b, sred);
 
     // ---- the matrix to work on ---------------------------------------------
     if (MODE == FAC_SOLVE || MODE == FAC_ASSEMBLE) {
@@ -1283,6 +1298,262 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
             od[(size_t)blk * 32 + 2 * ent] = pv.x;
             od[(size_t)blk * 32 + 2 * ent + 1] = pv.y;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Compiled-shape factor kernel (FAC_SOLVE, padded LP <= 16*RT <= 80).
+// Thread (ty, tx) = (tid/16, tid%16) owns the RT x RT entries
+// (ty + 16u, tx + 16v) of every L x L matrix.  The Gauss-Jordan sweep keeps
+// them in registers; only the pivot row / column of each step go through SMEM
+// (ping-pong staged by their owners, one barrier per pivot).  The two GEMMs of
+// A = P^H Sigma_hat P are register-tiled the same way, and each thread packs
+// the P'/A' fragment entries it owns straight into the fragment buffer.
+// ---------------------------------------------------------------------------
+template <int RT>
+__global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double sred[NWARP + 1];
+    __shared__ int s_flag;
+    const Geo geo = make_geo(a.L, a.nrb);
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int L = a.L, LP = geo.LP;
+    const int ld = LP + 1;
+    if (a.status[b] != PSCA_RUNNING) return;
+    if (a.k_new > 0) {
+        if (fac_finalize(a, b, &s_flag)) return;
+    }
+    const double prior_value = fac_prior_terms(a, b, sred);
+
+    double2* sm = reinterpret_cast<double2*>(smem_raw);
+    double2* rowb = sm;             // [2][LP]
+    double2* colb = sm + 2 * LP;    // [2][LP]
+    double2* X = sm + 4 * LP;       // [LP][ld]
+    double2* G = X + (size_t)LP * ld;
+
+    assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
+    double frob;
+    {
+        double s = 0.0;
+        for (int e = tid; e < L * L; e += NT) {
+            const int i = e / L, j = e - i * L;
+            const double2 v = X[i * ld + j];
+            s = fma(v.x, v.x, fma(v.y, v.y, s));
+        }
+        frob = sqrt(block_sum(s, sred));
+    }
+
+    const int ty = tid >> 4, tx = tid & 15;
+    double2 v[RT][RT];
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            v[u][w] = (i < L && j < L) ? X[i * ld + j] : make_double2(0.0, 0.0);
+        }
+    for (int e = tid; e < L; e += NT) {
+        rowb[e] = X[e];
+        colb[e] = X[e * ld];
+    }
+    __syncthreads();
+
+    // ---- Gauss-Jordan sweep (covlinalg.py:91-115 restated; pivots = LDL^H) ----
+    double logdet = 0.0;
+    bool ok = true;
+    for (int k = 0; k < L; ++k) {
+        const double2* rk = rowb + (k & 1) * LP;
+        const double2* ck = colb + (k & 1) * LP;
+        double2* rn = rowb + ((k + 1) & 1) * LP;
+        double2* cn = colb + ((k + 1) & 1) * LP;
+        const double piv = rk[k].x;
+        if (!(piv > 0.0)) {
+            ok = false;
+            break;
+        }
+        logdet += log(piv);
+        const double pinv = 1.0 / piv;
+        double2 cu[RT], rw[RT];
+#pragma unroll
+        for (int u = 0; u < RT; ++u) {
+            const int i = ty + 16 * u;
+            cu[u] = (i < L) ? ck[i] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int j = tx + 16 * w;
+            rw[w] = (j < L) ? rk[j] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < RT; ++u) {
+            const int i = ty + 16 * u;
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int j = tx + 16 * w;
+                if (i < L && j < L) {
+                    const double2 o = v[u][w];
+                    double2 nv;
+                    if (i == k) {
+                        nv = (j == k) ? make_double2(pinv, 0.0) : make_double2(o.x * pinv, o.y * pinv);
+                    } else if (j == k) {
+                        nv = make_double2(-o.x * pinv, -o.y * pinv);
+                    } else {
+                        const double2 pr = cmul(cu[u], rw[w]);
+                        nv = make_double2(o.x - pr.x * pinv, o.y - pr.y * pinv);
+                    }
+                    v[u][w] = nv;
+                    if (i == k + 1) rn[j] = nv;
+                    if (j == k + 1) cn[i] = nv;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (!ok) {
+        if (tid == 0) {
+            a.status[b] = PSCA_CHOL_FAIL;
+            if (a.cond_est) a.cond_est[b] = INFINITY;
+        }
+        return;
+    }
+    // ---- P = (P + P^H)/2 (covlinalg.py:107, 112-114) ---------------------------
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
+        }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            if (i < L && j < L) {
+                const double2 t = X[j * ld + i];
+                v[u][w] = (i == j) ? make_double2(v[u][w].x, 0.0)
+                                   : make_double2(0.5 * (v[u][w].x + t.x), 0.5 * (v[u][w].y - t.y));
+            }
+        }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
+        }
+    __syncthreads();
+
+    const double2* E = a.emp_cov + (size_t)b * L * L;
+    double trace = 0.0;
+    if (a.record_objective) {
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int i = ty + 16 * u, j = tx + 16 * w;
+                if (i < L && j < L) {
+                    const double2 ev = __ldg(E + (size_t)j * L + i);
+                    s = fma(v[u][w].x, ev.x, fma(-v[u][w].y, ev.y, s));
+                }
+            }
+        trace = block_sum(s, sred);
+    }
+    // ---- G = Sigma_hat P ------------------------------------------------------
+    {
+        double2 gacc[RT][RT];
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) gacc[u][w] = make_double2(0.0, 0.0);
+        for (int c = 0; c < L; ++c) {
+            double2 eu[RT], xw[RT];
+#pragma unroll
+            for (int u = 0; u < RT; ++u) {
+                const int i = ty + 16 * u;
+                eu[u] = (i < L) ? __ldg(E + (size_t)i * L + c) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int j = tx + 16 * w;
+                xw[w] = (j < LP) ? X[c * ld + j] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < RT; ++u)
+#pragma unroll
+                for (int w = 0; w < RT; ++w) gacc[u][w] = cfma(eu[u], xw[w], gacc[u][w]);
+        }
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int i = ty + 16 * u, j = tx + 16 * w;
+                if (i < LP && j < LP) G[i * ld + j] = gacc[u][w];
+            }
+    }
+    __syncthreads();
+    // ---- A = P^H G and the fragment pack ---------------------------------------
+    {
+        double2 aacc[RT][RT];
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) aacc[u][w] = make_double2(0.0, 0.0);
+        for (int t = 0; t < L; ++t) {
+            double2 pu[RT], gw[RT];
+#pragma unroll
+            for (int u = 0; u < RT; ++u) {
+                const int i = ty + 16 * u;
+                pu[u] = (i < LP) ? X[t * ld + i] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int j = tx + 16 * w;
+                gw[w] = (j < LP) ? G[t * ld + j] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < RT; ++u)
+#pragma unroll
+                for (int w = 0; w < RT; ++w) aacc[u][w] = cfma_conj_a(pu[u], gw[w], aacc[u][w]);
+        }
+        double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 16);
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int l = ty + 16 * u, m = tx + 16 * w;
+                if (l < LP && m <= 4 * (l >> 2) + 3) {
+                    double2 pv = make_double2(0.0, 0.0), av = make_double2(0.0, 0.0);
+                    if (l < L && m <= l) {
+                        pv = X[l * ld + m];
+                        av = aacc[u][w];
+                        if (m < l) {
+                            pv.x *= 2.0; pv.y *= 2.0; av.x *= 2.0; av.y *= 2.0;
+                        } else {
+                            pv.y = 0.0; av.y = 0.0;
+                        }
+                    }
+                    const int i4 = l >> 2;
+                    const int blk = i4 * (i4 + 1) + (m >> 1);
+                    const int ent = (l & 3) * 2 + (m & 1);
+                    double* o = od + (size_t)blk * 32;
+                    o[2 * ent] = pv.x;
+                    o[2 * ent + 1] = pv.y;
+                    o[16 + 2 * ent] = av.x;
+                    o[16 + 2 * ent + 1] = av.y;
+                }
+            }
+    }
+    if (tid == 0) {
+        double* in = a.inst + (size_t)b * 4;
+        in[0] = frob;
+        in[1] = logdet;
+        in[2] = trace;
+        in[3] = prior_value;
     }
 }
 
@@ -1449,6 +1720,37 @@ cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, c
     return launch_column<COL_SOLVE>(ca, g, n_chunks, st);
 }
 
+template <int RT>
+cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
+    const size_t sm = (size_t)4 * g.LP * 16 + (size_t)2 * g.LP * (g.LP + 1) * 16;
+    auto kfn = factor_solve_t<RT>;
+    cudaError_t err =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (err != cudaSuccess) return err;
+    ProfScope prof(st, 1);
+    kfn<<<fa.B, NT, sm, st>>>(fa);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st);
+
+cudaError_t launch_solve_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
+    if (!generic_forced()) {
+        const int rt = (g.LP + 15) / 16;
+        switch (rt) {
+            case 1: return launch_factor_t<1>(fa, g, st);
+            case 2: return launch_factor_t<2>(fa, g, st);
+            case 3: return launch_factor_t<3>(fa, g, st);
+            case 4: return launch_factor_t<4>(fa, g, st);
+            case 5: return launch_factor_t<5>(fa, g, st);
+            default: break;
+        }
+    }
+    return launch_factor<FAC_SOLVE>(fa, g, st);
+}
+
 template <int MODE>
 cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     size_t sm = fac_smem_bytes(g);
@@ -1600,12 +1902,12 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     double* xc = a->x_out;
     double* xn = lay.x_alt;
     fa.k_new = 0; fa.x_cur = xc; fa.x_next = xn;
-    if (launch_factor<FAC_SOLVE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+    if (launch_solve_factor(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
     for (int k = 0; k < a->max_iter; ++k) {
         ca.k = k; ca.x_cur = xc; ca.x_next = xn;
         if (launch_solve_column(ca, g, n_chunks, st) != cudaSuccess) return PSCA_E_CUDA;
         fa.k_new = k + 1; fa.x_cur = xc; fa.x_next = xn;
-        if (launch_factor<FAC_SOLVE>(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+        if (launch_solve_factor(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
         double* t = xc; xc = xn; xn = t;
     }
     if (xc != a->x_out) {

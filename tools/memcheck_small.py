@@ -1,0 +1,13 @@
+"""Small solve for compute-sanitizer (one tool per run; see B200_PROFILING.md)."""
+import sys
+sys.path.insert(0, ".")
+import __graft_entry__
+__graft_entry__.build()
+from paper_2503_15259_b200 import estimators, scenes
+for L, kind in ((40, "ml-ud"), (20, "map-ur"), (72, "map-k"), (33, "ml-k")):
+    cfg = scenes.SceneConfig(7, kind, 100, L, 64, 10, 4, 2)
+    ss = [scenes.make_scene(cfg, i) for i in range(2)]
+    b = scenes.stack_batch(ss)
+    res = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"], b["noise"],
+                                    64, gains=b["gains"], max_iter=4, record_objective=True)
+    print(L, kind, float(res["x"].sum()))
