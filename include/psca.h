@@ -127,12 +127,19 @@ int psca_eval_objective(const double* sigma, const double* sigma_inv, const doub
  * (reported as bench.py's gpu_launches). */
 int psca_last_launch_count(void);
 
+/* Execution path of the last psca_solve on this thread: 0 = two kernels per
+ * iteration (column chunks), 1 = one persistent launch for the whole solve. */
+int psca_last_path(void);
+
 /* Device timing of every column / factor kernel launched by this thread
  * between begin and end (CUDA events on the launch stream; bench.py's
  * roofline).  end() synchronises on the recorded events. */
 int psca_profile_begin(void);
 int psca_profile_end(double* column_ms, int* column_launches, double* factor_ms,
                      int* factor_launches);
+
+/* Description of the last CUDA error a call on this thread reported. */
+const char* psca_last_error(void);
 
 /* Library version string (host pointer). */
 const char* psca_version(void);

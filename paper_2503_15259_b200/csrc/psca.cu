@@ -49,6 +49,15 @@ constexpr int FAC_SMEM_MAX_LP = 80;
 constexpr int MAX_L_TILE = 128;    // tile path limit (SMEM: 1.5 KB per padded row)
 
 thread_local int g_launches = 0;
+thread_local cudaError_t g_last_err = cudaSuccess;
+
+inline bool ok_or_record(cudaError_t e) {
+    if (e != cudaSuccess) {
+        g_last_err = e;
+        return false;
+    }
+    return true;
+}
 
 // optional per-launch device timing (psca_profile_begin/end): CUDA events
 // recorded on the launch stream around each column / factor kernel
@@ -237,6 +246,7 @@ enum ColMode { COL_SOLVE = 0, COL_QUAD = 1, COL_REBUILD = 2 };
 
 struct ColArgs {
     int kind, B, N, L, nrb, n_chunks, chunk_cols, k, T, n_antennas, record_objective;
+    int incremental;            // 1: rebuild the increment S diag(rho cand g) S^H only
     const double2* pilots;      // [B][L][N]
     const double* gains;        // [B][N]
     const double* x_cur;        // [B][N]
@@ -527,342 +537,16 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
 }
 
 // ---------------------------------------------------------------------------
-// Compiled-shape column kernel (COL_SOLVE): NRB row blocks known at compile
-// time, loops fully unrolled, every SMEM address a per-lane base plus an
-// immediate.  SMEM per CTA: S tile double buffer, WS = S diag(w_new), and the
-// instance's packed P'/A' fragments (staged once per launch).  Per 32-column
-// tile:
-//   [cp.async prefetch of tile t+1; x, g of tile t into registers]
-//   quad forms    warp -> (8-column block, row-block half); B fragments of the
-//                 column block in registers; 4 independent DMMA chains
-//   sync
-//   update + WS   warp w builds rows w, w+8, ... of WS for the 32 columns
-//                 (lane = column); the per-device update is computed in every
-//                 warp (identical arithmetic), warp 0 stores x_next
-//   sync
-//   rebuild       warp -> its lower-triangle C blocks, 4 DMMA chains each
-// ---------------------------------------------------------------------------
-template <int NRB>
-struct TG {
-    static constexpr int LP = 4 * NRB;
-    static constexpr int LP8 = (LP + 7) & ~7;
-    static constexpr int NB = NRB * (NRB + 1);
-    static constexpr int NBLK = rebuild_block_count(NRB);
-    static constexpr int MAXBW = (NBLK + NWARP - 1) / NWARP;
-    static constexpr int RPT = LP8 / 8;            // tile rows per warp (copy / WS build)
-    static constexpr size_t S_BYTES = (size_t)LP8 * NCT * 16;
-    static constexpr size_t F_BYTES = (size_t)NB * 256;
-    static constexpr size_t SMEM = 3 * S_BYTES + F_BYTES + 2 * NCT * 2 * 8 + NWARP * 4 * 8;
-};
-
-template <int NRB>
-__global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColArgs a) {
-    using G = TG<NRB>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int b = blockIdx.y;
-    const int chunk = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int r8 = lane >> 2, c4 = lane & 3;
-    const size_t bN = (size_t)b * a.N;
-    const int n_begin = chunk * a.chunk_cols;
-    const int n_end = min(a.N, n_begin + a.chunk_cols);
-
-    if (a.status[b] != PSCA_RUNNING) {
-        for (int n = n_begin + tid; n < n_end; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
-        return;
-    }
-
-    double2* S0 = reinterpret_cast<double2*>(smem_raw);
-    double2* S1 = S0 + G::LP8 * NCT;
-    double2* WS = S1 + G::LP8 * NCT;
-    double* FR = reinterpret_cast<double*>(WS + G::LP8 * NCT);      // [NB][32]
-    double* qr_s = FR + G::NB * 32;                                 // [2][NCT][2]
-    double* red_s = qr_s + 2 * NCT * 2;                             // [NWARP][4]
-
-    const double2* sb = a.pilots + (size_t)b * a.L * a.N;
-
-    // ---- stage the instance's P'/A' fragments (one cp.async group) ----------
-    {
-        const double2* src = a.frags + (size_t)b * G::NB * 16;
-        double2* dst = reinterpret_cast<double2*>(FR);
-        for (int e = tid; e < G::NB * 16; e += NT) cp_async16(dst + e, src + e, 16);
-        cp_async_commit();
-    }
-
-    // ---- per-lane constants --------------------------------------------------
-    const int cp_dst = warp * NCT + (lane ^ swz(warp));   // tile copy slot (+ s*8*NCT)
-    const int cb = warp & (NCB - 1);
-    const int half = warp / NCB;
-    unsigned long long rowmask = 0ull;
-    {
-        int load0 = 0, load1 = 0;
-        for (int i = NRB - 1; i >= 0; --i) {
-            int cost = 2 * (i + 1);
-            int h = (load1 < load0) ? 1 : 0;
-            if (h) load1 += cost; else load0 += cost;
-            if (h == half) rowmask |= (1ull << i);
-        }
-    }
-    int qoff[2];   // quad B fragment, k-step parity
-#pragma unroll
-    for (int par = 0; par < 2; ++par) {
-        const int cpr = c4 >> 1;
-        const int sw = (cpr << 2) | (2 * par);
-        qoff[par] = 2 * (cpr * NCT + cb * 8 + (r8 ^ sw)) + (c4 & 1);
-    }
-    int epoff[2];  // epilogue S at C-fragment positions (+ i*8*NCT)
-    {
-        const int se = swz(r8 >> 1);
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-            epoff[j] = 2 * ((r8 >> 1) * NCT + cb * 8 + ((2 * c4 + j) ^ se)) + (r8 & 1);
-    }
-    const int foff = frag_lane_offset(lane);
-    const unsigned long long fsgn = frag_lane_sign(lane);
-    // rebuild block slots, packed (i << 8) | j
-    int slot[G::MAXBW];
-    int nbw = 0;
-    {
-        int idx = 0;
-#pragma unroll 1
-        for (int i = 0; i < NRB; ++i) {
-            const int jmax = (4 * i + 3) / 8;
-            for (int j = 0; j <= jmax; ++j, ++idx) {
-                if ((idx % NWARP) == warp) {
-#pragma unroll
-                    for (int t = 0; t < G::MAXBW; ++t)
-                        if (t == nbw) slot[t] = (i << 8) | j;
-                    ++nbw;
-                }
-            }
-        }
-    }
-    // rebuild fragments, k-step k2 = 4 g + h:
-    //   A (WS):  l = 4i + (r8>>1), n = 2 k2 + (c4>>1), component p^q, sign p&q
-    //            n ^ swz(l) = 8 g + 2 (h ^ sa) + (c4>>1)
-    //   B (S):   m = 8j + r8,      n = 2 k2 + (c4>>1), component q
-    //            n ^ swz(m) = 8 g + 2 (h ^ sbb) + (c4>>1)
-    int wa_lane[4], b_lane[4];
-    unsigned long long wsgn;
-    {
-        const int p = r8 & 1, q = c4 & 1, cpr = c4 >> 1;
-        const int sa = swz(r8 >> 1) >> 1;
-        const int sbb = swz(r8) >> 1;
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            wa_lane[h] = 4 * (h ^ sa) + 2 * cpr + (p ^ q);
-            b_lane[h] = 4 * (h ^ sbb) + 2 * cpr + q;
-        }
-        wsgn = (p & q) ? 0x8000000000000000ull : 0ull;
-    }
-    double acc[G::MAXBW][2];
-#pragma unroll
-    for (int t = 0; t < G::MAXBW; ++t) acc[t][0] = acc[t][1] = 0.0;
-
-    double p_dx2 = 0.0, p_minq = INFINITY;
-    const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
-    const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
-    const double rho = a.steps[a.k];
-    const double omr = __dsub_rn(1.0, rho);
-
-    auto issue_tile = [&](double2* buf, int col0) {
-        const int n = col0 + lane;
-        const bool colok = n < a.N;
-#pragma unroll
-        for (int s2 = 0; s2 < G::RPT; ++s2) {
-            const int m = warp + 8 * s2;
-            const bool ok = colok && (m < a.L);
-            const double2* src = ok ? (sb + (size_t)m * a.N + n) : sb;
-            cp_async16(buf + cp_dst + s2 * 8 * NCT, src, ok ? 16 : 0);
-        }
-        cp_async_commit();
-    };
-
-    const int ntiles = (n_end - n_begin + NCT - 1) / NCT;
-    if (ntiles > 0) issue_tile(S0, n_begin);
-
-    for (int t = 0; t < ntiles; ++t) {
-        double2* S = (t & 1) ? S1 : S0;
-        const double* Sd = reinterpret_cast<const double*>(S);
-        const int col0 = n_begin + t * NCT;
-        // per-device operands of this tile (lane = column), latency hidden by the quad stage
-        const int ncol = col0 + lane;
-        const bool cvalid = ncol < n_end;
-        double x = 0.0, g = 1.0, pg = 0.0;
-        if (cvalid) {
-            x = a.x_cur[bN + ncol];
-            if (known) g = a.gains[bN + ncol];
-            if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
-            else if (a.kind == PSCA_MAP_UR) pg = a.pgrad[bN + ncol];
-        }
-        cp_async_wait<0>();
-        __syncthreads();
-        if (t + 1 < ntiles) issue_tile((t & 1) ? S0 : S1, col0 + NCT);
-
-        // ---- quadratic forms ---------------------------------------------
-        {
-            double bq[2 * NRB];
-#pragma unroll
-            for (int kk = 0; kk < 2 * NRB; ++kk) bq[kk] = Sd[qoff[kk & 1] + kk * 4 * NCT];
-            double qa0 = 0.0, qa1 = 0.0, ra0 = 0.0, ra1 = 0.0;
-#pragma unroll
-            for (int i = 0; i < NRB; ++i) {
-                if ((rowmask >> i) & 1ull) {
-                    double t0[2] = {0.0, 0.0}, t1[2] = {0.0, 0.0};
-                    double u0[2] = {0.0, 0.0}, u1[2] = {0.0, 0.0};
-                    const double* f = FR + i * (i + 1) * 32 + foff;
-#pragma unroll
-                    for (int kk = 0; kk < 2 * (i + 1); ++kk) {
-                        const double pv = xsign(f[kk * 32], fsgn);
-                        const double av = xsign(f[kk * 32 + 16], fsgn);
-                        if (kk & 1) {
-                            dmma(t1, pv, bq[kk]);
-                            dmma(u1, av, bq[kk]);
-                        } else {
-                            dmma(t0, pv, bq[kk]);
-                            dmma(u0, av, bq[kk]);
-                        }
-                    }
-                    const double s0 = Sd[epoff[0] + i * 8 * NCT];
-                    const double s1 = Sd[epoff[1] + i * 8 * NCT];
-                    qa0 = fma(s0, t0[0] + t1[0], qa0);
-                    qa1 = fma(s1, t0[1] + t1[1], qa1);
-                    ra0 = fma(s0, u0[0] + u1[0], ra0);
-                    ra1 = fma(s1, u0[1] + u1[1], ra1);
-                }
-            }
-#pragma unroll
-            for (int o = 4; o < 32; o <<= 1) {
-                qa0 += __shfl_xor_sync(0xffffffffu, qa0, o);
-                qa1 += __shfl_xor_sync(0xffffffffu, qa1, o);
-                ra0 += __shfl_xor_sync(0xffffffffu, ra0, o);
-                ra1 += __shfl_xor_sync(0xffffffffu, ra1, o);
-            }
-            if (r8 == 0) {
-                const int n0 = cb * 8 + 2 * c4;
-                double* d = qr_s + half * NCT * 2;
-                d[2 * n0] = qa0;
-                d[2 * n0 + 1] = ra0;
-                d[2 * (n0 + 1)] = qa1;
-                d[2 * (n0 + 1) + 1] = ra1;
-            }
-        }
-        __syncthreads();
-
-        // ---- update (estimators.py:272-276) + WS = S diag(w_new) -------------
-        {
-            double w_new = 0.0;
-            if (cvalid) {
-                const double q = qr_s[2 * lane] + qr_s[NCT * 2 + 2 * lane];
-                const double r = qr_s[2 * lane + 1] + qr_s[NCT * 2 + 2 * lane + 1];
-                const double diff = __dsub_rn(q, r);
-                double grad;
-                if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
-                else if (a.kind == PSCA_MAP_K) grad = __dadd_rn(__dmul_rn(g, diff), pg);
-                else if (a.kind == PSCA_ML_UD) grad = diff;
-                else grad = __dadd_rn(diff, pg);
-                const double gq = known ? __dmul_rn(g, q) : q;
-                const double coef = __dmul_rn(gq, gq);
-                const double cand = np_clip(__dsub_rn(x, __ddiv_rn(grad, coef)), 0.0, hi);
-                const double xn = __dadd_rn(__dmul_rn(omr, x), __dmul_rn(rho, cand));
-                w_new = known ? __dmul_rn(xn, g) : xn;
-                if (warp == 0) {
-                    a.x_next[bN + ncol] = xn;
-                    if (a.iterates)
-                        a.iterates[((size_t)b * (a.T + 1) + a.k + 1) * a.N + ncol] = xn;
-                    const double dx = __dsub_rn(xn, x);
-                    p_dx2 = fma(dx, dx, p_dx2);
-                    p_minq = (q < p_minq) ? q : p_minq;
-                }
-            }
-#pragma unroll
-            for (int s2 = 0; s2 < G::RPT; ++s2) {
-                const int idx = cp_dst + s2 * 8 * NCT;     // row warp + 8 s2, column lane
-                const double2 v = S[idx];
-                WS[idx] = make_double2(w_new * v.x, w_new * v.y);
-            }
-        }
-        __syncthreads();
-
-        // ---- rebuild: Sigma_next += S diag(w) S^H (lower C blocks) ----------
-        {
-            const double* Wd = reinterpret_cast<const double*>(WS);
-#pragma unroll
-            for (int t2 = 0; t2 < G::MAXBW; ++t2) {
-                if (t2 < nbw) {
-                    const int bi = slot[t2] >> 8, bj = slot[t2] & 0xff;
-                    const int abase = 2 * (4 * bi + (r8 >> 1)) * NCT;
-                    const int bbase = 2 * (8 * bj + r8) * NCT;
-                    const double* A0 = Wd + abase + wa_lane[0];
-                    const double* A1 = Wd + abase + wa_lane[1];
-                    const double* A2 = Wd + abase + wa_lane[2];
-                    const double* A3 = Wd + abase + wa_lane[3];
-                    const double* B0 = Sd + bbase + b_lane[0];
-                    const double* B1 = Sd + bbase + b_lane[1];
-                    const double* B2 = Sd + bbase + b_lane[2];
-                    const double* B3 = Sd + bbase + b_lane[3];
-                    double e1[2] = {0.0, 0.0}, e2[2] = {0.0, 0.0}, e3[2] = {0.0, 0.0};
-#pragma unroll
-                    for (int k2 = 0; k2 < NCT / 2; ++k2) {
-                        const int h = k2 & 3, g8 = 16 * (k2 >> 2);
-                        const double* Ap = h == 0 ? A0 : h == 1 ? A1 : h == 2 ? A2 : A3;
-                        const double* Bp = h == 0 ? B0 : h == 1 ? B1 : h == 2 ? B2 : B3;
-                        const double av = xsign(Ap[g8], wsgn);
-                        const double bv = Bp[g8];
-                        switch (h) {
-                            case 0: dmma(acc[t2], av, bv); break;
-                            case 1: dmma(e1, av, bv); break;
-                            case 2: dmma(e2, av, bv); break;
-                            default: dmma(e3, av, bv); break;
-                        }
-                    }
-                    acc[t2][0] += (e1[0] + e2[0]) + e3[0];
-                    acc[t2][1] += (e1[1] + e2[1]) + e3[1];
-                }
-            }
-        }
-    }
-
-    // ---- chunk outputs --------------------------------------------------------
-    {
-        double2* sp = a.sig_part + ((size_t)b * a.n_chunks + chunk) * G::NBLK * 32;
-        int idx = 0, t2 = 0;
-        for (int i = 0; i < NRB; ++i) {
-            const int jmax = (4 * i + 3) / 8;
-            for (int j = 0; j <= jmax; ++j, ++idx) {
-                if ((idx % NWARP) == warp) {
-#pragma unroll
-                    for (int u = 0; u < G::MAXBW; ++u)
-                        if (u == t2) sp[(size_t)idx * 32 + lane] = make_double2(acc[u][0], acc[u][1]);
-                    ++t2;
-                }
-            }
-        }
-    }
-    if (warp == 0) {
-        for (int o = 16; o > 0; o >>= 1) {
-            p_dx2 += __shfl_xor_sync(0xffffffffu, p_dx2, o);
-            const double mq = __shfl_xor_sync(0xffffffffu, p_minq, o);
-            p_minq = (mq < p_minq) ? mq : p_minq;
-        }
-        if (lane == 0) {
-            double* rp = a.red_part + ((size_t)b * a.n_chunks + chunk) * 4;
-            rp[0] = p_dx2;
-            rp[1] = p_minq;
-            rp[2] = 0.0;
-            rp[3] = 0.0;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // factor kernel
 // ---------------------------------------------------------------------------
 enum FacMode { FAC_SOLVE = 0, FAC_INVERSE = 1, FAC_PREP = 2, FAC_ASSEMBLE = 3, FAC_OBJECTIVE = 4 };
 
 struct FacArgs {
     int B, N, L, nrb, T, n_chunks, k_new, kind, n_antennas, record_objective;
+    int incremental;            // Sigma - sigma^2 I = D, D_{k+1} = (1-rho_k) D_k + increment
     double tol;
+    const double* steps;        // [T] (incremental: rho_k)
+    double2* dmat;              // incremental: [B][L][L] D_k (lower triangle used)
     const double* noise;        // [B]
     const double2* emp_cov;     // [B][L][L]
     const double2* sig_part;    // [B][chunks][NBLK][32]
@@ -1006,6 +690,10 @@ __device__ void pack_frags(const double2* X, const double2* G, int ld, int L, co
 }
 
 // Sigma (lower + mirrored) from the chunk partial C fragments + sigma^2 I
+// Sigma (lower + mirrored) from the chunk partial C fragments + sigma^2 I.
+// Incremental mode: the partials are the increment S diag(rho_k cand g) S^H,
+// and D_{k+1} = (1 - rho_k) D_k + increment is kept per instance in a.dmat
+// (D_0 = 0); Sigma = D + sigma^2 I.  Full mode: the partials are D itself.
 __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2* X, int ld,
                                bool zero_weights) {
     const int L = a.L;
@@ -1015,7 +703,9 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
     }
     __syncthreads();
     double* Xd = reinterpret_cast<double*>(X);
-    if (!zero_weights) {
+    double* Dd = a.incremental ? reinterpret_cast<double*>(a.dmat + (size_t)b * L * L) : nullptr;
+    const double omr = (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[a.k_new - 1]) : 0.0;
+    {
         const int total = geo.NBLK * 32;
         const double2* sp = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
         for (int e = threadIdx.x; e < total; e += NT) {
@@ -1025,17 +715,30 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
             while (base + (4 * i + 3) / 8 + 1 <= blk) { base += (4 * i + 3) / 8 + 1; ++i; }
             int j = blk - base;
             double2 s = make_double2(0.0, 0.0);
-            for (int c = 0; c < a.n_chunks; ++c) {
-                double2 v = sp[(size_t)c * geo.NBLK * 32 + e];
-                s.x += v.x;
-                s.y += v.y;
+            if (!zero_weights) {
+                for (int c = 0; c < a.n_chunks; ++c) {
+                    double2 v = sp[(size_t)c * geo.NBLK * 32 + e];
+                    s.x += v.x;
+                    s.y += v.y;
+                }
             }
             int r8 = lane >> 2, c4 = lane & 3;
             int l = 4 * i + (r8 >> 1), p = r8 & 1;
             int m0 = 8 * j + 2 * c4;
             if (l < L) {
-                if (m0 <= l) Xd[2 * (l * ld + m0) + p] = s.x;
-                if (m0 + 1 <= l) Xd[2 * (l * ld + m0 + 1) + p] = s.y;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = m0 + h;
+                    if (m <= l) {
+                        const size_t o = 2 * ((size_t)l * L + m) + p;
+                        double val = h ? s.y : s.x;
+                        if (Dd) {
+                            val = zero_weights ? 0.0 : fma(omr, Dd[o], val);
+                            Dd[o] = val;
+                        }
+                        Xd[2 * (l * ld + m) + p] = val;
+                    }
+                }
             }
         }
     }
@@ -1053,38 +756,42 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
     __syncthreads();
 }
 
-// Finalise iteration k = k_new - 1 of instance b (estimators.py:267-286): the
-// q-floor guard on that iteration's q (chunk minima), its update norm, the
-// objective value and the tol stop.  Returns true when the CTA must stop
-// (instance frozen or no further factorisation needed).
+// Finalise iteration k of instance b from its reductions (estimators.py:
+// 267-286): the q-floor guard on that iteration's q, the update norm, the
+// objective value (in = frob, logdet, trace, prior value of iterate k) and
+// the tol stop.  Thread 0 only; returns 0 / PSCA_QFLOOR / PSCA_CONVERGED.
+__device__ int fac_finalize_core(const FacArgs& a, int b, int k, double dx2, double minq,
+                                 const double* in) {
+    const double qfloor = 0.5 * a.L / in[0];
+    if (minq < qfloor) {
+        a.status[b] = PSCA_QFLOOR;
+        a.n_iter[b] = k;
+        return PSCA_QFLOOR;
+    }
+    const double un = sqrt(dx2);
+    a.update_norm[(size_t)b * a.T + k] = un;
+    if (a.objective) a.objective[(size_t)b * a.T + k] = in[1] + in[2] + in[3];
+    a.n_iter[b] = k + 1;
+    if (un < a.tol) {
+        a.status[b] = PSCA_CONVERGED;
+        return PSCA_CONVERGED;
+    }
+    return 0;
+}
+
+// Two-kernel path: finalise iteration k = k_new - 1 from the chunk partials.
+// Returns true when the CTA must stop (instance frozen or no further
+// factorisation needed).
 __device__ bool fac_finalize(const FacArgs& a, int b, int* s_flag) {
     const int tid = threadIdx.x;
     if (tid == 0) {
-        const int k = a.k_new - 1;
         double dx2 = 0.0, minq = INFINITY;
         const double* rp = a.red_part + (size_t)b * a.n_chunks * 4;
         for (int c = 0; c < a.n_chunks; ++c) {
             dx2 += rp[4 * c];
             minq = (rp[4 * c + 1] < minq) ? rp[4 * c + 1] : minq;
         }
-        const double* in = a.inst + (size_t)b * 4;
-        const double qfloor = 0.5 * a.L / in[0];
-        int flag = 0;
-        if (minq < qfloor) {
-            flag = PSCA_QFLOOR;
-            a.status[b] = PSCA_QFLOOR;
-            a.n_iter[b] = k;
-        } else {
-            const double un = sqrt(dx2);
-            a.update_norm[(size_t)b * a.T + k] = un;
-            if (a.objective) a.objective[(size_t)b * a.T + k] = in[1] + in[2] + in[3];
-            a.n_iter[b] = k + 1;
-            if (un < a.tol) {
-                flag = PSCA_CONVERGED;
-                a.status[b] = PSCA_CONVERGED;
-            }
-        }
-        *s_flag = flag;
+        *s_flag = fac_finalize_core(a, b, a.k_new - 1, dx2, minq, a.inst + (size_t)b * 4);
     }
     __syncthreads();
     if (*s_flag == PSCA_QFLOOR) {
@@ -1098,12 +805,11 @@ __device__ bool fac_finalize(const FacArgs& a, int b, int* s_flag) {
 // Prior terms at the new iterate x_{k_new} (priors.py:145-159, 370-399): the
 // map-ur gradient for the next column pass (into a.pgrad) and, when the
 // objective is recorded, the prior penalty value.
-__device__ double fac_prior_terms(const FacArgs& a, int b, double* sred) {
+__device__ double fac_prior_terms_at(const FacArgs& a, int b, const double* xv, double* sred) {
     const int tid = threadIdx.x;
     double prior_value = 0.0;
     if ((a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.record_objective))) {
         const size_t bN = (size_t)b * a.N;
-        const double* xv = (a.k_new == 0 ? a.x_cur : a.x_next) + bN;
         double acc = 0.0;
         for (int n = tid; n < a.N; n += NT) {
             const double x = xv[n];
@@ -1130,6 +836,11 @@ __device__ double fac_prior_terms(const FacArgs& a, int b, double* sred) {
     }
 
     return prior_value;
+}
+
+__device__ double fac_prior_terms(const FacArgs& a, int b, double* sred) {
+    const size_t bN = (size_t)b * a.N;
+    return fac_prior_terms_at(a, b, (a.k_new == 0 ? a.x_cur : a.x_next) + bN, sred);
 }
 
 template <int MODE>
@@ -1301,261 +1012,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// Compiled-shape factor kernel (FAC_SOLVE, padded LP <= 16*RT <= 80).
-// Thread (ty, tx) = (tid/16, tid%16) owns the RT x RT entries
-// (ty + 16u, tx + 16v) of every L x L matrix.  The Gauss-Jordan sweep keeps
-// them in registers; only the pivot row / column of each step go through SMEM
-// (ping-pong staged by their owners, one barrier per pivot).  The two GEMMs of
-// A = P^H Sigma_hat P are register-tiled the same way, and each thread packs
-// the P'/A' fragment entries it owns straight into the fragment buffer.
-// ---------------------------------------------------------------------------
-template <int RT>
-__global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double sred[NWARP + 1];
-    __shared__ int s_flag;
-    const Geo geo = make_geo(a.L, a.nrb);
-    const int b = blockIdx.x;
-    const int tid = threadIdx.x;
-    const int L = a.L, LP = geo.LP;
-    const int ld = LP + 1;
-    if (a.status[b] != PSCA_RUNNING) return;
-    if (a.k_new > 0) {
-        if (fac_finalize(a, b, &s_flag)) return;
-    }
-    const double prior_value = fac_prior_terms(a, b, sred);
-
-    double2* sm = reinterpret_cast<double2*>(smem_raw);
-    double2* rowb = sm;             // [2][LP]
-    double2* colb = sm + 2 * LP;    // [2][LP]
-    double2* X = sm + 4 * LP;       // [LP][ld]
-    double2* G = X + (size_t)LP * ld;
-
-    assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
-    double frob;
-    {
-        double s = 0.0;
-        for (int e = tid; e < L * L; e += NT) {
-            const int i = e / L, j = e - i * L;
-            const double2 v = X[i * ld + j];
-            s = fma(v.x, v.x, fma(v.y, v.y, s));
-        }
-        frob = sqrt(block_sum(s, sred));
-    }
-
-    const int ty = tid >> 4, tx = tid & 15;
-    double2 v[RT][RT];
-#pragma unroll
-    for (int u = 0; u < RT; ++u)
-#pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            v[u][w] = (i < L && j < L) ? X[i * ld + j] : make_double2(0.0, 0.0);
-        }
-    for (int e = tid; e < L; e += NT) {
-        rowb[e] = X[e];
-        colb[e] = X[e * ld];
-    }
-    __syncthreads();
-
-    // ---- Gauss-Jordan sweep (covlinalg.py:91-115 restated; pivots = LDL^H) ----
-    double logdet = 0.0;
-    bool ok = true;
-    for (int k = 0; k < L; ++k) {
-        const double2* rk = rowb + (k & 1) * LP;
-        const double2* ck = colb + (k & 1) * LP;
-        double2* rn = rowb + ((k + 1) & 1) * LP;
-        double2* cn = colb + ((k + 1) & 1) * LP;
-        const double piv = rk[k].x;
-        if (!(piv > 0.0)) {
-            ok = false;
-            break;
-        }
-        logdet += log(piv);
-        const double pinv = 1.0 / piv;
-        double2 cu[RT], rw[RT];
-#pragma unroll
-        for (int u = 0; u < RT; ++u) {
-            const int i = ty + 16 * u;
-            cu[u] = (i < L) ? ck[i] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int j = tx + 16 * w;
-            rw[w] = (j < L) ? rk[j] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < RT; ++u) {
-            const int i = ty + 16 * u;
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int j = tx + 16 * w;
-                if (i < L && j < L) {
-                    const double2 o = v[u][w];
-                    double2 nv;
-                    if (i == k) {
-                        nv = (j == k) ? make_double2(pinv, 0.0) : make_double2(o.x * pinv, o.y * pinv);
-                    } else if (j == k) {
-                        nv = make_double2(-o.x * pinv, -o.y * pinv);
-                    } else {
-                        const double2 pr = cmul(cu[u], rw[w]);
-                        nv = make_double2(o.x - pr.x * pinv, o.y - pr.y * pinv);
-                    }
-                    v[u][w] = nv;
-                    if (i == k + 1) rn[j] = nv;
-                    if (j == k + 1) cn[i] = nv;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    if (!ok) {
-        if (tid == 0) {
-            a.status[b] = PSCA_CHOL_FAIL;
-            if (a.cond_est) a.cond_est[b] = INFINITY;
-        }
-        return;
-    }
-    // ---- P = (P + P^H)/2 (covlinalg.py:107, 112-114) ---------------------------
-#pragma unroll
-    for (int u = 0; u < RT; ++u)
-#pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
-        }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < RT; ++u)
-#pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            if (i < L && j < L) {
-                const double2 t = X[j * ld + i];
-                v[u][w] = (i == j) ? make_double2(v[u][w].x, 0.0)
-                                   : make_double2(0.5 * (v[u][w].x + t.x), 0.5 * (v[u][w].y - t.y));
-            }
-        }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < RT; ++u)
-#pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
-        }
-    __syncthreads();
-
-    const double2* E = a.emp_cov + (size_t)b * L * L;
-    double trace = 0.0;
-    if (a.record_objective) {
-        double s = 0.0;
-#pragma unroll
-        for (int u = 0; u < RT; ++u)
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int i = ty + 16 * u, j = tx + 16 * w;
-                if (i < L && j < L) {
-                    const double2 ev = __ldg(E + (size_t)j * L + i);
-                    s = fma(v[u][w].x, ev.x, fma(-v[u][w].y, ev.y, s));
-                }
-            }
-        trace = block_sum(s, sred);
-    }
-    // ---- G = Sigma_hat P ------------------------------------------------------
-    {
-        double2 gacc[RT][RT];
-#pragma unroll
-        for (int u = 0; u < RT; ++u)
-#pragma unroll
-            for (int w = 0; w < RT; ++w) gacc[u][w] = make_double2(0.0, 0.0);
-        for (int c = 0; c < L; ++c) {
-            double2 eu[RT], xw[RT];
-#pragma unroll
-            for (int u = 0; u < RT; ++u) {
-                const int i = ty + 16 * u;
-                eu[u] = (i < L) ? __ldg(E + (size_t)i * L + c) : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int j = tx + 16 * w;
-                xw[w] = (j < LP) ? X[c * ld + j] : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < RT; ++u)
-#pragma unroll
-                for (int w = 0; w < RT; ++w) gacc[u][w] = cfma(eu[u], xw[w], gacc[u][w]);
-        }
-#pragma unroll
-        for (int u = 0; u < RT; ++u)
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int i = ty + 16 * u, j = tx + 16 * w;
-                if (i < LP && j < LP) G[i * ld + j] = gacc[u][w];
-            }
-    }
-    __syncthreads();
-    // ---- A = P^H G and the fragment pack ---------------------------------------
-    {
-        double2 aacc[RT][RT];
-#pragma unroll
-        for (int u = 0; u < RT; ++u)
-#pragma unroll
-            for (int w = 0; w < RT; ++w) aacc[u][w] = make_double2(0.0, 0.0);
-        for (int t = 0; t < L; ++t) {
-            double2 pu[RT], gw[RT];
-#pragma unroll
-            for (int u = 0; u < RT; ++u) {
-                const int i = ty + 16 * u;
-                pu[u] = (i < LP) ? X[t * ld + i] : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int j = tx + 16 * w;
-                gw[w] = (j < LP) ? G[t * ld + j] : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < RT; ++u)
-#pragma unroll
-                for (int w = 0; w < RT; ++w) aacc[u][w] = cfma_conj_a(pu[u], gw[w], aacc[u][w]);
-        }
-        double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 16);
-#pragma unroll
-        for (int u = 0; u < RT; ++u)
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int l = ty + 16 * u, m = tx + 16 * w;
-                if (l < LP && m <= 4 * (l >> 2) + 3) {
-                    double2 pv = make_double2(0.0, 0.0), av = make_double2(0.0, 0.0);
-                    if (l < L && m <= l) {
-                        pv = X[l * ld + m];
-                        av = aacc[u][w];
-                        if (m < l) {
-                            pv.x *= 2.0; pv.y *= 2.0; av.x *= 2.0; av.y *= 2.0;
-                        } else {
-                            pv.y = 0.0; av.y = 0.0;
-                        }
-                    }
-                    const int i4 = l >> 2;
-                    const int blk = i4 * (i4 + 1) + (m >> 1);
-                    const int ent = (l & 3) * 2 + (m & 1);
-                    double* o = od + (size_t)blk * 32;
-                    o[2 * ent] = pv.x;
-                    o[2 * ent + 1] = pv.y;
-                    o[16 + 2 * ent] = av.x;
-                    o[16 + 2 * ent + 1] = av.y;
-                }
-            }
-    }
-    if (tid == 0) {
-        double* in = a.inst + (size_t)b * 4;
-        in[0] = frob;
-        in[1] = logdet;
-        in[2] = trace;
-        in[3] = prior_value;
-    }
-}
+#include "psca_fast.cuh"
 
 // ---------------------------------------------------------------------------
 // empirical covariance (HERK): Sigma_hat = Y Y^H / M
@@ -1643,6 +1100,14 @@ int auto_chunks(int B, int N) {
 // Other L are padded up to the next one; L > 80 uses the generic kernel.
 constexpr int kCompiledNrb[] = {2, 3, 4, 5, 6, 8, 10, 12, 16, 20};
 
+bool full_rebuild_forced() {
+    static const bool forced = [] {
+        const char* e = getenv("PSCA_FULL_REBUILD");
+        return e && e[0] == '1';
+    }();
+    return forced;
+}
+
 bool generic_forced() {
     static const bool forced = [] {
         const char* e = getenv("PSCA_GENERIC_COLUMN");
@@ -1662,7 +1127,7 @@ int solve_nrb(int L) {
 template <int NRB>
 cudaError_t launch_column_t(const ColArgs& ca, int n_chunks, cudaStream_t st) {
     auto kfn = column_kernel_t<NRB>;
-    const size_t sm = TG<NRB>::SMEM;
+    const size_t sm = TG<NRB>::COL_SMEM;
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
@@ -1722,7 +1187,8 @@ cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, c
 
 template <int RT>
 cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
-    const size_t sm = (size_t)4 * g.LP * 16 + (size_t)2 * g.LP * (g.LP + 1) * 16;
+    size_t sm = (size_t)4 * g.LP * 16 + (size_t)3 * g.LP * (g.LP + 1) * 16;
+    if (sm > 227 * 1024) sm -= (size_t)g.LP * (g.LP + 1) * 16;   // Sigma_hat read from L2 instead
     auto kfn = factor_solve_t<RT>;
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1751,6 +1217,69 @@ cudaError_t launch_solve_factor(const FacArgs& fa, const Geo& g, cudaStream_t st
     return launch_factor<FAC_SOLVE>(fa, g, st);
 }
 
+thread_local int g_last_path = 0;   // 0 two-kernel, 1 persistent
+
+bool persistent_disabled() {
+    static const bool off = [] {
+        const char* e = getenv("PSCA_NO_PERSISTENT");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
+
+int sm_count() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 1;
+    }();
+    return n;
+}
+
+bool persistent_shape(int nrb) {
+    switch (nrb) {
+        case 2: case 3: case 4: case 5: case 6: case 8: case 10: case 12: return true;
+        default: return false;
+    }
+}
+
+template <int NRB>
+cudaError_t launch_persistent_t(const ColArgs& ca, const FacArgs& fa, int* counter,
+                                cudaStream_t st) {
+    auto kfn = psca_persistent_t<NRB>;
+    const size_t sm = TG<NRB>::PERSIST_SMEM;
+    cudaError_t err =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (err != cudaSuccess) return err;
+    int occ = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, sm);
+    if (err != cudaSuccess) return err;
+    if (occ < 1) occ = 1;
+    int grid = sm_count() * occ;
+    if (grid > ca.B) grid = ca.B;
+    if (cudaMemsetAsync(counter, 0, sizeof(int), st) != cudaSuccess) return cudaGetLastError();
+    ProfScope prof(st, 0);
+    kfn<<<grid, NT, sm, st>>>(ca, fa, counter);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_persistent(const ColArgs& ca, const FacArgs& fa, int* counter, int nrb,
+                              cudaStream_t st) {
+    switch (nrb) {
+        case 2: return launch_persistent_t<2>(ca, fa, counter, st);
+        case 3: return launch_persistent_t<3>(ca, fa, counter, st);
+        case 4: return launch_persistent_t<4>(ca, fa, counter, st);
+        case 5: return launch_persistent_t<5>(ca, fa, counter, st);
+        case 6: return launch_persistent_t<6>(ca, fa, counter, st);
+        case 8: return launch_persistent_t<8>(ca, fa, counter, st);
+        case 10: return launch_persistent_t<10>(ca, fa, counter, st);
+        case 12: return launch_persistent_t<12>(ca, fa, counter, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <int MODE>
 cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     size_t sm = fac_smem_bytes(g);
@@ -1771,6 +1300,8 @@ struct SolveLayout {
     double* x_alt;
     double* inst;
     double* pgrad;
+    int* counter;
+    double2* dmat;
     double2* scratch;
     size_t total;
 };
@@ -1784,6 +1315,8 @@ SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, v
     s.x_alt = cv.take<double>((size_t)a->B * a->N * 8);
     s.inst = cv.take<double>((size_t)a->B * 4 * 8);
     s.pgrad = cv.take<double>(a->kind == PSCA_MAP_UR ? (size_t)a->B * a->N * 8 : 0);
+    s.counter = cv.take<int>(sizeof(int));
+    s.dmat = cv.take<double2>((size_t)a->B * a->L * a->L * 16);
     s.scratch = cv.take<double2>(fac_scratch_bytes(g, a->B));
     s.total = cv.off;
     return s;
@@ -1816,7 +1349,11 @@ extern "C" {
 
 const char* psca_version(void) { return PSCA_VERSION_STR; }
 
+const char* psca_last_error(void) { return cudaGetErrorString(g_last_err); }
+
 int psca_last_launch_count(void) { return g_launches; }
+
+int psca_last_path(void) { return g_last_path; }
 
 int psca_profile_begin(void) {
     g_prof.on = true;
@@ -1886,11 +1423,17 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     ca.sig_part = lay.sig_part; ca.red_part = lay.red_part; ca.status = a->status;
     ca.steps = a->steps; ca.prior_lin = a->prior_lin; ca.prior_p = a->prior_p; ca.eff = a->eff;
     ca.pgrad = lay.pgrad;
+    // incremental rebuild needs the compiled column kernel (psca_fast.cuh)
+    const bool fast_col = !generic_forced() && g.NRB <= 20 &&
+                          (g.NRB == 2 || g.NRB == 3 || g.NRB == 4 || g.NRB == 5 || g.NRB == 6 ||
+                           g.NRB == 8 || g.NRB == 10 || g.NRB == 12 || g.NRB == 16 || g.NRB == 20);
+    ca.incremental = (fast_col && !full_rebuild_forced()) ? 1 : 0;
 
     FacArgs fa{};
     fa.B = a->B; fa.N = a->N; fa.L = a->L; fa.nrb = g.NRB; fa.T = a->max_iter;
     fa.n_chunks = n_chunks;
     fa.prior_lin = a->prior_lin; fa.prior_p = a->prior_p; fa.eff = a->eff; fa.pgrad = lay.pgrad;
+    fa.incremental = ca.incremental; fa.steps = a->steps; fa.dmat = lay.dmat;
     fa.kind = a->kind; fa.n_antennas = a->n_antennas;
     fa.record_objective = ca.record_objective; fa.tol = a->tol;
     fa.noise = a->noise; fa.emp_cov = reinterpret_cast<const double2*>(a->emp_cov);
@@ -1901,13 +1444,24 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
 
     double* xc = a->x_out;
     double* xn = lay.x_alt;
+    // persistent path: whole instances per CTA (one chunk), enough instances
+    // to fill every SM twice, a compiled persistent shape
+    const bool persistent = !generic_forced() && !persistent_disabled() &&
+                            persistent_shape(g.NRB) && n_chunks == 1 &&
+                            (a->n_chunks == 1 || a->B >= 2 * sm_count());
+    g_last_path = persistent ? 1 : 0;
+    if (persistent) {
+        fa.x_cur = xc; fa.x_next = xn;
+        if (!ok_or_record(launch_persistent(ca, fa, lay.counter, g.NRB, st))) return PSCA_E_CUDA;
+        return cudaGetLastError() == cudaSuccess ? PSCA_OK : PSCA_E_CUDA;
+    }
     fa.k_new = 0; fa.x_cur = xc; fa.x_next = xn;
-    if (launch_solve_factor(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+    if (!ok_or_record(launch_solve_factor(fa, g, st))) return PSCA_E_CUDA;
     for (int k = 0; k < a->max_iter; ++k) {
         ca.k = k; ca.x_cur = xc; ca.x_next = xn;
-        if (launch_solve_column(ca, g, n_chunks, st) != cudaSuccess) return PSCA_E_CUDA;
+        if (!ok_or_record(launch_solve_column(ca, g, n_chunks, st))) return PSCA_E_CUDA;
         fa.k_new = k + 1; fa.x_cur = xc; fa.x_next = xn;
-        if (launch_solve_factor(fa, g, st) != cudaSuccess) return PSCA_E_CUDA;
+        if (!ok_or_record(launch_solve_factor(fa, g, st))) return PSCA_E_CUDA;
         double* t = xc; xc = xn; xn = t;
     }
     if (xc != a->x_out) {

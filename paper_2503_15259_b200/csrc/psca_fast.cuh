@@ -1,0 +1,861 @@
+// psca_fast.cuh -- compiled-shape kernels of the PSCA hot path (sm_100a).
+// Included by psca.cu inside its anonymous namespace (uses its helpers,
+// ColArgs / FacArgs, assemble_sigma, fac_* and the fragment layout).
+//
+// Two device functions carry the work:
+//   col_pass<NRB>     one column pass of one instance over a column range:
+//                     quadratic forms on DMMA, fused per-device update,
+//                     WS = S diag(w_new), covariance rebuild on DMMA
+//   factor_pass<RT>   Hermitian PD inverse of the L x L Sigma held in SMEM
+//                     (register-tiled Gauss-Jordan), A = P^H Sigma_hat P, and
+//                     the packed P'/A' fragments for the next col_pass
+// and three kernels use them:
+//   column_kernel_t / factor_solve_t   the two-kernel-per-iteration path
+//                                      (any batch, column chunks per instance)
+//   psca_persistent_t                  one launch for the whole solve: each CTA
+//                                      owns one instance at a time for all T
+//                                      iterations; fragments never leave SMEM,
+//                                      Sigma goes from the rebuild accumulators
+//                                      straight into the factor's SMEM, and the
+//                                      latency-bound factor phase of one CTA
+//                                      overlaps the DMMA work of the other
+//                                      resident CTA.
+
+template <int NRB>
+struct TG {
+    static constexpr int LP = 4 * NRB;
+    static constexpr int LP8 = (LP + 7) & ~7;
+    static constexpr int NB = NRB * (NRB + 1);
+    static constexpr int NBLK = rebuild_block_count(NRB);
+    static constexpr int MAXBW = (NBLK + NWARP - 1) / NWARP;
+    static constexpr int RPT = LP8 / 8;            // tile rows per warp (copy / WS build)
+    static constexpr int RT = (LP + 15) / 16;       // factor register tile
+    static constexpr size_t S_BYTES = (size_t)LP8 * NCT * 16;
+    static constexpr size_t F_BYTES = (size_t)NB * 256;
+    static constexpr size_t SMALL = 2 * NCT * 2 * 8 + NWARP * 4 * 8;
+    // fragments staged in SMEM when they fit beside the four tile buffers
+    // (NRB <= 16); otherwise col_pass reads them through L1 from global
+    static constexpr bool FR_SMEM = 4 * S_BYTES + F_BYTES + SMALL <= 227 * 1024;
+    static constexpr size_t COL_SMEM = 4 * S_BYTES + (FR_SMEM ? F_BYTES : 0) + SMALL;
+    static constexpr size_t FAC_BYTES = (size_t)4 * LP * 16 + (size_t)3 * LP * (LP + 1) * 16;
+    static constexpr size_t UNION = (4 * S_BYTES > FAC_BYTES) ? 4 * S_BYTES : FAC_BYTES;
+    static constexpr size_t PERSIST_SMEM = F_BYTES + UNION + SMALL;
+};
+
+// rebuild C blocks owned by this warp: w, w+8, ... in row-major lower order,
+// packed (i << 8) | j
+template <int NRB>
+__device__ __forceinline__ void rebuild_slots(int (&slot)[TG<NRB>::MAXBW], int& nbw) {
+    const int warp = threadIdx.x >> 5;
+    nbw = 0;
+    int idx = 0;
+#pragma unroll 1
+    for (int i = 0; i < NRB; ++i) {
+        const int jmax = (4 * i + 3) / 8;
+        for (int j = 0; j <= jmax; ++j, ++idx) {
+            if ((idx % NWARP) == warp) {
+#pragma unroll
+                for (int t = 0; t < TG<NRB>::MAXBW; ++t)
+                    if (t == nbw) slot[t] = (i << 8) | j;
+                ++nbw;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// col_pass: one PSCA column pass (estimators.py:262-276 for columns
+// [n_begin, n_end)) of instance b at iteration k.
+//   FR    packed P'/A' fragments in SMEM (pack_frags layout)
+//   S0/S1 tile double buffer, WS = S diag(w_new) (all SMEM, swizzled rows)
+// Per 32-column tile:
+//   [cp.async prefetch of tile t+1; x, g of tile t into registers]
+//   quad forms    warp -> (8-column block, row-block half); B fragments of the
+//                 column block in registers; 4 independent DMMA chains
+//   sync
+//   update + WS   warp w builds rows w, w+8, ... of WS for the 32 columns
+//                 (lane = column); the per-device update is computed by every
+//                 warp with identical arithmetic, warp 0 stores x_next
+//   sync
+//   rebuild       warp -> its lower-triangle C blocks, 4 DMMA chains each
+// On return acc holds this pass's rebuild C fragments and warp 0 holds the
+// per-lane partial sum of (x_next - x)^2 and min q; all cp.async groups are
+// retired and the CTA is synchronised.
+// ---------------------------------------------------------------------------
+template <int NRB>
+__device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
+                                         const double* __restrict__ x_cur,
+                                         double* __restrict__ x_next, int n_begin, int n_end,
+                                         double2* S0, double2* S1, double2* WS, double2* SP,
+                                         const double* FR,
+                                         double* qr_s, double (&acc)[TG<NRB>::MAXBW][2],
+                                         const int (&slot)[TG<NRB>::MAXBW], int nbw,
+                                         double& p_dx2, double& p_minq) {
+    using G = TG<NRB>;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const size_t bN = (size_t)b * a.N;
+    const double2* sb = a.pilots + (size_t)b * a.L * a.N;
+
+    // ---- per-lane constants --------------------------------------------------
+    const int cp_dst = warp * NCT + (lane ^ swz(warp));   // tile slot (+ s*8*NCT)
+    const int cb = warp & (NCB - 1);
+    const int half = warp / NCB;
+    unsigned long long rowmask = 0ull;
+    {
+        int load0 = 0, load1 = 0;
+        for (int i = NRB - 1; i >= 0; --i) {
+            const int cost = 2 * (i + 1);
+            const int h = (load1 < load0) ? 1 : 0;
+            if (h) load1 += cost; else load0 += cost;
+            if (h == half) rowmask |= (1ull << i);
+        }
+    }
+    int qoff[2];   // quad B fragment (m = 2kk + c4/2, n = 8cb + r8), k-step parity
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+        const int cpr = c4 >> 1;
+        const int sw = (cpr << 2) | (2 * par);
+        qoff[par] = 2 * (cpr * NCT + cb * 8 + (r8 ^ sw)) + (c4 & 1);
+    }
+    int epoff[2];  // epilogue S at C-fragment positions (+ i*8*NCT)
+    {
+        const int se = swz(r8 >> 1);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            epoff[j] = 2 * ((r8 >> 1) * NCT + cb * 8 + ((2 * c4 + j) ^ se)) + (r8 & 1);
+    }
+    const int foff = frag_lane_offset(lane);
+    const unsigned long long fsgn = frag_lane_sign(lane);
+    // rebuild fragments, k-step k2 = 4 g + h:
+    //   A (WS):  l = 4i + (r8>>1), n = 2 k2 + (c4>>1), component p^q, sign p&q
+    //            n ^ swz(l) = 8 g + 2 (h ^ sa) + (c4>>1)
+    //   B (S):   m = 8j + r8,      n = 2 k2 + (c4>>1), component q
+    //            n ^ swz(m) = 8 g + 2 (h ^ sbb) + (c4>>1)
+    int wa_lane[4], b_lane[4];
+    unsigned long long wsgn;
+    {
+        const int p = r8 & 1, q = c4 & 1, cpr = c4 >> 1;
+        const int sa = swz(r8 >> 1) >> 1;
+        const int sbb = swz(r8) >> 1;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            wa_lane[h] = 4 * (h ^ sa) + 2 * cpr + (p ^ q);
+            b_lane[h] = 4 * (h ^ sbb) + 2 * cpr + q;
+        }
+        wsgn = (p & q) ? 0x8000000000000000ull : 0ull;
+    }
+#pragma unroll
+    for (int t = 0; t < G::MAXBW; ++t) acc[t][0] = acc[t][1] = 0.0;
+    p_dx2 = 0.0;
+    p_minq = INFINITY;
+
+    const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
+    const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
+    const double rho = a.steps[k];
+    const double omr = __dsub_rn(1.0, rho);
+
+    auto issue_tile = [&](double2* buf, int col0) {
+        const int n = col0 + lane;
+        const bool colok = n < a.N;
+#pragma unroll
+        for (int s2 = 0; s2 < G::RPT; ++s2) {
+            const int m = warp + 8 * s2;
+            const bool ok = colok && (m < a.L);
+            const double2* src = ok ? (sb + (size_t)m * a.N + n) : sb;
+            cp_async16(buf + cp_dst + s2 * 8 * NCT, src, ok ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+
+    const int ntiles = (n_end - n_begin + NCT - 1) / NCT;
+    if (ntiles > 0) issue_tile(S0, n_begin);
+
+    for (int t = 0; t < ntiles; ++t) {
+        double2* S = (t & 1) ? S1 : S0;
+        const double* Sd = reinterpret_cast<const double*>(S);
+        const int col0 = n_begin + t * NCT;
+        // per-device operands of this tile (lane = column), latency hidden by the quad stage
+        const int ncol = col0 + lane;
+        const bool cvalid = ncol < n_end;
+        double x = 0.0, g = 1.0, pg = 0.0;
+        if (cvalid) {
+            x = x_cur[ncol];
+            if (known) g = a.gains[bN + ncol];
+            if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
+            else if (a.kind == PSCA_MAP_UR) pg = a.pgrad[bN + ncol];
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        if (t + 1 < ntiles) issue_tile((t & 1) ? S0 : S1, col0 + NCT);
+
+        // ---- quadratic forms ---------------------------------------------
+        {
+            double bq[2 * NRB];
+#pragma unroll
+            for (int kk = 0; kk < 2 * NRB; ++kk) bq[kk] = Sd[qoff[kk & 1] + kk * 4 * NCT];
+            double qa0 = 0.0, qa1 = 0.0, ra0 = 0.0, ra1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < NRB; ++i) {
+                if ((rowmask >> i) & 1ull) {
+                    double t0[2] = {0.0, 0.0}, t1[2] = {0.0, 0.0};
+                    double u0[2] = {0.0, 0.0}, u1[2] = {0.0, 0.0};
+                    const double* f = FR + i * (i + 1) * 32 + foff;
+#pragma unroll
+                    for (int kk = 0; kk < 2 * (i + 1); ++kk) {
+                        const double pv = xsign(f[kk * 32], fsgn);
+                        const double av = xsign(f[kk * 32 + 16], fsgn);
+                        if (kk & 1) {
+                            dmma(t1, pv, bq[kk]);
+                            dmma(u1, av, bq[kk]);
+                        } else {
+                            dmma(t0, pv, bq[kk]);
+                            dmma(u0, av, bq[kk]);
+                        }
+                    }
+                    const double s0 = Sd[epoff[0] + i * 8 * NCT];
+                    const double s1 = Sd[epoff[1] + i * 8 * NCT];
+                    qa0 = fma(s0, t0[0] + t1[0], qa0);
+                    qa1 = fma(s1, t0[1] + t1[1], qa1);
+                    ra0 = fma(s0, u0[0] + u1[0], ra0);
+                    ra1 = fma(s1, u0[1] + u1[1], ra1);
+                }
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                qa0 += __shfl_xor_sync(0xffffffffu, qa0, o);
+                qa1 += __shfl_xor_sync(0xffffffffu, qa1, o);
+                ra0 += __shfl_xor_sync(0xffffffffu, ra0, o);
+                ra1 += __shfl_xor_sync(0xffffffffu, ra1, o);
+            }
+            if (r8 == 0) {
+                const int n0 = cb * 8 + 2 * c4;
+                double* d = qr_s + half * NCT * 2;
+                d[2 * n0] = qa0;
+                d[2 * n0 + 1] = ra0;
+                d[2 * (n0 + 1)] = qa1;
+                d[2 * (n0 + 1) + 1] = ra1;
+            }
+        }
+        __syncthreads();
+
+        // ---- update (estimators.py:272-276) + packed rebuild operands ---------
+        // v = w_new (full rebuild) or rho * cand * g (incremental: the increment
+        // of D = Sigma - sigma^2 I); the nonzero-v columns are compacted (ballot,
+        // identical in every warp) into slots 0..nnz-1 of WS = S diag(v) and of
+        // SP = S, so the rebuild runs over ceil(nnz/2) k-steps only.
+        int nnz;
+        {
+            double v = 0.0;
+            if (cvalid) {
+                const double q = qr_s[2 * lane] + qr_s[NCT * 2 + 2 * lane];
+                const double r = qr_s[2 * lane + 1] + qr_s[NCT * 2 + 2 * lane + 1];
+                const double diff = __dsub_rn(q, r);
+                double grad;
+                if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
+                else if (a.kind == PSCA_MAP_K) grad = __dadd_rn(__dmul_rn(g, diff), pg);
+                else if (a.kind == PSCA_ML_UD) grad = diff;
+                else grad = __dadd_rn(diff, pg);
+                const double gq = known ? __dmul_rn(g, q) : q;
+                const double coef = __dmul_rn(gq, gq);
+                const double cand = np_clip(__dsub_rn(x, __ddiv_rn(grad, coef)), 0.0, hi);
+                const double rc = __dmul_rn(rho, cand);
+                const double xn = __dadd_rn(__dmul_rn(omr, x), rc);
+                if (a.incremental) v = known ? __dmul_rn(rc, g) : rc;
+                else v = known ? __dmul_rn(xn, g) : xn;
+                if (warp == 0) {
+                    x_next[ncol] = xn;
+                    if (a.iterates)
+                        a.iterates[((size_t)b * (a.T + 1) + k + 1) * a.N + ncol] = xn;
+                    const double dx = __dsub_rn(xn, x);
+                    p_dx2 = fma(dx, dx, p_dx2);
+                    p_minq = (q < p_minq) ? q : p_minq;
+                }
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
+            nnz = __popc(mask);
+            const int pos = __popc(mask & ((1u << lane) - 1u));
+            const bool pad = (lane == nnz) && (nnz & 1);     // zero slot after an odd count
+#pragma unroll
+            for (int s2 = 0; s2 < G::RPT; ++s2) {
+                const int l = warp + 8 * s2;
+                const int sw = swz(warp);
+                if (v != 0.0) {
+                    const double2 sv = S[cp_dst + s2 * 8 * NCT];
+                    const int o = l * NCT + (pos ^ sw);
+                    WS[o] = make_double2(v * sv.x, v * sv.y);
+                    SP[o] = sv;
+                }
+                if (pad) {
+                    const int o = l * NCT + (nnz ^ sw);
+                    WS[o] = make_double2(0.0, 0.0);
+                    SP[o] = make_double2(0.0, 0.0);
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- rebuild: += WS SP^H over the packed slots (lower C blocks) -------
+        if (nnz > 0) {
+            const double* Wd = reinterpret_cast<const double*>(WS);
+            const double* Pd = reinterpret_cast<const double*>(SP);
+            const int nk2 = (nnz + 1) >> 1;
+#pragma unroll
+            for (int t2 = 0; t2 < G::MAXBW; ++t2) {
+                if (t2 < nbw) {
+                    const int bi = slot[t2] >> 8, bj = slot[t2] & 0xff;
+                    const int abase = 2 * (4 * bi + (r8 >> 1)) * NCT;
+                    const int bbase = 2 * (8 * bj + r8) * NCT;
+                    const double* A0 = Wd + abase + wa_lane[0];
+                    const double* A1 = Wd + abase + wa_lane[1];
+                    const double* A2 = Wd + abase + wa_lane[2];
+                    const double* A3 = Wd + abase + wa_lane[3];
+                    const double* B0 = Pd + bbase + b_lane[0];
+                    const double* B1 = Pd + bbase + b_lane[1];
+                    const double* B2 = Pd + bbase + b_lane[2];
+                    const double* B3 = Pd + bbase + b_lane[3];
+                    double e1[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int k2 = 0; k2 < NCT / 2; ++k2) {
+                        if (k2 < nk2) {
+                            const int h = k2 & 3, g8 = 16 * (k2 >> 2);
+                            const double* Ap = h == 0 ? A0 : h == 1 ? A1 : h == 2 ? A2 : A3;
+                            const double* Bp = h == 0 ? B0 : h == 1 ? B1 : h == 2 ? B2 : B3;
+                            const double av = xsign(Ap[g8], wsgn);
+                            const double bv = Bp[g8];
+                            if (k2 & 1) dmma(e1, av, bv);
+                            else dmma(acc[t2], av, bv);
+                        }
+                    }
+                    acc[t2][0] += e1[0];
+                    acc[t2][1] += e1[1];
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+}
+
+// Reduce warp 0's per-lane (dx2, min q) partials; result valid in thread 0.
+__device__ __forceinline__ void reduce_pass_partials(double& dx2, double& minq) {
+    if ((threadIdx.x >> 5) == 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            dx2 += __shfl_xor_sync(0xffffffffu, dx2, o);
+            const double mq = __shfl_xor_sync(0xffffffffu, minq, o);
+            minq = (mq < minq) ? mq : minq;
+        }
+    }
+}
+
+// Rebuild C fragments -> lower triangle of Sigma in X (rows / cols < L).
+// Incremental mode (Dd != nullptr): D_{k+1} = omr * D_k + acc, kept in Dd.
+template <int NRB>
+__device__ __forceinline__ void acc_to_sigma(const double (&acc)[TG<NRB>::MAXBW][2],
+                                             const int (&slot)[TG<NRB>::MAXBW], int nbw,
+                                             double2* X, int ld, int L, double* Dd, double omr) {
+    const int lane = threadIdx.x & 31;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    double* Xd = reinterpret_cast<double*>(X);
+#pragma unroll
+    for (int t = 0; t < TG<NRB>::MAXBW; ++t) {
+        if (t < nbw) {
+            const int i = slot[t] >> 8, j = slot[t] & 0xff;
+            const int l = 4 * i + (r8 >> 1), p = r8 & 1;
+            const int m0 = 8 * j + 2 * c4;
+            if (l < L) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = m0 + h;
+                    if (m <= l) {
+                        double val = acc[t][h];
+                        if (Dd) {
+                            const size_t o = 2 * ((size_t)l * L + m) + p;
+                            val = fma(omr, Dd[o], val);
+                            Dd[o] = val;
+                        }
+                        Xd[2 * (l * ld + m) + p] = val;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Upper triangle by conjugation, sigma^2 on the (real) diagonal.
+__device__ __forceinline__ void finish_sigma(double2* X, int ld, int L, double s2) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < L * L; e += NT) {
+        const int i = e / L, j = e - i * L;
+        if (i < j) {
+            const double2 v = X[j * ld + i];
+            X[i * ld + j] = make_double2(v.x, -v.y);
+        } else if (i == j) {
+            X[i * ld + i] = make_double2(X[i * ld + i].x + s2, 0.0);
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// factor_pass: X holds Sigma (L x L Hermitian, row stride ld = LP + 1) on
+// entry.  Thread (ty, tx) = (tid/16, tid%16) owns the RT x RT entries
+// (ty + 16u, tx + 16v).  Gauss-Jordan sweep in registers (pivot row / column
+// ping-pong staged in SMEM, one barrier per pivot; pivots = LDL^H pivots),
+// symmetrisation (covlinalg.py:107, 112-114), trace(P Sigma_hat) when the
+// objective is recorded, G = Sigma_hat P and A = P^H G register-tiled, and
+// the packed P'/A' fragments written to od (SMEM or global).  Returns false
+// (uniformly) when a pivot is not positive.  Ends synchronised.
+// ---------------------------------------------------------------------------
+// Issue the cp.async copy of Sigma_hat (L x L, row stride ld) into Es.
+__device__ __forceinline__ void stage_emp(const FacArgs& a, int b, double2* Es, int ld) {
+    const double2* E = a.emp_cov + (size_t)b * a.L * a.L;
+    const int L = a.L;
+    for (int e = threadIdx.x; e < L * L; e += NT) {
+        const int i = e / L, j = e - i * L;
+        cp_async16(Es + i * ld + j, E + e, 16);
+    }
+    cp_async_commit();
+}
+
+template <int RT>
+__device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, int b, double2* X,
+                                            double2* G, double2* rowb, double2* colb,
+                                            const double2* Es, double* od, double* sred,
+                                            double& frob, double& logdet, double& trace) {
+    const int tid = threadIdx.x;
+    const int L = a.L, LP = geo.LP;
+    const int ld = LP + 1;
+    {
+        double s = 0.0;
+        for (int e = tid; e < L * L; e += NT) {
+            const int i = e / L, j = e - i * L;
+            const double2 v = X[i * ld + j];
+            s = fma(v.x, v.x, fma(v.y, v.y, s));
+        }
+        frob = sqrt(block_sum(s, sred));
+    }
+    const int ty = tid >> 4, tx = tid & 15;
+    double2 v[RT][RT];
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            v[u][w] = (i < L && j < L) ? X[i * ld + j] : make_double2(0.0, 0.0);
+        }
+    for (int e = tid; e < L; e += NT) {
+        rowb[e] = X[e];
+        colb[e] = X[e * ld];
+    }
+    __syncthreads();
+
+    logdet = 0.0;
+    bool ok = true;
+    const bool want_logdet = a.record_objective;
+    for (int k = 0; k < L; ++k) {
+        const double2* rk = rowb + (k & 1) * LP;
+        const double2* ck = colb + (k & 1) * LP;
+        double2* rn = rowb + ((k + 1) & 1) * LP;
+        double2* cn = colb + ((k + 1) & 1) * LP;
+        const double piv = rk[k].x;
+        if (!(piv > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (want_logdet) logdet += log(piv);
+        const double pinv = __drcp_rn(piv);
+        double2 cu[RT], rw[RT];
+#pragma unroll
+        for (int u = 0; u < RT; ++u) {
+            const int i = ty + 16 * u;
+            cu[u] = (i < L) ? ck[i] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int j = tx + 16 * w;
+            rw[w] = (j < L) ? rk[j] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < RT; ++u) {
+            const int i = ty + 16 * u;
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int j = tx + 16 * w;
+                // branch-free: general update, pivot row, pivot column, pivot
+                const double2 o = v[u][w];
+                const double2 pr = cmul(cu[u], rw[w]);
+                double nx = o.x - pr.x * pinv, ny = o.y - pr.y * pinv;
+                const double sx = o.x * pinv, sy = o.y * pinv;
+                nx = (j == k) ? -sx : nx;
+                ny = (j == k) ? -sy : ny;
+                nx = (i == k) ? ((j == k) ? pinv : sx) : nx;
+                ny = (i == k) ? ((j == k) ? 0.0 : sy) : ny;
+                const double2 nv = make_double2(nx, ny);
+                v[u][w] = nv;
+                if (i == k + 1 && j < L) rn[j] = nv;
+                if (j == k + 1 && i < L) cn[i] = nv;
+            }
+        }
+        __syncthreads();
+    }
+    if (!ok) {
+        __syncthreads();
+        return false;
+    }
+    // ---- P = (P + P^H)/2 -------------------------------------------------------
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
+        }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            if (i < L && j < L) {
+                const double2 t = X[j * ld + i];
+                v[u][w] = (i == j) ? make_double2(v[u][w].x, 0.0)
+                                   : make_double2(0.5 * (v[u][w].x + t.x), 0.5 * (v[u][w].y - t.y));
+            }
+        }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < RT; ++u)
+#pragma unroll
+        for (int w = 0; w < RT; ++w) {
+            const int i = ty + 16 * u, j = tx + 16 * w;
+            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
+        }
+    __syncthreads();
+
+    cp_async_wait<0>();   // Sigma_hat staged by the caller (stage_emp), if in SMEM
+    __syncthreads();
+    const double2* Eg = a.emp_cov + (size_t)b * L * L;   // used when Es == nullptr
+    trace = 0.0;
+    if (a.record_objective) {
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int i = ty + 16 * u, j = tx + 16 * w;
+                if (i < L && j < L) {
+                    const double2 ev = Es ? Es[j * ld + i] : __ldg(Eg + (size_t)j * L + i);
+                    s = fma(v[u][w].x, ev.x, fma(-v[u][w].y, ev.y, s));
+                }
+            }
+        trace = block_sum(s, sred);
+    }
+    // ---- G = Sigma_hat P ------------------------------------------------------
+    {
+        double2 gacc[RT][RT];
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) gacc[u][w] = make_double2(0.0, 0.0);
+        for (int c = 0; c < L; ++c) {
+            double2 eu[RT], xw[RT];
+#pragma unroll
+            for (int u = 0; u < RT; ++u) {
+                const int i = ty + 16 * u;
+                eu[u] = (i < L) ? (Es ? Es[i * ld + c] : __ldg(Eg + (size_t)i * L + c))
+                                : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int j = tx + 16 * w;
+                xw[w] = (j < LP) ? X[c * ld + j] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < RT; ++u)
+#pragma unroll
+                for (int w = 0; w < RT; ++w) gacc[u][w] = cfma(eu[u], xw[w], gacc[u][w]);
+        }
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int i = ty + 16 * u, j = tx + 16 * w;
+                if (i < LP && j < LP) G[i * ld + j] = gacc[u][w];
+            }
+    }
+    __syncthreads();
+    // ---- A = P^H G and the fragment pack ---------------------------------------
+    {
+        double2 aacc[RT][RT];
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) aacc[u][w] = make_double2(0.0, 0.0);
+        for (int t = 0; t < L; ++t) {
+            double2 pu[RT], gw[RT];
+#pragma unroll
+            for (int u = 0; u < RT; ++u) {
+                const int i = ty + 16 * u;
+                pu[u] = (i < LP) ? X[t * ld + i] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int j = tx + 16 * w;
+                gw[w] = (j < LP) ? G[t * ld + j] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < RT; ++u)
+#pragma unroll
+                for (int w = 0; w < RT; ++w) aacc[u][w] = cfma_conj_a(pu[u], gw[w], aacc[u][w]);
+        }
+#pragma unroll
+        for (int u = 0; u < RT; ++u)
+#pragma unroll
+            for (int w = 0; w < RT; ++w) {
+                const int l = ty + 16 * u, m = tx + 16 * w;
+                if (l < LP && m <= 4 * (l >> 2) + 3) {
+                    double2 pv = make_double2(0.0, 0.0), av = make_double2(0.0, 0.0);
+                    if (l < L && m <= l) {
+                        pv = X[l * ld + m];
+                        av = aacc[u][w];
+                        if (m < l) {
+                            pv.x *= 2.0; pv.y *= 2.0; av.x *= 2.0; av.y *= 2.0;
+                        } else {
+                            pv.y = 0.0; av.y = 0.0;
+                        }
+                    }
+                    const int i4 = l >> 2;
+                    const int blk = i4 * (i4 + 1) + (m >> 1);
+                    const int ent = (l & 3) * 2 + (m & 1);
+                    double* o = od + (size_t)blk * 32;
+                    o[2 * ent] = pv.x;
+                    o[2 * ent + 1] = pv.y;
+                    o[16 + 2 * ent] = av.x;
+                    o[16 + 2 * ent + 1] = av.y;
+                }
+            }
+    }
+    __syncthreads();
+    return true;
+}
+
+// ===========================================================================
+// two-kernel path
+// ===========================================================================
+template <int NRB>
+__global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColArgs a) {
+    using G = TG<NRB>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const size_t bN = (size_t)b * a.N;
+    const int n_begin = chunk * a.chunk_cols;
+    const int n_end = min(a.N, n_begin + a.chunk_cols);
+
+    if (a.status[b] != PSCA_RUNNING) {
+        for (int n = n_begin + tid; n < n_end; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
+        return;
+    }
+    double2* S0 = reinterpret_cast<double2*>(smem_raw);
+    double2* S1 = S0 + G::LP8 * NCT;
+    double2* WS = S1 + G::LP8 * NCT;
+    double2* SP = WS + G::LP8 * NCT;
+    double* FRs = reinterpret_cast<double*>(SP + G::LP8 * NCT);     // [NB][32] if staged
+    double* qr_s = FRs + (G::FR_SMEM ? G::NB * 32 : 0);             // [2][NCT][2]
+    const double* FR;
+    if (G::FR_SMEM) {   // stage the instance's packed P'/A' fragments (one cp.async group)
+        const double2* src = a.frags + (size_t)b * G::NB * 16;
+        double2* dst = reinterpret_cast<double2*>(FRs);
+        for (int e = tid; e < G::NB * 16; e += NT) cp_async16(dst + e, src + e, 16);
+        cp_async_commit();
+        FR = FRs;
+    } else {
+        FR = reinterpret_cast<const double*>(a.frags + (size_t)b * G::NB * 16);
+    }
+    int slot[G::MAXBW];
+    int nbw;
+    rebuild_slots<NRB>(slot, nbw);
+    double acc[G::MAXBW][2];
+    double dx2, minq;
+    col_pass<NRB>(a, b, a.k, a.x_cur + bN, a.x_next + bN, n_begin, n_end, S0, S1, WS, SP, FR,
+                  qr_s, acc, slot, nbw, dx2, minq);
+
+    {
+        double2* sp = a.sig_part + ((size_t)b * a.n_chunks + chunk) * G::NBLK * 32;
+        int idx = 0, t2 = 0;
+        for (int i = 0; i < NRB; ++i) {
+            const int jmax = (4 * i + 3) / 8;
+            for (int j = 0; j <= jmax; ++j, ++idx) {
+                if ((idx % NWARP) == warp) {
+#pragma unroll
+                    for (int u = 0; u < G::MAXBW; ++u)
+                        if (u == t2) sp[(size_t)idx * 32 + lane] = make_double2(acc[u][0], acc[u][1]);
+                    ++t2;
+                }
+            }
+        }
+    }
+    reduce_pass_partials(dx2, minq);
+    if (tid == 0) {
+        double* rp = a.red_part + ((size_t)b * a.n_chunks + chunk) * 4;
+        rp[0] = dx2;
+        rp[1] = minq;
+        rp[2] = 0.0;
+        rp[3] = 0.0;
+    }
+}
+
+template <int RT>
+__global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double sred[NWARP + 1];
+    __shared__ int s_flag;
+    const Geo geo = make_geo(a.L, a.nrb);
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int LP = geo.LP;
+    const int ld = LP + 1;
+    if (a.status[b] != PSCA_RUNNING) return;
+    if (a.k_new > 0) {
+        if (fac_finalize(a, b, &s_flag)) return;
+    }
+    const double prior_value = fac_prior_terms(a, b, sred);
+    double2* sm = reinterpret_cast<double2*>(smem_raw);
+    double2* rowb = sm;             // [2][LP]
+    double2* colb = sm + 2 * LP;    // [2][LP]
+    double2* X = sm + 4 * LP;       // [LP][ld]
+    double2* G = X + (size_t)LP * ld;
+    // Sigma_hat in SMEM when three L x L buffers fit (L <= 64), else read from L2
+    double2* Es = ((size_t)4 * LP * 16 + (size_t)3 * LP * ld * 16 <= 227 * 1024)
+                      ? G + (size_t)LP * ld : nullptr;
+    if (Es) stage_emp(a, b, Es, ld);
+    assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
+    double frob, logdet, trace;
+    double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 16);
+    if (!factor_pass<RT>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet, trace)) {
+        if (tid == 0) {
+            a.status[b] = PSCA_CHOL_FAIL;
+            if (a.cond_est) a.cond_est[b] = INFINITY;
+        }
+        return;
+    }
+    if (tid == 0) {
+        double* in = a.inst + (size_t)b * 4;
+        in[0] = frob;
+        in[1] = logdet;
+        in[2] = trace;
+        in[3] = prior_value;
+    }
+}
+
+// ===========================================================================
+// persistent path: one launch for the whole solve
+// ===========================================================================
+template <int NRB>
+__global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs fa, int* counter) {
+    using G = TG<NRB>;
+    constexpr int RT = G::RT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double sred[NWARP + 1];
+    __shared__ double s_inst[4];
+    __shared__ int s_b, s_flag;
+    const Geo geo = make_geo(fa.L, fa.nrb);
+    const int tid = threadIdx.x;
+    const int L = fa.L, LP = geo.LP, ld = LP + 1;
+
+    double* FR = reinterpret_cast<double*>(smem_raw);                      // [NB][32]
+    unsigned char* U = smem_raw + G::F_BYTES;                                 // union
+    double2* S0 = reinterpret_cast<double2*>(U);
+    double2* S1 = S0 + G::LP8 * NCT;
+    double2* WS = S1 + G::LP8 * NCT;
+    double2* SP = WS + G::LP8 * NCT;
+    double2* rowb = reinterpret_cast<double2*>(U);
+    double2* colb = rowb + 2 * LP;
+    double2* X = rowb + 4 * LP;
+    double2* Gm = X + (size_t)LP * ld;
+    double2* Es = Gm + (size_t)LP * ld;
+    double* qr_s = reinterpret_cast<double*>(U + G::UNION);
+
+    int slot[G::MAXBW];
+    int nbw;
+    rebuild_slots<NRB>(slot, nbw);
+
+    for (;;) {
+        if (tid == 0) s_b = atomicAdd(counter, 1);
+        __syncthreads();
+        const int b = s_b;
+        if (b >= fa.B) break;
+        const size_t bN = (size_t)b * fa.N;
+        double* xc = const_cast<double*>(fa.x_cur) + bN;   // x_out slice (zeroed by psca_solve)
+        double* xn = fa.x_next + bN;  // workspace slice
+        double* final_x = xc;
+
+        // ---- iterate 0: prior terms at x = 0, Sigma_0 = sigma^2 I, D_0 = 0 --
+        stage_emp(fa, b, Es, ld);
+        if (fa.incremental) {
+            double2* D = fa.dmat + (size_t)b * L * L;
+            for (int e = tid; e < L * L; e += NT) D[e] = make_double2(0.0, 0.0);
+        }
+        double pv = fac_prior_terms_at(fa, b, xc, sred);
+        {
+            const double s2 = fa.noise[b];
+            for (int e = tid; e < L * L; e += NT) {
+                const int i = e / L, j = e - i * L;
+                X[i * ld + j] = make_double2(i == j ? s2 : 0.0, 0.0);
+            }
+            __syncthreads();
+        }
+        double frob, logdet, trace;
+        bool ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, FR, sred, frob, logdet, trace);
+        if (!ok) {
+            if (tid == 0) {
+                fa.status[b] = PSCA_CHOL_FAIL;
+                if (fa.cond_est) fa.cond_est[b] = INFINITY;
+            }
+        } else {
+            if (tid == 0) {
+                s_inst[0] = frob; s_inst[1] = logdet; s_inst[2] = trace; s_inst[3] = pv;
+            }
+            for (int k = 0; k < fa.T; ++k) {
+                double acc[G::MAXBW][2];
+                double dx2, minq;
+                col_pass<NRB>(ca, b, k, xc, xn, 0, fa.N, S0, S1, WS, SP, FR, qr_s, acc, slot,
+                              nbw, dx2, minq);
+                reduce_pass_partials(dx2, minq);
+                if (tid == 0) s_flag = fac_finalize_core(fa, b, k, dx2, minq, s_inst);
+                __syncthreads();
+                const int flag = s_flag;
+                if (flag == PSCA_QFLOOR) { final_x = xc; break; }
+                final_x = xn;
+                if (flag == PSCA_CONVERGED || k + 1 == fa.T) break;
+                // ---- factorisation at x_{k+1} ---------------------------------
+                stage_emp(fa, b, Es, ld);
+                pv = fac_prior_terms_at(fa, b, xn, sred);
+                acc_to_sigma<NRB>(acc, slot, nbw, X, ld, L,
+                                  fa.incremental ? reinterpret_cast<double*>(fa.dmat + (size_t)b * L * L)
+                                                 : nullptr,
+                                  __dsub_rn(1.0, fa.steps[k]));
+                finish_sigma(X, ld, L, fa.noise[b]);
+                ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, FR, sred, frob, logdet, trace);
+                if (!ok) {
+                    if (tid == 0) {
+                        fa.status[b] = PSCA_CHOL_FAIL;
+                        if (fa.cond_est) fa.cond_est[b] = INFINITY;
+                    }
+                    break;
+                }
+                if (tid == 0) {
+                    s_inst[0] = frob; s_inst[1] = logdet; s_inst[2] = trace; s_inst[3] = pv;
+                }
+                double* tsw = xc; xc = xn; xn = tsw;
+            }
+        }
+        if (final_x != fa.x_cur + bN) {
+            double* out = const_cast<double*>(fa.x_cur) + bN;
+            for (int n = tid; n < fa.N; n += NT) out[n] = final_x[n];
+        }
+        __syncthreads();
+    }
+}

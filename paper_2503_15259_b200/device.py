@@ -51,7 +51,9 @@ class SolveArgsC(ctypes.Structure):
 # exported symbols and their signatures (must match include/psca.h)
 _SIGS = {
     "psca_version": (ctypes.c_char_p, []),
+    "psca_last_error": (ctypes.c_char_p, []),
     "psca_last_launch_count": (ctypes.c_int, []),
+    "psca_last_path": (ctypes.c_int, []),
     "psca_profile_begin": (ctypes.c_int, []),
     "psca_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
@@ -113,7 +115,10 @@ def _check(rc: int, what: str):
     if rc != 0:
         names = {-1: "bad argument", -2: "CUDA error", -3: "workspace too small",
                  -4: "unsupported shape"}
-        raise PscaNativeError(f"{what} failed: {names.get(rc, rc)}")
+        detail = ""
+        if rc == -2 and _lib is not None:
+            detail = f" ({_lib.psca_last_error().decode()})"
+        raise PscaNativeError(f"{what} failed: {names.get(rc, rc)}{detail}")
 
 
 def _stream(torch):
@@ -215,7 +220,8 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
                           _stream(torch)), "psca_solve")
     return {"x": x, "update_norm": un[:, :T], "objective": obj[:, :T] if obj is not None else None,
             "iterates": its, "status": status, "n_iter": n_iter, "cond_est": cond, "_ws": ws,
-            "launches": lib.psca_last_launch_count()}
+            "launches": lib.psca_last_launch_count(),
+            "path": "persistent" if lib.psca_last_path() == 1 else "two-kernel"}
 
 
 # ---------------------------------------------------------------------------

@@ -30,9 +30,11 @@ for L, kind in ((40, "ml-ud"), (33, "map-k"), (20, "map-ur"), (52, "ml-k"), (72,
     ss = [scenes.make_scene(cfg, i) for i in range(3)]
     b = scenes.stack_batch(ss)
     res = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"], b["noise"],
-                                    64, gains=b["gains"], max_iter=25, record_objective=True)
-    out[f"{L}-{kind}"] = {"x": res["x"].cpu().numpy().tolist(),
-                          "obj": res["objective"].cpu().numpy().tolist()}
+                                    64, gains=b["gains"], max_iter=25, record_objective=True,
+                                    n_chunks=1)
+    out[f"{L}-{kind}"] = {"x": res["x"].cpu().numpy().tolist(), "path": res["path"],
+                          "obj": res["objective"].cpu().numpy().tolist(),
+                          "un": res["update_norm"].cpu().numpy().tolist()}
 print(json.dumps(out))
 """
 
@@ -53,3 +55,16 @@ def test_generic_and_compiled_kernels_agree(cuda_device):
         tol = 1e-9 if "map-ur" not in key else 1e-7
         assert max_rel(xf, xs) <= tol, key
         assert max_rel(np.array(fast[key]["obj"]), np.array(slow[key]["obj"])) <= 1e-10, key
+
+
+def test_persistent_equals_two_kernel_bitwise(cuda_device):
+    """One chunk per instance: the persistent kernel and the two-kernel path run the
+    same device functions in the same order, so the results are bit-identical."""
+    pers = run_script({})
+    two = run_script({"PSCA_NO_PERSISTENT": "1"})
+    assert any(v["path"] == "persistent" for v in pers.values())
+    assert all(v["path"] == "two-kernel" for v in two.values())
+    for key in pers:
+        for field in ("x", "obj", "un"):
+            np.testing.assert_array_equal(np.array(pers[key][field]), np.array(two[key][field]),
+                                          err_msg=f"{key} {field}")
