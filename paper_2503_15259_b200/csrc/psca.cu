@@ -171,13 +171,16 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
 __device__ __forceinline__ double comp(double2 v, int c) { return c ? v.y : v.x; }
 
 // lane -> packed P'/A' fragment entry (see pack_frags)
-__device__ __forceinline__ int frag_lane_offset(int lane) {
+// Fragment block = 24 double2 (P', A') slots: entry e (0..7) x variant
+// (0: re, 1: im, 2: -im).  Lane (r,c) of the DMMA A fragment needs entry
+// e = 2*(r>>1) + (c>>1) of the real 2x2 expansion [[re,-im],[im,re]]:
+// (r&1, c&1) = (0,0)/(1,1) -> re, (1,0) -> im, (0,1) -> -im.
+constexpr int FRAG_SLOTS = 24;
+__device__ __forceinline__ int frag_lane_slot(int lane) {
     const int r8 = lane >> 2, c4 = lane & 3;
-    return 2 * (2 * (r8 >> 1) + (c4 >> 1)) + ((r8 & 1) ^ (c4 & 1));
-}
-__device__ __forceinline__ unsigned long long frag_lane_sign(int lane) {
-    const int r8 = lane >> 2, c4 = lane & 3;
-    return ((r8 & 1) == 0 && (c4 & 1) == 1) ? 0x8000000000000000ull : 0ull;
+    const int p = r8 & 1, q = c4 & 1;
+    const int var = (p == q) ? 0 : (p ? 1 : 2);
+    return 3 * (2 * (r8 >> 1) + (c4 >> 1)) + var;
 }
 __device__ __forceinline__ double xsign(double v, unsigned long long m) {
     return __longlong_as_double(__double_as_longlong(v) ^ m);
@@ -247,6 +250,7 @@ enum ColMode { COL_SOLVE = 0, COL_QUAD = 1, COL_REBUILD = 2 };
 struct ColArgs {
     int kind, B, N, L, nrb, n_chunks, chunk_cols, k, T, n_antennas, record_objective;
     int incremental;            // 1: rebuild the increment S diag(rho cand g) S^H only
+    int dbg_delay_ns;           // experiment: odd instances start this much later
     const double2* pilots;      // [B][L][N]
     const double* gains;        // [B][N]
     const double* x_cur;        // [B][N]
@@ -304,9 +308,8 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
     double* wv_s = qr_s + 2 * NCT * 2;                              // [NCT]
 
     const double2* sb = a.pilots + (size_t)b * a.L * a.N;
-    const double* frd = reinterpret_cast<const double*>(a.frags) + (size_t)b * geo.NB * 32;
-    const int foff = frag_lane_offset(lane);
-    const unsigned long long fsgn = frag_lane_sign(lane);
+    const double2* frd = a.frags + (size_t)b * geo.NB * FRAG_SLOTS;
+    const int fslot = frag_lane_slot(lane);
 
     // ---- static work split -------------------------------------------------
     // quad forms: warp -> (column block, row-block half); halves balanced by a
@@ -374,12 +377,12 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
             for (int i = 0; i < geo.NRB; ++i) {
                 if (!((rowmask >> i) & 1ull)) continue;
                 double tp[2] = {0.0, 0.0}, ta[2] = {0.0, 0.0};
-                const double* f = frd + (size_t)(i * (i + 1)) * 32 + foff;
+                const double2* f = frd + (size_t)(i * (i + 1)) * FRAG_SLOTS + fslot;
                 const int nk = 2 * (i + 1);
 #pragma unroll 4
                 for (int kk = 0; kk < nk; ++kk) {
-                    const double pv = xsign(__ldg(f + kk * 32), fsgn);
-                    const double av = xsign(__ldg(f + kk * 32 + 16), fsgn);
+                    const double2 pa = __ldg(f + kk * FRAG_SLOTS);
+                    const double pv = pa.x, av = pa.y;
                     int m = 2 * kk + (c4 >> 1);
                     double bv = Sd[2 * tile_idx(m, nb_col) + (c4 & 1)];
                     dmma(tp, pv, bv);
@@ -652,12 +655,12 @@ __device__ void gemm_EX(const double2* __restrict__ E, const double2* X, int ld,
 
 // Pack P' (from X) and A' = P^H G for the quad-form DMMAs.  Fragment block
 // (i,kk) covers complex rows l = 4i..4i+3 and cols m = 2kk..2kk+1 and is stored
-// as 32 doubles: the 8 complex P' entries (e = 2*(l-4i) + (m-2kk)), then the
-// 8 complex A' entries.  Off-diagonal entries are doubled (lower-triangle
+// as 24 double2 (P', A') slots: entry e = 2*(l-4i) + (m-2kk), variants re, im,
+// -im (one LDS.128 gives a lane both of its DMMA operands).  Off-diagonal entries are doubled (lower-triangle
 // quadratic form), diagonal entries real, strictly upper / padded entries 0.
 // Lane (r,c) of the DMMA A fragment reads entry e = 2*(r>>1) + (c>>1),
 // component (r&1)^(c&1), negated when (r&1)==0 && (c&1)==1 -- the real 2x2
-// expansion [[re,-im],[im,re]] (see frag_lane_offset / frag_lane_sign).
+// expansion [[re,-im],[im,re]] (see frag_lane_slot).
 __device__ void pack_frags(const double2* X, const double2* G, int ld, int L, const Geo& geo,
                            double2* __restrict__ out) {
     double* od = reinterpret_cast<double*>(out);
@@ -681,11 +684,10 @@ __device__ void pack_frags(const double2* X, const double2* G, int ld, int L, co
             }
         }
         const int ent = a4 * 2 + cc;
-        double* o = od + (size_t)blk * 32;
-        o[2 * ent] = pv.x;
-        o[2 * ent + 1] = pv.y;
-        o[16 + 2 * ent] = av.x;
-        o[16 + 2 * ent + 1] = av.y;
+        double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
+        o[0] = pv.x; o[1] = av.x;
+        o[2] = pv.y; o[3] = av.y;
+        o[4] = -pv.y; o[5] = -av.y;
     }
 }
 
@@ -977,7 +979,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
     // FAC_PREP (quad_forms drop-in, P given by the caller): A' = P^H E P is
     // packed from the raw P; the P' half is then replaced by (P + P^H)/2,
     // which leaves q = Re s^H P s unchanged for any P.
-    pack_frags(X, G, ld, L, geo, a.frags + (size_t)b * geo.NB * 16);
+    pack_frags(X, G, ld, L, geo, a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
     if (MODE == FAC_PREP) {
         __syncthreads();
         // overwrite the P' halves with the symmetrised P (exact for q)
@@ -989,7 +991,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
             }
         }
         __syncthreads();
-        double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 16);
+        double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
         const int total = geo.NB * 8;
         for (int e = tid; e < total; e += NT) {
             int blk = e >> 3, a4 = (e >> 1) & 3, cc = e & 1;
@@ -1006,8 +1008,8 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
                 pv = make_double2(X[l * ld + l].x, 0.0);
             }
             const int ent = a4 * 2 + cc;
-            od[(size_t)blk * 32 + 2 * ent] = pv.x;
-            od[(size_t)blk * 32 + 2 * ent + 1] = pv.y;
+            double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
+            o[0] = pv.x; o[2] = pv.y; o[4] = -pv.y;
         }
     }
 }
@@ -1219,10 +1221,12 @@ cudaError_t launch_solve_factor(const FacArgs& fa, const Geo& g, cudaStream_t st
 
 thread_local int g_last_path = 0;   // 0 two-kernel, 1 persistent
 
+// The persistent fused kernel is opt-in (PSCA_PERSISTENT=1): measured slower
+// than the two-kernel path on B200 (profiles/README.md, round 1).
 bool persistent_disabled() {
     static const bool off = [] {
-        const char* e = getenv("PSCA_NO_PERSISTENT");
-        return e && e[0] == '1';
+        const char* e = getenv("PSCA_PERSISTENT");
+        return !(e && e[0] == '1');
     }();
     return off;
 }
@@ -1309,7 +1313,7 @@ struct SolveLayout {
 SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, void* ws) {
     Carve cv{static_cast<char*>(ws)};
     SolveLayout s;
-    s.frags = cv.take<double2>((size_t)a->B * g.NB * 256);
+    s.frags = cv.take<double2>((size_t)a->B * g.NB * FRAG_SLOTS * 16);
     s.sig_part = cv.take<double2>((size_t)a->B * n_chunks * g.NBLK * 32 * 16);
     s.red_part = cv.take<double>((size_t)a->B * n_chunks * 4 * 8);
     s.x_alt = cv.take<double>((size_t)a->B * a->N * 8);
@@ -1428,6 +1432,10 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
                           (g.NRB == 2 || g.NRB == 3 || g.NRB == 4 || g.NRB == 5 || g.NRB == 6 ||
                            g.NRB == 8 || g.NRB == 10 || g.NRB == 12 || g.NRB == 16 || g.NRB == 20);
     ca.incremental = (fast_col && !full_rebuild_forced()) ? 1 : 0;
+    {
+        const char* e = getenv("PSCA_DBG_DELAY_NS");
+        ca.dbg_delay_ns = e ? atoi(e) : 0;
+    }
 
     FacArgs fa{};
     fa.B = a->B; fa.N = a->N; fa.L = a->L; fa.nrb = g.NRB; fa.T = a->max_iter;
@@ -1551,7 +1559,7 @@ size_t psca_quad_workspace_bytes(int B, int N, int L) {
     if (B < 0 || N < 1 || L < 1 || L > MAX_L_TILE) return 0;
     Geo g = make_geo(L);
     Carve cv{nullptr};
-    cv.take<double2>((size_t)B * g.NB * 256);
+    cv.take<double2>((size_t)B * g.NB * FRAG_SLOTS * 16);
     cv.take<double2>(fac_scratch_bytes(g, B));
     return cv.off;
 }
@@ -1568,7 +1576,7 @@ int psca_quad_forms(const double* pilots, const double* sigma_inv, const double*
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Geo g = make_geo(L);
     Carve cv{static_cast<char*>(workspace)};
-    double2* frags = cv.take<double2>((size_t)B * g.NB * 256);
+    double2* frags = cv.take<double2>((size_t)B * g.NB * FRAG_SLOTS * 16);
     double2* scratch = cv.take<double2>(fac_scratch_bytes(g, B));
     FacArgs fa{};
     fa.B = B; fa.L = L; fa.nrb = g.NRB; fa.in_mat = reinterpret_cast<const double2*>(sigma_inv);

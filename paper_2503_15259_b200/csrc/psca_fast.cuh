@@ -30,15 +30,18 @@ struct TG {
     static constexpr int MAXBW = (NBLK + NWARP - 1) / NWARP;
     static constexpr int RPT = LP8 / 8;            // tile rows per warp (copy / WS build)
     static constexpr int RT = (LP + 15) / 16;       // factor register tile
+    static constexpr int WCAP = 16;                 // packed rebuild slots per round
     static constexpr size_t S_BYTES = (size_t)LP8 * NCT * 16;
-    static constexpr size_t F_BYTES = (size_t)NB * 256;
+    static constexpr size_t W_BYTES = (size_t)LP8 * WCAP * 16;
+    static constexpr size_t F_BYTES = (size_t)NB * FRAG_SLOTS * 16;
     static constexpr size_t SMALL = 2 * NCT * 2 * 8 + NWARP * 4 * 8;
-    // fragments staged in SMEM when they fit beside the four tile buffers
-    // (NRB <= 16); otherwise col_pass reads them through L1 from global
-    static constexpr bool FR_SMEM = 4 * S_BYTES + F_BYTES + SMALL <= 227 * 1024;
-    static constexpr size_t COL_SMEM = 4 * S_BYTES + (FR_SMEM ? F_BYTES : 0) + SMALL;
+    static constexpr size_t TILE_BYTES = 2 * S_BYTES + 2 * W_BYTES;
+    // fragments staged in SMEM when they fit beside the tile buffers (NRB <= 16);
+    // otherwise col_pass reads them through L1 from global
+    static constexpr bool FR_SMEM = TILE_BYTES + F_BYTES + SMALL <= 227 * 1024;
+    static constexpr size_t COL_SMEM = TILE_BYTES + (FR_SMEM ? F_BYTES : 0) + SMALL;
     static constexpr size_t FAC_BYTES = (size_t)4 * LP * 16 + (size_t)3 * LP * (LP + 1) * 16;
-    static constexpr size_t UNION = (4 * S_BYTES > FAC_BYTES) ? 4 * S_BYTES : FAC_BYTES;
+    static constexpr size_t UNION = (TILE_BYTES > FAC_BYTES) ? TILE_BYTES : FAC_BYTES;
     static constexpr size_t PERSIST_SMEM = F_BYTES + UNION + SMALL;
 };
 
@@ -66,28 +69,39 @@ __device__ __forceinline__ void rebuild_slots(int (&slot)[TG<NRB>::MAXBW], int& 
 // ---------------------------------------------------------------------------
 // col_pass: one PSCA column pass (estimators.py:262-276 for columns
 // [n_begin, n_end)) of instance b at iteration k.
-//   FR    packed P'/A' fragments in SMEM (pack_frags layout)
-//   S0/S1 tile double buffer, WS = S diag(w_new) (all SMEM, swizzled rows)
-// Per 32-column tile:
-//   [cp.async prefetch of tile t+1; x, g of tile t into registers]
-//   quad forms    warp -> (8-column block, row-block half); B fragments of the
-//                 column block in registers; 4 independent DMMA chains
+//   FR    P'/A' fragments (SMEM or global), FRAG_SLOTS double2 per block
+//   S0/S1 tile double buffer (swizzled rows of 32 columns)
+//   WS/SP packed rebuild operands: S diag(v) and S for the columns with v != 0
+// Software pipeline over 32-column tiles, two barriers per tile:
+//   [barrier; cp.async prefetch of tile t+1]
+//   phase A(t)  quad forms of tile t (warp -> 8-column block x row-block half,
+//               B fragments in registers, 4 DMMA chains) and the deferred
+//               rebuild of tile t-1 over its packed slots (warp -> its lower
+//               C blocks) -- both pure DMMA work on disjoint buffers
 //   sync
-//   update + WS   warp w builds rows w, w+8, ... of WS for the 32 columns
-//                 (lane = column); the per-device update is computed by every
-//                 warp with identical arithmetic, warp 0 stores x_next
+//   phase B(t)  per-device update of tile t (every warp, lane = column; warp 0
+//               stores), ballot-compaction of the moving columns into WS/SP,
+//               then S(t)'s buffer is refilled with tile t+2
 //   sync
-//   rebuild       warp -> its lower-triangle C blocks, 4 DMMA chains each
-// On return acc holds this pass's rebuild C fragments and warp 0 holds the
-// per-lane partial sum of (x_next - x)^2 and min q; all cp.async groups are
-// retired and the CTA is synchronised.
+// v = w_new (full rebuild) or rho * cand * g (incremental: the increment of
+// D = Sigma - sigma^2 I).  On return acc holds the pass's rebuild C fragments,
+// warp 0 holds the per-lane partial sum of (x_next - x)^2 and min q, all
+// cp.async groups are retired and the CTA is synchronised.
 // ---------------------------------------------------------------------------
+#ifndef PSCA_QCH
+#define PSCA_QCH 1
+#endif
+#ifndef PSCA_BQREG
+#define PSCA_BQREG 0
+#endif
+constexpr int QCH = PSCA_QCH;   // independent DMMA chains per matrix in the quad stage
+
 template <int NRB>
 __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
                                          const double* __restrict__ x_cur,
                                          double* __restrict__ x_next, int n_begin, int n_end,
                                          double2* S0, double2* S1, double2* WS, double2* SP,
-                                         const double* FR,
+                                         const double2* FR,
                                          double* qr_s, double (&acc)[TG<NRB>::MAXBW][2],
                                          const int (&slot)[TG<NRB>::MAXBW], int nbw,
                                          double& p_dx2, double& p_minq) {
@@ -125,19 +139,19 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         for (int j = 0; j < 2; ++j)
             epoff[j] = 2 * ((r8 >> 1) * NCT + cb * 8 + ((2 * c4 + j) ^ se)) + (r8 & 1);
     }
-    const int foff = frag_lane_offset(lane);
-    const unsigned long long fsgn = frag_lane_sign(lane);
-    // rebuild fragments, k-step k2 = 4 g + h:
-    //   A (WS):  l = 4i + (r8>>1), n = 2 k2 + (c4>>1), component p^q, sign p&q
-    //            n ^ swz(l) = 8 g + 2 (h ^ sa) + (c4>>1)
-    //   B (S):   m = 8j + r8,      n = 2 k2 + (c4>>1), component q
-    //            n ^ swz(m) = 8 g + 2 (h ^ sbb) + (c4>>1)
+    const int fslot = frag_lane_slot(lane);
+    // rebuild fragments over the packed slots (WS / SP rows of WCAP = 16 slots,
+    // slot swizzle 2*(row & 3)), k-step k2 = 4 g + h, slot n = 2 k2 + (c4>>1):
+    //   A (WS):  l = 4i + (r8>>1), component p^q, sign p&q
+    //            n ^ 2(l&3) = 8 g + 2 (h ^ sa) + (c4>>1),  sa = r8>>1
+    //   B (SP):  m = 8j + r8, component q
+    //            n ^ 2(m&3) = 8 g + 2 (h ^ sbb) + (c4>>1), sbb = r8&3
     int wa_lane[4], b_lane[4];
     unsigned long long wsgn;
     {
         const int p = r8 & 1, q = c4 & 1, cpr = c4 >> 1;
-        const int sa = swz(r8 >> 1) >> 1;
-        const int sbb = swz(r8) >> 1;
+        const int sa = r8 >> 1;
+        const int sbb = r8 & 3;
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             wa_lane[h] = 4 * (h ^ sa) + 2 * cpr + (p ^ q);
@@ -168,14 +182,43 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         cp_async_commit();
     };
 
+    // rebuild over packed slots [0, cnt) of WS / SP (warp -> its lower C blocks)
+    auto rebuild = [&](int cnt) {
+        const double* Wd = reinterpret_cast<const double*>(WS);
+        const double* Pd = reinterpret_cast<const double*>(SP);
+        const int nk2 = (cnt + 1) >> 1;
+#pragma unroll
+        for (int t2 = 0; t2 < G::MAXBW; ++t2) {
+            if (t2 < nbw) {
+                const int bi = slot[t2] >> 8, bj = slot[t2] & 0xff;
+                const int abase = 2 * (4 * bi + (r8 >> 1)) * G::WCAP;
+                const int bbase = 2 * (8 * bj + r8) * G::WCAP;
+                double e1[2] = {0.0, 0.0};
+#pragma unroll
+                for (int k2 = 0; k2 < G::WCAP / 2; ++k2) {
+                    if (k2 < nk2) {
+                        const int h = k2 & 3, g8 = 16 * (k2 >> 2);
+                        const double av = xsign(Wd[abase + wa_lane[h] + g8], wsgn);
+                        const double bv = Pd[bbase + b_lane[h] + g8];
+                        if (k2 & 1) dmma(e1, av, bv);
+                        else dmma(acc[t2], av, bv);
+                    }
+                }
+                acc[t2][0] += e1[0];
+                acc[t2][1] += e1[1];
+            }
+        }
+    };
+
     const int ntiles = (n_end - n_begin + NCT - 1) / NCT;
     if (ntiles > 0) issue_tile(S0, n_begin);
+    int pend = 0;   // packed slots of the previous tile awaiting their rebuild
 
     for (int t = 0; t < ntiles; ++t) {
         double2* S = (t & 1) ? S1 : S0;
         const double* Sd = reinterpret_cast<const double*>(S);
         const int col0 = n_begin + t * NCT;
-        // per-device operands of this tile (lane = column), latency hidden by the quad stage
+        // per-device operands of this tile (lane = column), latency hidden by phase A
         const int ncol = col0 + lane;
         const bool cvalid = ncol < n_end;
         double x = 0.0, g = 1.0, pg = 0.0;
@@ -187,38 +230,46 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         }
         cp_async_wait<0>();
         __syncthreads();
+        // prefetch tile t+1 into the other buffer (its tile t-1 was consumed in B(t-1))
         if (t + 1 < ntiles) issue_tile((t & 1) ? S0 : S1, col0 + NCT);
 
-        // ---- quadratic forms ---------------------------------------------
+        // ---- phase A: deferred rebuild of tile t-1, quad forms of tile t -----
+        if (pend > 0) rebuild(pend);
         {
+#if PSCA_BQREG
             double bq[2 * NRB];
 #pragma unroll
             for (int kk = 0; kk < 2 * NRB; ++kk) bq[kk] = Sd[qoff[kk & 1] + kk * 4 * NCT];
+#define PSCA_BQ(kk) bq[kk]
+#else
+#define PSCA_BQ(kk) Sd[qoff[(kk) & 1] + (kk) * 4 * NCT]
+#endif
             double qa0 = 0.0, qa1 = 0.0, ra0 = 0.0, ra1 = 0.0;
 #pragma unroll
             for (int i = 0; i < NRB; ++i) {
                 if ((rowmask >> i) & 1ull) {
-                    double t0[2] = {0.0, 0.0}, t1[2] = {0.0, 0.0};
-                    double u0[2] = {0.0, 0.0}, u1[2] = {0.0, 0.0};
-                    const double* f = FR + i * (i + 1) * 32 + foff;
+                    double tc[QCH][2], uc[QCH][2];
+#pragma unroll
+                    for (int c = 0; c < QCH; ++c) tc[c][0] = tc[c][1] = uc[c][0] = uc[c][1] = 0.0;
+                    const double2* f = FR + i * (i + 1) * FRAG_SLOTS + fslot;
 #pragma unroll
                     for (int kk = 0; kk < 2 * (i + 1); ++kk) {
-                        const double pv = xsign(f[kk * 32], fsgn);
-                        const double av = xsign(f[kk * 32 + 16], fsgn);
-                        if (kk & 1) {
-                            dmma(t1, pv, bq[kk]);
-                            dmma(u1, av, bq[kk]);
-                        } else {
-                            dmma(t0, pv, bq[kk]);
-                            dmma(u0, av, bq[kk]);
-                        }
+                        const double2 pa = f[kk * FRAG_SLOTS];
+                        const double bv = PSCA_BQ(kk);
+                        dmma(tc[kk % QCH], pa.x, bv);
+                        dmma(uc[kk % QCH], pa.y, bv);
+                    }
+#pragma unroll
+                    for (int c = 1; c < QCH; ++c) {
+                        tc[0][0] += tc[c][0]; tc[0][1] += tc[c][1];
+                        uc[0][0] += uc[c][0]; uc[0][1] += uc[c][1];
                     }
                     const double s0 = Sd[epoff[0] + i * 8 * NCT];
                     const double s1 = Sd[epoff[1] + i * 8 * NCT];
-                    qa0 = fma(s0, t0[0] + t1[0], qa0);
-                    qa1 = fma(s1, t0[1] + t1[1], qa1);
-                    ra0 = fma(s0, u0[0] + u1[0], ra0);
-                    ra1 = fma(s1, u0[1] + u1[1], ra1);
+                    qa0 = fma(s0, tc[0][0], qa0);
+                    qa1 = fma(s1, tc[0][1], qa1);
+                    ra0 = fma(s0, uc[0][0], ra0);
+                    ra1 = fma(s1, uc[0][1], ra1);
                 }
             }
 #pragma unroll
@@ -239,12 +290,7 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         }
         __syncthreads();
 
-        // ---- update (estimators.py:272-276) + packed rebuild operands ---------
-        // v = w_new (full rebuild) or rho * cand * g (incremental: the increment
-        // of D = Sigma - sigma^2 I); the nonzero-v columns are compacted (ballot,
-        // identical in every warp) into slots 0..nnz-1 of WS = S diag(v) and of
-        // SP = S, so the rebuild runs over ceil(nnz/2) k-steps only.
-        int nnz;
+        // ---- phase B: update (estimators.py:272-276) + packed WS / SP --------
         {
             double v = 0.0;
             if (cvalid) {
@@ -273,66 +319,42 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
                 }
             }
             const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
-            nnz = __popc(mask);
+            const int nnz = __popc(mask);
             const int pos = __popc(mask & ((1u << lane) - 1u));
-            const bool pad = (lane == nnz) && (nnz & 1);     // zero slot after an odd count
+            const int sw = 2 * (warp & 3);
+            // WCAP slots per round; a tile with more than 16 moving columns
+            // (early iterations only) rebuilds its first 16 here, the rest in A(t+1)
+            int lo = 0;
+            for (;;) {
+                const int cnt = min(nnz - lo, G::WCAP);
 #pragma unroll
-            for (int s2 = 0; s2 < G::RPT; ++s2) {
-                const int l = warp + 8 * s2;
-                const int sw = swz(warp);
-                if (v != 0.0) {
-                    const double2 sv = S[cp_dst + s2 * 8 * NCT];
-                    const int o = l * NCT + (pos ^ sw);
-                    WS[o] = make_double2(v * sv.x, v * sv.y);
-                    SP[o] = sv;
-                }
-                if (pad) {
-                    const int o = l * NCT + (nnz ^ sw);
-                    WS[o] = make_double2(0.0, 0.0);
-                    SP[o] = make_double2(0.0, 0.0);
-                }
-            }
-        }
-        __syncthreads();
-
-        // ---- rebuild: += WS SP^H over the packed slots (lower C blocks) -------
-        if (nnz > 0) {
-            const double* Wd = reinterpret_cast<const double*>(WS);
-            const double* Pd = reinterpret_cast<const double*>(SP);
-            const int nk2 = (nnz + 1) >> 1;
-#pragma unroll
-            for (int t2 = 0; t2 < G::MAXBW; ++t2) {
-                if (t2 < nbw) {
-                    const int bi = slot[t2] >> 8, bj = slot[t2] & 0xff;
-                    const int abase = 2 * (4 * bi + (r8 >> 1)) * NCT;
-                    const int bbase = 2 * (8 * bj + r8) * NCT;
-                    const double* A0 = Wd + abase + wa_lane[0];
-                    const double* A1 = Wd + abase + wa_lane[1];
-                    const double* A2 = Wd + abase + wa_lane[2];
-                    const double* A3 = Wd + abase + wa_lane[3];
-                    const double* B0 = Pd + bbase + b_lane[0];
-                    const double* B1 = Pd + bbase + b_lane[1];
-                    const double* B2 = Pd + bbase + b_lane[2];
-                    const double* B3 = Pd + bbase + b_lane[3];
-                    double e1[2] = {0.0, 0.0};
-#pragma unroll
-                    for (int k2 = 0; k2 < NCT / 2; ++k2) {
-                        if (k2 < nk2) {
-                            const int h = k2 & 3, g8 = 16 * (k2 >> 2);
-                            const double* Ap = h == 0 ? A0 : h == 1 ? A1 : h == 2 ? A2 : A3;
-                            const double* Bp = h == 0 ? B0 : h == 1 ? B1 : h == 2 ? B2 : B3;
-                            const double av = xsign(Ap[g8], wsgn);
-                            const double bv = Bp[g8];
-                            if (k2 & 1) dmma(e1, av, bv);
-                            else dmma(acc[t2], av, bv);
-                        }
+                for (int s2 = 0; s2 < G::RPT; ++s2) {
+                    const int l = warp + 8 * s2;
+                    if (v != 0.0 && pos >= lo && pos < lo + G::WCAP) {
+                        const double2 sv = S[cp_dst + s2 * 8 * NCT];
+                        const int o = l * G::WCAP + ((pos - lo) ^ sw);
+                        WS[o] = make_double2(v * sv.x, v * sv.y);
+                        SP[o] = sv;
                     }
-                    acc[t2][0] += e1[0];
-                    acc[t2][1] += e1[1];
+                    if (lane == 0 && (cnt & 1)) {   // zero slot after an odd count
+                        const int o = l * G::WCAP + (cnt ^ sw);
+                        WS[o] = make_double2(0.0, 0.0);
+                        SP[o] = make_double2(0.0, 0.0);
+                    }
                 }
+                if (nnz - lo <= G::WCAP) {
+                    pend = cnt > 0 ? cnt : 0;
+                    break;
+                }
+                __syncthreads();
+                rebuild(G::WCAP);
+                __syncthreads();
+                lo += G::WCAP;
             }
         }
     }
+    __syncthreads();
+    if (pend > 0) rebuild(pend);
     cp_async_wait<0>();
     __syncthreads();
 }
@@ -628,11 +650,10 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                     const int i4 = l >> 2;
                     const int blk = i4 * (i4 + 1) + (m >> 1);
                     const int ent = (l & 3) * 2 + (m & 1);
-                    double* o = od + (size_t)blk * 32;
-                    o[2 * ent] = pv.x;
-                    o[2 * ent + 1] = pv.y;
-                    o[16 + 2 * ent] = av.x;
-                    o[16 + 2 * ent + 1] = av.y;
+                    double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
+                    o[0] = pv.x; o[1] = av.x;
+                    o[2] = pv.y; o[3] = av.y;
+                    o[4] = -pv.y; o[5] = -av.y;
                 }
             }
     }
@@ -661,22 +682,22 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColAr
     double2* S0 = reinterpret_cast<double2*>(smem_raw);
     double2* S1 = S0 + G::LP8 * NCT;
     double2* WS = S1 + G::LP8 * NCT;
-    double2* SP = WS + G::LP8 * NCT;
-    double* FRs = reinterpret_cast<double*>(SP + G::LP8 * NCT);     // [NB][32] if staged
-    double* qr_s = FRs + (G::FR_SMEM ? G::NB * 32 : 0);             // [2][NCT][2]
-    const double* FR;
-    if (G::FR_SMEM) {   // stage the instance's packed P'/A' fragments (one cp.async group)
-        const double2* src = a.frags + (size_t)b * G::NB * 16;
-        double2* dst = reinterpret_cast<double2*>(FRs);
-        for (int e = tid; e < G::NB * 16; e += NT) cp_async16(dst + e, src + e, 16);
+    double2* SP = WS + G::LP8 * G::WCAP;
+    double2* FRs = SP + G::LP8 * G::WCAP;                            // [NB][24] if staged
+    double* qr_s = reinterpret_cast<double*>(FRs + (G::FR_SMEM ? G::NB * FRAG_SLOTS : 0));
+    const double2* FR;
+    if (G::FR_SMEM) {   // stage the instance's P'/A' fragments (one cp.async group)
+        const double2* src = a.frags + (size_t)b * G::NB * FRAG_SLOTS;
+        for (int e = tid; e < G::NB * FRAG_SLOTS; e += NT) cp_async16(FRs + e, src + e, 16);
         cp_async_commit();
         FR = FRs;
     } else {
-        FR = reinterpret_cast<const double*>(a.frags + (size_t)b * G::NB * 16);
+        FR = a.frags + (size_t)b * G::NB * FRAG_SLOTS;
     }
     int slot[G::MAXBW];
     int nbw;
     rebuild_slots<NRB>(slot, nbw);
+    if (a.dbg_delay_ns > 0 && (b & 1)) __nanosleep(a.dbg_delay_ns);
     double acc[G::MAXBW][2];
     double dx2, minq;
     col_pass<NRB>(a, b, a.k, a.x_cur + bN, a.x_next + bN, n_begin, n_end, S0, S1, WS, SP, FR,
@@ -733,7 +754,7 @@ __global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs 
     if (Es) stage_emp(a, b, Es, ld);
     assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
     double frob, logdet, trace;
-    double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * 16);
+    double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
     if (!factor_pass<RT>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet, trace)) {
         if (tid == 0) {
             a.status[b] = PSCA_CHOL_FAIL;
@@ -765,12 +786,12 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
     const int tid = threadIdx.x;
     const int L = fa.L, LP = geo.LP, ld = LP + 1;
 
-    double* FR = reinterpret_cast<double*>(smem_raw);                      // [NB][32]
+    double2* FR = reinterpret_cast<double2*>(smem_raw);                    // [NB][24]
     unsigned char* U = smem_raw + G::F_BYTES;                                 // union
     double2* S0 = reinterpret_cast<double2*>(U);
     double2* S1 = S0 + G::LP8 * NCT;
     double2* WS = S1 + G::LP8 * NCT;
-    double2* SP = WS + G::LP8 * NCT;
+    double2* SP = WS + G::LP8 * G::WCAP;
     double2* rowb = reinterpret_cast<double2*>(U);
     double2* colb = rowb + 2 * LP;
     double2* X = rowb + 4 * LP;
@@ -808,7 +829,8 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
             __syncthreads();
         }
         double frob, logdet, trace;
-        bool ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, FR, sred, frob, logdet, trace);
+        bool ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
+                                  sred, frob, logdet, trace);
         if (!ok) {
             if (tid == 0) {
                 fa.status[b] = PSCA_CHOL_FAIL;
@@ -838,7 +860,8 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
                                                  : nullptr,
                                   __dsub_rn(1.0, fa.steps[k]));
                 finish_sigma(X, ld, L, fa.noise[b]);
-                ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, FR, sred, frob, logdet, trace);
+                ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
+                                     sred, frob, logdet, trace);
                 if (!ok) {
                     if (tid == 0) {
                         fa.status[b] = PSCA_CHOL_FAIL;

@@ -60,8 +60,8 @@ def test_generic_and_compiled_kernels_agree(cuda_device):
 def test_persistent_equals_two_kernel_bitwise(cuda_device):
     """One chunk per instance: the persistent kernel and the two-kernel path run the
     same device functions in the same order, so the results are bit-identical."""
-    pers = run_script({})
-    two = run_script({"PSCA_NO_PERSISTENT": "1"})
+    pers = run_script({"PSCA_PERSISTENT": "1"})
+    two = run_script({"PSCA_PERSISTENT": "0"})
     assert any(v["path"] == "persistent" for v in pers.values())
     assert all(v["path"] == "two-kernel" for v in two.values())
     for key in pers:
