@@ -1187,11 +1187,11 @@ cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, c
     return launch_column<COL_SOLVE>(ca, g, n_chunks, st);
 }
 
-template <int RT>
+template <int NRB>
 cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     size_t sm = (size_t)4 * g.LP * 16 + (size_t)3 * g.LP * (g.LP + 1) * 16;
     if (sm > 227 * 1024) sm -= (size_t)g.LP * (g.LP + 1) * 16;   // Sigma_hat read from L2 instead
-    auto kfn = factor_solve_t<RT>;
+    auto kfn = factor_solve_t<NRB>;
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
@@ -1206,13 +1206,17 @@ cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st);
 
 cudaError_t launch_solve_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     if (!generic_forced()) {
-        const int rt = (g.LP + 15) / 16;
-        switch (rt) {
-            case 1: return launch_factor_t<1>(fa, g, st);
+        switch (g.NRB) {
             case 2: return launch_factor_t<2>(fa, g, st);
             case 3: return launch_factor_t<3>(fa, g, st);
             case 4: return launch_factor_t<4>(fa, g, st);
             case 5: return launch_factor_t<5>(fa, g, st);
+            case 6: return launch_factor_t<6>(fa, g, st);
+            case 8: return launch_factor_t<8>(fa, g, st);
+            case 10: return launch_factor_t<10>(fa, g, st);
+            case 12: return launch_factor_t<12>(fa, g, st);
+            case 16: return launch_factor_t<16>(fa, g, st);
+            case 20: return launch_factor_t<20>(fa, g, st);
             default: break;
         }
     }

@@ -440,13 +440,48 @@ __device__ __forceinline__ void stage_emp(const FacArgs& a, int b, double2* Es, 
     cp_async_commit();
 }
 
-template <int RT>
+template <int NRB>
+struct TF {
+    static constexpr int LP = 4 * NRB;
+    static constexpr int NBL = LP / 2;                 // 2x2 block rows
+    static constexpr int NLB = NBL * (NBL + 1) / 2;    // lower 2x2 blocks (incl. diagonal)
+    static constexpr int SL = (NLB + NT - 1) / NT;     // lower-block slots per thread
+    static constexpr int NFB = NBL * NBL;              // all 2x2 blocks
+    static constexpr int SG = (NFB + NT - 1) / NT;     // full-block slots per thread
+};
+
+// (bi, bj), bi >= bj, of lower 2x2 block number t (row-major)
+__device__ __forceinline__ void lower_block(int t, int& bi, int& bj) {
+    int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > t) --i;
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    bi = i;
+    bj = t - i * (i + 1) / 2;
+}
+
+// ---------------------------------------------------------------------------
+// factor_pass: X holds Sigma (L x L Hermitian, row stride ld = LP + 1) on
+// entry.  Hermitian sweep-operator Gauss-Jordan on the lower triangle only:
+// sweeping pivot k maps a_kk -> -1/d, a_ik, a_kj -> a/d, a_ij -> a_ij -
+// c_i conj(c_j) / d with c = column k, so the matrix stays exactly Hermitian
+// and the sweep over all pivots yields -Sigma^-1 (same pivots as LDL^H /
+// Cholesky: log|Sigma| = sum log d).  Each thread owns whole 2x2 blocks of
+// the lower triangle (registers); the pivot column is staged in SMEM by its
+// owners (ping-pong, one barrier per pivot).  Then trace(P Sigma_hat) when the
+// objective is recorded, G = Sigma_hat P (all 2x2 blocks), A = P G (lower
+// blocks only, P Hermitian), and the P'/A' fragments written to od (SMEM or
+// global).  Returns false (uniformly) when a pivot is not positive.  Ends
+// synchronised.
+// ---------------------------------------------------------------------------
+template <int NRB>
 __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, int b, double2* X,
-                                            double2* G, double2* rowb, double2* colb,
+                                            double2* G, double2* cbuf, double2* /*unused*/,
                                             const double2* Es, double* od, double* sred,
                                             double& frob, double& logdet, double& trace) {
+    using F = TF<NRB>;
     const int tid = threadIdx.x;
-    const int L = a.L, LP = geo.LP;
+    const int L = a.L;
+    constexpr int LP = F::LP;
     const int ld = LP + 1;
     {
         double s = 0.0;
@@ -457,67 +492,66 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         }
         frob = sqrt(block_sum(s, sred));
     }
-    const int ty = tid >> 4, tx = tid & 15;
-    double2 v[RT][RT];
+    // ---- lower 2x2 blocks of this thread ---------------------------------------
+    int bi[F::SL], bj[F::SL];
+    double2 v[F::SL][2][2];
 #pragma unroll
-    for (int u = 0; u < RT; ++u)
+    for (int u = 0; u < F::SL; ++u) {
+        const int t = tid + NT * u;
+        if (t < F::NLB) lower_block(t, bi[u], bj[u]); else { bi[u] = -1; bj[u] = 0; }
 #pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            v[u][w] = (i < L && j < L) ? X[i * ld + j] : make_double2(0.0, 0.0);
-        }
-    for (int e = tid; e < L; e += NT) {
-        rowb[e] = X[e];
-        colb[e] = X[e * ld];
+        for (int di = 0; di < 2; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj) {
+                const int i = 2 * bi[u] + di, j = 2 * bj[u] + dj;
+                v[u][di][dj] = (bi[u] >= 0 && i < L && j < L && i >= j) ? X[i * ld + j]
+                                                                       : make_double2(0.0, 0.0);
+            }
     }
+    for (int e = tid; e < 2 * LP; e += NT)
+        cbuf[e] = (e < L) ? X[e * ld] : make_double2(0.0, 0.0);   // padding stays zero
     __syncthreads();
 
     logdet = 0.0;
     bool ok = true;
     const bool want_logdet = a.record_objective;
     for (int k = 0; k < L; ++k) {
-        const double2* rk = rowb + (k & 1) * LP;
-        const double2* ck = colb + (k & 1) * LP;
-        double2* rn = rowb + ((k + 1) & 1) * LP;
-        double2* cn = colb + ((k + 1) & 1) * LP;
-        const double piv = rk[k].x;
-        if (!(piv > 0.0)) {
+        const double2* cb = cbuf + (k & 1) * LP;
+        double2* cn = cbuf + ((k + 1) & 1) * LP;
+        const double d = cb[k].x;
+        if (!(d > 0.0)) {
             ok = false;
             break;
         }
-        if (want_logdet) logdet += log(piv);
-        const double pinv = __drcp_rn(piv);
-        double2 cu[RT], rw[RT];
+        if (want_logdet) logdet += log(d);
+        const double dinv = __drcp_rn(d);
 #pragma unroll
-        for (int u = 0; u < RT; ++u) {
-            const int i = ty + 16 * u;
-            cu[u] = (i < L) ? ck[i] : make_double2(0.0, 0.0);
-        }
+        for (int u = 0; u < F::SL; ++u) {
+            if (bi[u] < 0) continue;
+            const int i0 = 2 * bi[u], j0 = 2 * bj[u];
+            const double2 ci[2] = {cb[i0], cb[i0 + 1]};
+            const double2 cj[2] = {cb[j0], cb[j0 + 1]};
 #pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int j = tx + 16 * w;
-            rw[w] = (j < L) ? rk[j] : make_double2(0.0, 0.0);
-        }
+            for (int di = 0; di < 2; ++di)
 #pragma unroll
-        for (int u = 0; u < RT; ++u) {
-            const int i = ty + 16 * u;
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int j = tx + 16 * w;
-                // branch-free: general update, pivot row, pivot column, pivot
-                const double2 o = v[u][w];
-                const double2 pr = cmul(cu[u], rw[w]);
-                double nx = o.x - pr.x * pinv, ny = o.y - pr.y * pinv;
-                const double sx = o.x * pinv, sy = o.y * pinv;
-                nx = (j == k) ? -sx : nx;
-                ny = (j == k) ? -sy : ny;
-                nx = (i == k) ? ((j == k) ? pinv : sx) : nx;
-                ny = (i == k) ? ((j == k) ? 0.0 : sy) : ny;
-                const double2 nv = make_double2(nx, ny);
-                v[u][w] = nv;
-                if (i == k + 1 && j < L) rn[j] = nv;
-                if (j == k + 1 && i < L) cn[i] = nv;
-            }
+                for (int dj = 0; dj < 2; ++dj) {
+                    const int i = i0 + di, j = j0 + dj;
+                    const double2 o = v[u][di][dj];
+                    // c_i conj(c_j)
+                    const double pr = ci[di].x * cj[dj].x + ci[di].y * cj[dj].y;
+                    const double pim = ci[di].y * cj[dj].x - ci[di].x * cj[dj].y;
+                    double nx = o.x - pr * dinv, ny = o.y - pim * dinv;
+                    const bool onrow = (i == k) || (j == k);
+                    nx = onrow ? o.x * dinv : nx;
+                    ny = onrow ? o.y * dinv : ny;
+                    nx = (i == k && j == k) ? -dinv : nx;
+                    ny = (i == k && j == k) ? 0.0 : ny;
+                    if (i < j) { nx = 0.0; ny = 0.0; }
+                    v[u][di][dj] = make_double2(nx, ny);
+                    // stage column k+1 of the swept matrix
+                    if (j == k + 1 && i >= j && i < L) cn[i] = make_double2(nx, ny);
+                    if (i == k + 1 && j < i) cn[j] = make_double2(nx, -ny);
+                }
         }
         __syncthreads();
     }
@@ -525,137 +559,137 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         __syncthreads();
         return false;
     }
-    // ---- P = (P + P^H)/2 -------------------------------------------------------
+    // ---- P = -(swept): full Hermitian into X ----------------------------------
 #pragma unroll
-    for (int u = 0; u < RT; ++u)
+    for (int u = 0; u < F::SL; ++u) {
+        if (bi[u] < 0) continue;
 #pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
-        }
-    __syncthreads();
+        for (int di = 0; di < 2; ++di)
 #pragma unroll
-    for (int u = 0; u < RT; ++u)
-#pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            if (i < L && j < L) {
-                const double2 t = X[j * ld + i];
-                v[u][w] = (i == j) ? make_double2(v[u][w].x, 0.0)
-                                   : make_double2(0.5 * (v[u][w].x + t.x), 0.5 * (v[u][w].y - t.y));
+            for (int dj = 0; dj < 2; ++dj) {
+                const int i = 2 * bi[u] + di, j = 2 * bj[u] + dj;
+                if (i >= j) {
+                    const double2 pv = (i < L && j < L) ? make_double2(-v[u][di][dj].x, -v[u][di][dj].y)
+                                                        : make_double2(0.0, 0.0);
+                    X[i * ld + j] = (i == j) ? make_double2(pv.x, 0.0) : pv;
+                    if (i != j) X[j * ld + i] = make_double2(pv.x, -pv.y);
+                }
             }
-        }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < RT; ++u)
-#pragma unroll
-        for (int w = 0; w < RT; ++w) {
-            const int i = ty + 16 * u, j = tx + 16 * w;
-            if (i < LP && j < LP) X[i * ld + j] = v[u][w];
-        }
-    __syncthreads();
-
+    }
     cp_async_wait<0>();   // Sigma_hat staged by the caller (stage_emp), if in SMEM
     __syncthreads();
     const double2* Eg = a.emp_cov + (size_t)b * L * L;   // used when Es == nullptr
+    auto Ev = [&](int i, int c) -> double2 {
+        return Es ? Es[i * ld + c] : __ldg(Eg + (size_t)i * L + c);
+    };
     trace = 0.0;
     if (a.record_objective) {
         double s = 0.0;
-#pragma unroll
-        for (int u = 0; u < RT; ++u)
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int i = ty + 16 * u, j = tx + 16 * w;
-                if (i < L && j < L) {
-                    const double2 ev = Es ? Es[j * ld + i] : __ldg(Eg + (size_t)j * L + i);
-                    s = fma(v[u][w].x, ev.x, fma(-v[u][w].y, ev.y, s));
-                }
-            }
+        for (int e = tid; e < L * L; e += NT) {
+            const int i = e / L, j = e - i * L;
+            const double2 pv = X[i * ld + j], ev = Ev(j, i);
+            s = fma(pv.x, ev.x, fma(-pv.y, ev.y, s));
+        }
         trace = block_sum(s, sred);
     }
-    // ---- G = Sigma_hat P ------------------------------------------------------
+    // ---- G = Sigma_hat P (all 2x2 blocks) ----------------------------------------
     {
-        double2 gacc[RT][RT];
+        int gi[F::SG], gj[F::SG];
+        double2 gacc[F::SG][2][2];
 #pragma unroll
-        for (int u = 0; u < RT; ++u)
+        for (int u = 0; u < F::SG; ++u) {
+            const int t = tid + NT * u;
+            gi[u] = (t < F::NFB) ? t / F::NBL : -1;
+            gj[u] = (t < F::NFB) ? t % F::NBL : 0;
 #pragma unroll
-            for (int w = 0; w < RT; ++w) gacc[u][w] = make_double2(0.0, 0.0);
+            for (int di = 0; di < 2; ++di)
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) gacc[u][di][dj] = make_double2(0.0, 0.0);
+        }
         for (int c = 0; c < L; ++c) {
-            double2 eu[RT], xw[RT];
 #pragma unroll
-            for (int u = 0; u < RT; ++u) {
-                const int i = ty + 16 * u;
-                eu[u] = (i < L) ? (Es ? Es[i * ld + c] : __ldg(Eg + (size_t)i * L + c))
-                                : make_double2(0.0, 0.0);
+            for (int u = 0; u < F::SG; ++u) {
+                if (gi[u] < 0) continue;
+                const int i0 = 2 * gi[u], j0 = 2 * gj[u];
+                const double2 e0 = (i0 < L) ? Ev(i0, c) : make_double2(0.0, 0.0);
+                const double2 e1 = (i0 + 1 < L) ? Ev(i0 + 1, c) : make_double2(0.0, 0.0);
+                const double2 x0 = X[c * ld + j0], x1 = X[c * ld + j0 + 1];
+                gacc[u][0][0] = cfma(e0, x0, gacc[u][0][0]);
+                gacc[u][0][1] = cfma(e0, x1, gacc[u][0][1]);
+                gacc[u][1][0] = cfma(e1, x0, gacc[u][1][0]);
+                gacc[u][1][1] = cfma(e1, x1, gacc[u][1][1]);
             }
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int j = tx + 16 * w;
-                xw[w] = (j < LP) ? X[c * ld + j] : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < RT; ++u)
-#pragma unroll
-                for (int w = 0; w < RT; ++w) gacc[u][w] = cfma(eu[u], xw[w], gacc[u][w]);
         }
 #pragma unroll
-        for (int u = 0; u < RT; ++u)
+        for (int u = 0; u < F::SG; ++u) {
+            if (gi[u] < 0) continue;
 #pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int i = ty + 16 * u, j = tx + 16 * w;
-                if (i < LP && j < LP) G[i * ld + j] = gacc[u][w];
-            }
+            for (int di = 0; di < 2; ++di)
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj)
+                    G[(2 * gi[u] + di) * ld + 2 * gj[u] + dj] = gacc[u][di][dj];
+        }
     }
     __syncthreads();
-    // ---- A = P^H G and the fragment pack ---------------------------------------
+    // ---- A = P G (lower 2x2 blocks) and the fragment pack ------------------------
     {
-        double2 aacc[RT][RT];
+        double2 aacc[F::SL][2][2];
 #pragma unroll
-        for (int u = 0; u < RT; ++u)
+        for (int u = 0; u < F::SL; ++u)
 #pragma unroll
-            for (int w = 0; w < RT; ++w) aacc[u][w] = make_double2(0.0, 0.0);
+            for (int di = 0; di < 2; ++di)
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) aacc[u][di][dj] = make_double2(0.0, 0.0);
         for (int t = 0; t < L; ++t) {
-            double2 pu[RT], gw[RT];
 #pragma unroll
-            for (int u = 0; u < RT; ++u) {
-                const int i = ty + 16 * u;
-                pu[u] = (i < LP) ? X[t * ld + i] : make_double2(0.0, 0.0);
+            for (int u = 0; u < F::SL; ++u) {
+                if (bi[u] < 0) continue;
+                const int l0 = 2 * bi[u], m0 = 2 * bj[u];
+                const double2 p0 = X[l0 * ld + t], p1 = X[(l0 + 1) * ld + t];
+                const double2 g0 = G[t * ld + m0], g1 = G[t * ld + m0 + 1];
+                aacc[u][0][0] = cfma(p0, g0, aacc[u][0][0]);
+                aacc[u][0][1] = cfma(p0, g1, aacc[u][0][1]);
+                aacc[u][1][0] = cfma(p1, g0, aacc[u][1][0]);
+                aacc[u][1][1] = cfma(p1, g1, aacc[u][1][1]);
             }
-#pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int j = tx + 16 * w;
-                gw[w] = (j < LP) ? G[t * ld + j] : make_double2(0.0, 0.0);
-            }
-#pragma unroll
-            for (int u = 0; u < RT; ++u)
-#pragma unroll
-                for (int w = 0; w < RT; ++w) aacc[u][w] = cfma_conj_a(pu[u], gw[w], aacc[u][w]);
         }
+        auto put = [&](int l, int m, double2 pv, double2 av) {
+            const int i4 = l >> 2;
+            const int blk = i4 * (i4 + 1) + (m >> 1);
+            const int ent = (l & 3) * 2 + (m & 1);
+            double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
+            o[0] = pv.x; o[1] = av.x;
+            o[2] = pv.y; o[3] = av.y;
+            o[4] = -pv.y; o[5] = -av.y;
+        };
 #pragma unroll
-        for (int u = 0; u < RT; ++u)
+        for (int u = 0; u < F::SL; ++u) {
+            if (bi[u] < 0) continue;
 #pragma unroll
-            for (int w = 0; w < RT; ++w) {
-                const int l = ty + 16 * u, m = tx + 16 * w;
-                if (l < LP && m <= 4 * (l >> 2) + 3) {
+            for (int di = 0; di < 2; ++di)
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) {
+                    const int l = 2 * bi[u] + di, m = 2 * bj[u] + dj;
                     double2 pv = make_double2(0.0, 0.0), av = make_double2(0.0, 0.0);
                     if (l < L && m <= l) {
                         pv = X[l * ld + m];
-                        av = aacc[u][w];
+                        av = aacc[u][di][dj];
                         if (m < l) {
                             pv.x *= 2.0; pv.y *= 2.0; av.x *= 2.0; av.y *= 2.0;
                         } else {
                             pv.y = 0.0; av.y = 0.0;
                         }
                     }
-                    const int i4 = l >> 2;
-                    const int blk = i4 * (i4 + 1) + (m >> 1);
-                    const int ent = (l & 3) * 2 + (m & 1);
-                    double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
-                    o[0] = pv.x; o[1] = av.x;
-                    o[2] = pv.y; o[3] = av.y;
-                    o[4] = -pv.y; o[5] = -av.y;
+                    put(l, m, pv, av);
                 }
-            }
+        }
+        // upper 2x2 blocks inside the diagonal 4x4 fragment groups are zero
+        if (tid < NRB) {
+            const int l0 = 4 * tid, m0 = 4 * tid + 2;
+            const double2 z = make_double2(0.0, 0.0);
+            put(l0, m0, z, z); put(l0, m0 + 1, z, z);
+            put(l0 + 1, m0, z, z); put(l0 + 1, m0 + 1, z, z);
+        }
     }
     __syncthreads();
     return true;
@@ -728,8 +762,8 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColAr
     }
 }
 
-template <int RT>
-__global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs a) {
+template <int NRB>
+__global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) factor_solve_t(FacArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double sred[NWARP + 1];
     __shared__ int s_flag;
@@ -744,8 +778,8 @@ __global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs 
     }
     const double prior_value = fac_prior_terms(a, b, sred);
     double2* sm = reinterpret_cast<double2*>(smem_raw);
-    double2* rowb = sm;             // [2][LP]
-    double2* colb = sm + 2 * LP;    // [2][LP]
+    double2* rowb = sm;             // [2][LP] pivot column ping-pong
+    double2* colb = sm + 2 * LP;    // (unused)
     double2* X = sm + 4 * LP;       // [LP][ld]
     double2* G = X + (size_t)LP * ld;
     // Sigma_hat in SMEM when three L x L buffers fit (L <= 64), else read from L2
@@ -755,7 +789,7 @@ __global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs 
     assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
     double frob, logdet, trace;
     double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
-    if (!factor_pass<RT>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet, trace)) {
+    if (!factor_pass<NRB>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet, trace)) {
         if (tid == 0) {
             a.status[b] = PSCA_CHOL_FAIL;
             if (a.cond_est) a.cond_est[b] = INFINITY;
@@ -777,7 +811,6 @@ __global__ void __launch_bounds__(NT, (RT <= 3) ? 2 : 1) factor_solve_t(FacArgs 
 template <int NRB>
 __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs fa, int* counter) {
     using G = TG<NRB>;
-    constexpr int RT = G::RT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double sred[NWARP + 1];
     __shared__ double s_inst[4];
@@ -829,7 +862,7 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
             __syncthreads();
         }
         double frob, logdet, trace;
-        bool ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
+        bool ok = factor_pass<NRB>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
                                   sred, frob, logdet, trace);
         if (!ok) {
             if (tid == 0) {
@@ -860,7 +893,7 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
                                                  : nullptr,
                                   __dsub_rn(1.0, fa.steps[k]));
                 finish_sigma(X, ld, L, fa.noise[b]);
-                ok = factor_pass<RT>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
+                ok = factor_pass<NRB>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
                                      sred, frob, logdet, trace);
                 if (!ok) {
                     if (tid == 0) {
