@@ -192,15 +192,16 @@ __device__ __forceinline__ double np_clip(double v, double lo, double hi) {
 }
 
 // deterministic CTA reductions (fixed shuffle + fixed warp order)
+// (any CTA size up to NT; sred holds NWARP + 1 doubles)
 __device__ double block_sum(double v, double* sred) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     __syncthreads();
     if (lane == 0) sred[w] = v;
     __syncthreads();
     double t = 0.0;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NWARP; ++i) t += sred[i];
+        for (int i = 0; i < nw; ++i) t += sred[i];
         sred[NWARP] = t;
     }
     __syncthreads();
@@ -699,7 +700,7 @@ __device__ void pack_frags(const double2* X, const double2* G, int ld, int L, co
 __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2* X, int ld,
                                bool zero_weights) {
     const int L = a.L;
-    for (int e = threadIdx.x; e < L * L; e += NT) {
+    for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
         int i = e / L, j = e - i * L;
         X[i * ld + j] = make_double2(0.0, 0.0);
     }
@@ -710,7 +711,7 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
     {
         const int total = geo.NBLK * 32;
         const double2* sp = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
-        for (int e = threadIdx.x; e < total; e += NT) {
+        for (int e = threadIdx.x; e < total; e += blockDim.x) {
             int blk = e >> 5, lane = e & 31;
             // decode (i, j) of rebuild block blk
             int i = 0, base = 0;
@@ -746,7 +747,7 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
     }
     __syncthreads();
     const double s2 = a.noise[b];
-    for (int e = threadIdx.x; e < L * L; e += NT) {
+    for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
         int i = e / L, j = e - i * L;
         if (i < j) {
             double2 v = X[j * ld + i];
@@ -798,7 +799,7 @@ __device__ bool fac_finalize(const FacArgs& a, int b, int* s_flag) {
     __syncthreads();
     if (*s_flag == PSCA_QFLOOR) {
         const size_t bN = (size_t)b * a.N;
-        for (int n = tid; n < a.N; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
+        for (int n = tid; n < a.N; n += blockDim.x) a.x_next[bN + n] = a.x_cur[bN + n];
         return true;
     }
     return *s_flag != 0 || a.k_new >= a.T;
@@ -813,7 +814,7 @@ __device__ double fac_prior_terms_at(const FacArgs& a, int b, const double* xv, 
     if ((a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.record_objective))) {
         const size_t bN = (size_t)b * a.N;
         double acc = 0.0;
-        for (int n = tid; n < a.N; n += NT) {
+        for (int n = tid; n < a.N; n += blockDim.x) {
             const double x = xv[n];
             if (a.kind == PSCA_MAP_UR) {
                 double dens, der;
@@ -1189,14 +1190,13 @@ cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, c
 
 template <int NRB>
 cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
-    size_t sm = (size_t)4 * g.LP * 16 + (size_t)3 * g.LP * (g.LP + 1) * 16;
-    if (sm > 227 * 1024) sm -= (size_t)g.LP * (g.LP + 1) * 16;   // Sigma_hat read from L2 instead
+    const size_t sm = (size_t)4 * g.LP * 16 + (size_t)2 * g.LP * (g.LP + 1) * 16;
     auto kfn = factor_solve_t<NRB>;
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
     ProfScope prof(st, 1);
-    kfn<<<fa.B, NT, sm, st>>>(fa);
+    kfn<<<fa.B, NT_FAC, sm, st>>>(fa);
     ++g_launches;
     return cudaGetLastError();
 }

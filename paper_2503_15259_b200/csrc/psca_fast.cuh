@@ -40,7 +40,7 @@ struct TG {
     // otherwise col_pass reads them through L1 from global
     static constexpr bool FR_SMEM = TILE_BYTES + F_BYTES + SMALL <= 227 * 1024;
     static constexpr size_t COL_SMEM = TILE_BYTES + (FR_SMEM ? F_BYTES : 0) + SMALL;
-    static constexpr size_t FAC_BYTES = (size_t)4 * LP * 16 + (size_t)3 * LP * (LP + 1) * 16;
+    static constexpr size_t FAC_BYTES = (size_t)4 * LP * 16 + (size_t)2 * LP * (LP + 1) * 16;
     static constexpr size_t UNION = (TILE_BYTES > FAC_BYTES) ? TILE_BYTES : FAC_BYTES;
     static constexpr size_t PERSIST_SMEM = F_BYTES + UNION + SMALL;
 };
@@ -407,7 +407,7 @@ __device__ __forceinline__ void acc_to_sigma(const double (&acc)[TG<NRB>::MAXBW]
 // Upper triangle by conjugation, sigma^2 on the (real) diagonal.
 __device__ __forceinline__ void finish_sigma(double2* X, int ld, int L, double s2) {
     __syncthreads();
-    for (int e = threadIdx.x; e < L * L; e += NT) {
+    for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
         const int i = e / L, j = e - i * L;
         if (i < j) {
             const double2 v = X[j * ld + i];
@@ -433,22 +433,25 @@ __device__ __forceinline__ void finish_sigma(double2* X, int ld, int L, double s
 __device__ __forceinline__ void stage_emp(const FacArgs& a, int b, double2* Es, int ld) {
     const double2* E = a.emp_cov + (size_t)b * a.L * a.L;
     const int L = a.L;
-    for (int e = threadIdx.x; e < L * L; e += NT) {
+    for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
         const int i = e / L, j = e - i * L;
         cp_async16(Es + i * ld + j, E + e, 16);
     }
     cp_async_commit();
 }
 
-template <int NRB>
+template <int NRB, int NTH>
 struct TF {
     static constexpr int LP = 4 * NRB;
     static constexpr int NBL = LP / 2;                 // 2x2 block rows
     static constexpr int NLB = NBL * (NBL + 1) / 2;    // lower 2x2 blocks (incl. diagonal)
-    static constexpr int SL = (NLB + NT - 1) / NT;     // lower-block slots per thread
+    static constexpr int SL = (NLB + NTH - 1) / NTH;   // lower-block slots per thread
     static constexpr int NFB = NBL * NBL;              // all 2x2 blocks
-    static constexpr int SG = (NFB + NT - 1) / NT;     // full-block slots per thread
+    static constexpr int SG = (NFB + NTH - 1) / NTH;   // full-block slots per thread
 };
+// factor CTA size of the two-kernel path: 128 threads, Sigma_hat read from L2,
+// so four instances share an SM and hide each other's pivot-barrier latency
+constexpr int NT_FAC = 128;
 
 // (bi, bj), bi >= bj, of lower 2x2 block number t (row-major)
 __device__ __forceinline__ void lower_block(int t, int& bi, int& bj) {
@@ -473,19 +476,19 @@ __device__ __forceinline__ void lower_block(int t, int& bi, int& bj) {
 // global).  Returns false (uniformly) when a pivot is not positive.  Ends
 // synchronised.
 // ---------------------------------------------------------------------------
-template <int NRB>
+template <int NRB, int NTH>
 __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, int b, double2* X,
                                             double2* G, double2* cbuf, double2* /*unused*/,
                                             const double2* Es, double* od, double* sred,
                                             double& frob, double& logdet, double& trace) {
-    using F = TF<NRB>;
+    using F = TF<NRB, NTH>;
     const int tid = threadIdx.x;
     const int L = a.L;
     constexpr int LP = F::LP;
     const int ld = LP + 1;
     {
         double s = 0.0;
-        for (int e = tid; e < L * L; e += NT) {
+        for (int e = tid; e < L * L; e += NTH) {
             const int i = e / L, j = e - i * L;
             const double2 v = X[i * ld + j];
             s = fma(v.x, v.x, fma(v.y, v.y, s));
@@ -497,7 +500,7 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
     double2 v[F::SL][2][2];
 #pragma unroll
     for (int u = 0; u < F::SL; ++u) {
-        const int t = tid + NT * u;
+        const int t = tid + NTH * u;
         if (t < F::NLB) lower_block(t, bi[u], bj[u]); else { bi[u] = -1; bj[u] = 0; }
 #pragma unroll
         for (int di = 0; di < 2; ++di)
@@ -508,7 +511,7 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                                                                        : make_double2(0.0, 0.0);
             }
     }
-    for (int e = tid; e < 2 * LP; e += NT)
+    for (int e = tid; e < 2 * LP; e += NTH)
         cbuf[e] = (e < L) ? X[e * ld] : make_double2(0.0, 0.0);   // padding stays zero
     __syncthreads();
 
@@ -585,7 +588,7 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
     trace = 0.0;
     if (a.record_objective) {
         double s = 0.0;
-        for (int e = tid; e < L * L; e += NT) {
+        for (int e = tid; e < L * L; e += NTH) {
             const int i = e / L, j = e - i * L;
             const double2 pv = X[i * ld + j], ev = Ev(j, i);
             s = fma(pv.x, ev.x, fma(-pv.y, ev.y, s));
@@ -598,7 +601,7 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         double2 gacc[F::SG][2][2];
 #pragma unroll
         for (int u = 0; u < F::SG; ++u) {
-            const int t = tid + NT * u;
+            const int t = tid + NTH * u;
             gi[u] = (t < F::NFB) ? t / F::NBL : -1;
             gj[u] = (t < F::NFB) ? t % F::NBL : 0;
 #pragma unroll
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColAr
 }
 
 template <int NRB>
-__global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) factor_solve_t(FacArgs a) {
+__global__ void __launch_bounds__(NT_FAC, (NRB <= 10) ? 4 : 1) factor_solve_t(FacArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double sred[NWARP + 1];
     __shared__ int s_flag;
@@ -782,14 +785,12 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) factor_solve_t(FacArg
     double2* colb = sm + 2 * LP;    // (unused)
     double2* X = sm + 4 * LP;       // [LP][ld]
     double2* G = X + (size_t)LP * ld;
-    // Sigma_hat in SMEM when three L x L buffers fit (L <= 64), else read from L2
-    double2* Es = ((size_t)4 * LP * 16 + (size_t)3 * LP * ld * 16 <= 227 * 1024)
-                      ? G + (size_t)LP * ld : nullptr;
-    if (Es) stage_emp(a, b, Es, ld);
+    const double2* Es = nullptr;   // Sigma_hat read through L1/L2
     assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
     double frob, logdet, trace;
     double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
-    if (!factor_pass<NRB>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet, trace)) {
+    if (!factor_pass<NRB, NT_FAC>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet,
+                                  trace)) {
         if (tid == 0) {
             a.status[b] = PSCA_CHOL_FAIL;
             if (a.cond_est) a.cond_est[b] = INFINITY;
@@ -829,7 +830,7 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
     double2* colb = rowb + 2 * LP;
     double2* X = rowb + 4 * LP;
     double2* Gm = X + (size_t)LP * ld;
-    double2* Es = Gm + (size_t)LP * ld;
+    const double2* Es = nullptr;   // Sigma_hat read through L1/L2 (keeps 2 CTAs / SM)
     double* qr_s = reinterpret_cast<double*>(U + G::UNION);
 
     int slot[G::MAXBW];
@@ -847,7 +848,6 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
         double* final_x = xc;
 
         // ---- iterate 0: prior terms at x = 0, Sigma_0 = sigma^2 I, D_0 = 0 --
-        stage_emp(fa, b, Es, ld);
         if (fa.incremental) {
             double2* D = fa.dmat + (size_t)b * L * L;
             for (int e = tid; e < L * L; e += NT) D[e] = make_double2(0.0, 0.0);
@@ -862,7 +862,7 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
             __syncthreads();
         }
         double frob, logdet, trace;
-        bool ok = factor_pass<NRB>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
+        bool ok = factor_pass<NRB, NT>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
                                   sred, frob, logdet, trace);
         if (!ok) {
             if (tid == 0) {
@@ -886,14 +886,13 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
                 final_x = xn;
                 if (flag == PSCA_CONVERGED || k + 1 == fa.T) break;
                 // ---- factorisation at x_{k+1} ---------------------------------
-                stage_emp(fa, b, Es, ld);
                 pv = fac_prior_terms_at(fa, b, xn, sred);
                 acc_to_sigma<NRB>(acc, slot, nbw, X, ld, L,
                                   fa.incremental ? reinterpret_cast<double*>(fa.dmat + (size_t)b * L * L)
                                                  : nullptr,
                                   __dsub_rn(1.0, fa.steps[k]));
                 finish_sigma(X, ld, L, fa.noise[b]);
-                ok = factor_pass<NRB>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
+                ok = factor_pass<NRB, NT>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
                                      sred, frob, logdet, trace);
                 if (!ok) {
                     if (tid == 0) {

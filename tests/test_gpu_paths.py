@@ -59,12 +59,14 @@ def test_generic_and_compiled_kernels_agree(cuda_device):
 
 def test_persistent_equals_two_kernel_bitwise(cuda_device):
     """One chunk per instance: the persistent kernel and the two-kernel path run the
-    same device functions in the same order, so the results are bit-identical."""
+    same device functions, so the iterates are bit-identical."""
     pers = run_script({"PSCA_PERSISTENT": "1"})
     two = run_script({"PSCA_PERSISTENT": "0"})
     assert any(v["path"] == "persistent" for v in pers.values())
     assert all(v["path"] == "two-kernel" for v in two.values())
     for key in pers:
-        for field in ("x", "obj", "un"):
+        for field in ("x", "un"):
             np.testing.assert_array_equal(np.array(pers[key][field]), np.array(two[key][field]),
                                           err_msg=f"{key} {field}")
+        # the objective's trace / Frobenius reductions run over different CTA sizes
+        assert max_rel(np.array(pers[key]["obj"]), np.array(two[key]["obj"])) <= 1e-13
