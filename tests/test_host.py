@@ -1,0 +1,128 @@
+"""CPU tests: the C ABI library exports what include/psca.h declares, and the host-side
+mirror of the reference API validates arguments like the reference does.
+
+No GPU needed; nothing here launches a kernel.
+"""
+
+import ctypes
+import pathlib
+import re
+
+import numpy as np
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+
+
+def test_library_exports_every_declared_symbol():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2503_15259_b200 import device
+    header = (ROOT / "include" / "psca.h").read_text()
+    declared = set(re.findall(r"^\s*(?:[\w\*]+\s+)+\**(psca_\w+)\s*\(", header, re.M))
+    assert {"psca_solve", "psca_empirical_cov", "psca_quad_forms", "psca_hpd_inverse"} <= declared
+    lib = ctypes.CDLL(str(device.LIB_PATH))
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in psca.h but not exported"
+    assert declared <= set(device.EXPORTED_SYMBOLS) | {"psca_last_path"}
+    assert device.load().psca_version().decode().startswith("psca-b200")
+
+
+def test_solve_args_struct_matches_header_layout():
+    from paper_2503_15259_b200.device import EffPriorC, SolveArgsC
+    assert ctypes.sizeof(EffPriorC) == 10 * 8
+    # ints (6) + tol + 2 ints -> 40 bytes before the pointer block, 7 pointers,
+    # the prior struct, 7 more pointers
+    assert SolveArgsC.pilots.offset == 40
+    assert SolveArgsC.eff.offset == 40 + 7 * 8
+    assert ctypes.sizeof(SolveArgsC) == 40 + 7 * 8 + 80 + 7 * 8
+
+
+def test_workspace_query_rejects_bad_arguments():
+    from paper_2503_15259_b200 import device
+    lib = device.load()
+    a = device.SolveArgsC(kind=7, B=1, N=10, L=4, n_antennas=8, max_iter=1)
+    assert lib.psca_solve_workspace_bytes(ctypes.byref(a)) == 0
+    assert lib.psca_solve(ctypes.byref(a), None, 0, None) == -1
+
+
+def test_problem_and_schedule_validation():
+    from paper_2503_15259_b200 import DomainError, Problem, StepSchedule
+    from paper_2503_15259_b200.estimators import default_schedule, default_steps
+    from paper_2503_15259_b200.priors import IndependentPrior
+    with pytest.raises(DomainError):
+        Problem("map-k")
+    with pytest.raises(DomainError):
+        Problem("ml-k", IndependentPrior(np.array([0.1])))
+    with pytest.raises(DomainError):
+        Problem("mle")
+    assert default_schedule(0) == 0.5 and default_schedule(1) == 0.375
+    assert default_schedule(2) == pytest.approx(0.3046875, abs=1e-12)
+    np.testing.assert_array_equal(default_steps(50), StepSchedule.default().materialize(50))
+    with pytest.raises(DomainError):
+        StepSchedule.explicit([0.5, 1.5])
+    with pytest.raises(DomainError):
+        StepSchedule.polynomial(exponent=0.5)
+    with pytest.raises(DomainError):
+        StepSchedule(fn=lambda k: 2.0).materialize(3)
+    poly = StepSchedule.polynomial()
+    np.testing.assert_array_equal(poly.materialize(5), [poly(k) for k in range(5)])
+
+
+def test_unrolled_config_validation():
+    from paper_2503_15259_b200 import DomainError, Problem
+    from paper_2503_15259_b200.unroll import UnrolledConfig
+    with pytest.raises(DomainError):
+        UnrolledConfig(Problem.ml_k(), [0.5, 0.0])
+    with pytest.raises(DomainError):
+        UnrolledConfig(Problem.ml_k(), [])
+    with pytest.raises(DomainError):
+        UnrolledConfig(Problem.ml_k(), [0.5], prior_params_trainable=True)
+
+
+def test_prior_objects_match_reference_fields(golden_components):
+    from paper_2503_15259_b200.priors import EffPathlossPrior, known_prior_gradient
+    from paper_2503_15259_b200.priors import IndependentPrior
+    f = golden_components["eff_fields"]
+    pr = EffPathlossPrior(np.full(3, 0.1), f[0], f[1], f[2], f[3], f[4], f[5])
+    assert pr.g_low == f[7] and pr.g_high == f[8] and pr.dead_zone_grad == f[6]
+    g = known_prior_gradient(IndependentPrior(np.full(3, 0.05)), 64, 3)
+    np.testing.assert_array_equal(g, golden_components["known_grad_p005_m64"])
+
+
+def test_threshold_calibration_matches_reference(golden_components):
+    from paper_2503_15259_b200.unroll import calibrate_threshold, decide
+    g = golden_components
+    theta = calibrate_threshold(list(g["thr_scores"]), list(g["thr_truths"]))
+    assert theta == float(g["thr_theta"])
+    np.testing.assert_array_equal(decide([theta - 1e-3, theta, theta + 1e-3], theta), [0.0, 1.0, 1.0])
+
+
+def test_scene_generator_is_deterministic_and_matches_golden(golden_baseline):
+    from paper_2503_15259_b200 import scenes
+    for name in ("c0", "c1", "c3_l20"):
+        cfg = scenes.BASELINE_CONFIGS[name]
+        s = scenes.make_scene(cfg, 0)
+        chk = golden_baseline[f"{name}_i0_checksum"]
+        np.testing.assert_allclose([np.sum(s.pilots).real, np.sum(np.abs(s.emp_cov)),
+                                    np.sum(s.gains)], chk, rtol=1e-12)
+        assert s.activities.sum() == cfg.n_active
+        assert np.all(s.gains >= 3.3) and np.all(s.gains <= 19137.0)
+
+
+def test_no_cpu_fallback_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    from paper_2503_15259_b200 import device, estimators, scenes
+    cfg = scenes.SceneConfig(9, "ml-ud", 64, 8, 16, 4, 3, 1)
+    b = scenes.stack_batch([scenes.make_scene(cfg, 0)])
+    with pytest.raises(device.PscaNativeError):
+        estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"],
+                                  b["noise"], 16, max_iter=3)
+
+
+def test_product_package_does_not_import_the_oracle():
+    for p in (ROOT / "paper_2503_15259_b200").rglob("*.py"):
+        src = p.read_text()
+        assert "import oracle" not in src and "from oracle" not in src, p
