@@ -123,6 +123,56 @@ int psca_eval_objective(const double* sigma, const double* sigma_inv, const doub
                         int B, int L, double* out, int* status, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Large pilot length (L <= 256; BASELINE config 4: N = 100,000, L = 256) as a
+ * host-driven step loop for ONE instance, whose columns may be sharded over
+ * ranks (multi-GPU column sharding):
+ *     psca_large_begin                         x = 0, Sigma_0 = sigma^2 I, factor
+ *     for k: psca_large_columns(k)             this rank's columns: quad forms,
+ *                                              update, Sigma-increment partial
+ *            [all-reduce the exchange buffers: dsig (sum), red[0] (sum),
+ *             red[1] (min) -- ncclAllReduce over NVLink when sharded]
+ *            psca_large_factor(k)              finalise iteration k (q-floor,
+ *                                              update norm, tol), factor k+1
+ *            stop when *flag (device int) != 0
+ * x after iteration k is x_b for even k, x_a for odd k (x_a holds x_0 = 0).
+ * Replaces the same psca_run loop (estimators.py:259-286) for large L. */
+typedef struct {
+    int kind, N, L, n_antennas, max_iter, record_objective;
+    double tol, noise;
+    const double* pilots;   /* [L][N] complex128: this rank's columns         */
+    const double* gains;    /* [N]                                             */
+    const double* emp_cov;  /* [L][L] complex128                               */
+    const double* steps;    /* [max_iter]                                      */
+    const double* prior_lin;/* map-k [N]                                       */
+    const double* prior_p;  /* map-ur [N]                                      */
+    psca_eff_prior eff;
+    double* x_a;            /* [N] x for even iterates                         */
+    double* x_b;            /* [N] x for odd iterates                          */
+    double* update_norm;    /* [max_iter]                                      */
+    double* objective;      /* [max_iter] or 0                                 */
+    double* iterates;       /* [max_iter+1][N] or 0                            */
+    int* status;            /* [1]                                             */
+    int* n_iter;            /* [1]                                             */
+    double* cond_est;       /* [1] or 0                                        */
+} psca_large_args;
+
+size_t psca_large_workspace_bytes(const psca_large_args* a);
+/* Device addresses (inside the workspace) of the per-iteration exchange
+ * buffers: dsig (dsig_len doubles, summed over ranks) and red (red[0] summed,
+ * red[1] min-reduced over ranks). */
+int psca_large_exchange(const psca_large_args* a, void* workspace, double** dsig,
+                        size_t* dsig_len, double** red);
+/* Device address of the stop flag (int, 0 = continue) inside the workspace;
+ * written through flag_dev (an int** passed as void*). */
+int psca_large_flag(const psca_large_args* a, void* workspace, int* flag_dev);
+int psca_large_begin(const psca_large_args* a, void* workspace, size_t workspace_bytes,
+                     void* stream);
+int psca_large_columns(const psca_large_args* a, int k, void* workspace, size_t workspace_bytes,
+                       void* stream);
+int psca_large_factor(const psca_large_args* a, int k, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
 /* Number of kernel launches the last psca_solve on this thread issued
  * (reported as bench.py's gpu_launches). */
 int psca_last_launch_count(void);

@@ -27,6 +27,7 @@
 //
 // All arithmetic is IEEE float64.  Reductions use fixed orders (no float
 // atomics), so reruns are bit-identical.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -1016,6 +1017,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
 }
 
 #include "psca_fast.cuh"
+#include "psca_large.cuh"
 
 // ---------------------------------------------------------------------------
 // empirical covariance (HERK): Sigma_hat = Y Y^H / M
@@ -1348,6 +1350,126 @@ int resolved_chunks(const psca_solve_args* a) {
     return a->n_chunks > 0 ? fit_chunks(a->n_chunks, a->N) : auto_chunks(a->B, a->N);
 }
 
+// ---------------------------------------------------------------------------
+// large-L host side
+// ---------------------------------------------------------------------------
+struct LargeLayout {
+    double2* frags;
+    double* q_part;
+    double* r_part;
+    double* v;
+    double* pgrad;
+    double* red_part;
+    double2* dsig_part;
+    double2* dsig;
+    double* red;
+    double2* dmat;
+    double2* Xg;
+    double2* Gg;
+    double2* Ag;
+    double* inst;
+    int* flag;
+    int LP, NRB, NBLK, n_red, ks, ntiles;
+    size_t total;
+};
+
+int large_lp(int L) { return ((L + 31) / 32) * 32; }
+
+LargeLayout large_layout(const psca_large_args* a, void* ws) {
+    LargeLayout l;
+    l.LP = large_lp(a->L);
+    l.NRB = l.LP / 4;
+    l.NBLK = rebuild_block_count(l.NRB);
+    l.n_red = (a->N + NT - 1) / NT;
+    l.ntiles = 0;
+    for (int rt = 0; rt < l.LP / QL_RT; ++rt) l.ntiles += (32 * rt + 31) / 64 + 1;
+    l.ks = (2 * 148 + l.ntiles - 1) / l.ntiles;
+    const int max_ks = (a->N + RL_NC - 1) / RL_NC;
+    if (l.ks > max_ks) l.ks = max_ks;
+    if (l.ks < 1) l.ks = 1;
+    Carve cv{static_cast<char*>(ws)};
+    const size_t NB = (size_t)l.NRB * (l.NRB + 1);
+    l.frags = cv.take<double2>(NB * FRAG_SLOTS * 16);
+    l.q_part = cv.take<double>((size_t)(l.LP / QL_RT) * a->N * 8);
+    l.r_part = cv.take<double>((size_t)(l.LP / QL_RT) * a->N * 8);
+    l.v = cv.take<double>((size_t)a->N * 8);
+    l.pgrad = cv.take<double>((size_t)a->N * 8);
+    l.red_part = cv.take<double>((size_t)l.n_red * 2 * 8);
+    l.dsig_part = cv.take<double2>((size_t)l.ks * l.NBLK * 32 * 16);
+    l.dsig = cv.take<double2>((size_t)l.NBLK * 32 * 16);
+    l.red = cv.take<double>(4 * 8);
+    l.dmat = cv.take<double2>((size_t)a->L * a->L * 16);
+    l.Xg = cv.take<double2>((size_t)l.LP * l.LP * 16);
+    l.Gg = cv.take<double2>((size_t)l.LP * l.LP * 16);
+    l.Ag = cv.take<double2>((size_t)l.LP * l.LP * 16);
+    l.inst = cv.take<double>(4 * 8);
+    l.flag = cv.take<int>(sizeof(int));
+    l.total = cv.off;
+    return l;
+}
+
+LargeArgs large_kargs(const psca_large_args* a, const LargeLayout& l, int k) {
+    LargeArgs g{};
+    g.kind = a->kind; g.N = a->N; g.L = a->L; g.LP = l.LP; g.NRB = l.NRB; g.T = a->max_iter;
+    g.n_antennas = a->n_antennas; g.record_objective = a->record_objective && a->objective;
+    g.k = k; g.tol = a->tol; g.noise = a->noise;
+    g.pilots = reinterpret_cast<const double2*>(a->pilots); g.gains = a->gains;
+    g.emp_cov = reinterpret_cast<const double2*>(a->emp_cov); g.steps = a->steps;
+    g.prior_lin = a->prior_lin; g.prior_p = a->prior_p; g.eff = a->eff;
+    const bool even = ((k < 0 ? 0 : k) % 2) == 0;
+    g.x_cur = even ? a->x_a : a->x_b;
+    g.x_next = even ? a->x_b : a->x_a;
+    g.iterates = a->iterates; g.update_norm = a->update_norm;
+    g.objective = g.record_objective ? a->objective : nullptr;
+    g.status = a->status; g.n_iter = a->n_iter; g.cond_est = a->cond_est;
+    g.frags = l.frags; g.q_part = l.q_part; g.r_part = l.r_part; g.v = l.v; g.pgrad = l.pgrad;
+    g.red_part = l.red_part; g.n_red = l.n_red; g.dsig_part = l.dsig_part; g.ks = l.ks;
+    g.n_rtiles_lower = l.ntiles; g.dsig = l.dsig; g.red = l.red; g.dmat = l.dmat; g.Xg = l.Xg;
+    g.Gg = l.Gg; g.Ag = l.Ag; g.inst = l.inst; g.flag = l.flag;
+    return g;
+}
+
+int check_large_args(const psca_large_args* a) {
+    if (!a || a->N < 1 || a->L < 1 || a->max_iter < 0 || a->n_antennas < 1) return PSCA_E_ARG;
+    if (a->kind < PSCA_ML_K || a->kind > PSCA_MAP_UR) return PSCA_E_ARG;
+    if (a->L > 256) return PSCA_E_UNSUPPORTED;
+    if (!a->pilots || !a->emp_cov || !a->x_a || !a->x_b || !a->status || !a->n_iter ||
+        !a->steps || !a->update_norm || !(a->noise > 0))
+        return PSCA_E_ARG;
+    if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_K && !a->prior_lin) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_UR && !a->prior_p) return PSCA_E_ARG;
+    return PSCA_OK;
+}
+
+#define PSCA_K(launch)                                        \
+    do {                                                      \
+        launch;                                               \
+        ++g_launches;                                         \
+        if (!ok_or_record(cudaGetLastError())) return PSCA_E_CUDA; \
+    } while (0)
+
+int large_factor_chain(const LargeArgs& g, const LargeLayout& l, const double* x_new,
+                       cudaStream_t st) {
+    const int nblk32 = l.NBLK * 32;
+    if (g.kind == PSCA_MAP_UR || (g.kind == PSCA_MAP_K && g.record_objective))
+        PSCA_K((prior_large<<<1, NT, 0, st>>>(g, x_new)));
+    PSCA_K((assemble_large<<<(nblk32 + NT - 1) / NT, NT, 0, st>>>(g)));
+    PSCA_K((finish_sigma_large<<<(l.LP * l.LP + NT - 1) / NT, NT, 0, st>>>(g)));
+    PSCA_K((frob_large<<<1, NT, 0, st>>>(g)));
+    {
+        const size_t sm = (size_t)2 * l.LP * 16;
+        PSCA_K((gj_cluster<<<GJ_CL, GJ_NT, sm, st>>>(g)));
+    }
+    if (g.record_objective) PSCA_K((trace_large<<<1, NT, 0, st>>>(g)));
+    const int nbl = l.LP / 2;
+    PSCA_K((gemm_large<0><<<(nbl * nbl + NT - 1) / NT, NT, 0, st>>>(g)));
+    PSCA_K((gemm_large<1><<<(nbl * (nbl + 1) / 2 + NT - 1) / NT, NT, 0, st>>>(g)));
+    const int nb8 = l.NRB * (l.NRB + 1) * 8;
+    PSCA_K((pack_large<<<(nb8 + NT - 1) / NT, NT, 0, st>>>(g)));
+    return PSCA_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1615,6 +1737,94 @@ int psca_eval_objective(const double* sigma, const double* sigma_inv, const doub
     fa.out_vec = out; fa.status = status; fa.scratch = static_cast<double2*>(workspace);
     if (launch_factor<FAC_OBJECTIVE>(fa, g, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return PSCA_E_CUDA;
+    return PSCA_OK;
+}
+
+size_t psca_large_workspace_bytes(const psca_large_args* a) {
+    if (check_large_args(a) != PSCA_OK) return 0;
+    return large_layout(a, nullptr).total;
+}
+
+int psca_large_exchange(const psca_large_args* a, void* workspace, double** dsig,
+                        size_t* dsig_len, double** red) {
+    if (check_large_args(a) != PSCA_OK || !workspace) return PSCA_E_ARG;
+    LargeLayout l = large_layout(a, workspace);
+    if (dsig) *dsig = reinterpret_cast<double*>(l.dsig);
+    if (dsig_len) *dsig_len = (size_t)l.NBLK * 32 * 2;
+    if (red) *red = l.red;
+    return PSCA_OK;
+}
+
+int psca_large_begin(const psca_large_args* a, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    int rc = check_large_args(a);
+    if (rc != PSCA_OK) return rc;
+    LargeLayout l = large_layout(a, workspace);
+    if (!workspace || workspace_bytes < l.total) return PSCA_E_WORKSPACE;
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(a->x_a, 0, (size_t)a->N * 8, st);
+    cudaMemsetAsync(a->status, 0, sizeof(int), st);
+    cudaMemsetAsync(a->n_iter, 0, sizeof(int), st);
+    cudaMemsetAsync(l.flag, 0, sizeof(int), st);
+    cudaMemsetAsync(l.inst, 0, 4 * 8, st);
+    cudaMemsetAsync(l.Xg, 0, (size_t)l.LP * l.LP * 16, st);
+    cudaMemsetAsync(a->update_norm, 0, (size_t)(a->max_iter > 0 ? a->max_iter : 1) * 8, st);
+    if (a->iterates) cudaMemsetAsync(a->iterates, 0, (size_t)a->N * 8, st);
+    if (a->cond_est) cudaMemsetAsync(a->cond_est, 0, 8, st);
+    LargeArgs g = large_kargs(a, l, -1);
+    return large_factor_chain(g, l, a->x_a, st);
+}
+
+int psca_large_columns(const psca_large_args* a, int k, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+    int rc = check_large_args(a);
+    if (rc != PSCA_OK) return rc;
+    if (k < 0 || k >= a->max_iter) return PSCA_E_ARG;
+    LargeLayout l = large_layout(a, workspace);
+    if (!workspace || workspace_bytes < l.total) return PSCA_E_WORKSPACE;
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LargeArgs g = large_kargs(a, l, k);
+    {
+        constexpr size_t stage = (size_t)(QL_KC * QL_NC + 8 * 8 * FRAG_SLOTS) * 16;
+        const size_t sm = 2 * stage + (size_t)NWARP * QL_NC * 2 * 8;
+        auto kfn = quad_large;
+        if (!ok_or_record(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sm)))
+            return PSCA_E_CUDA;
+        dim3 grid((a->N + QL_NC - 1) / QL_NC, l.LP / QL_RT);
+        ProfScope prof(st, 0);
+        PSCA_K((quad_large<<<grid, NT, sm, st>>>(g)));
+    }
+    PSCA_K((update_large<<<l.n_red, NT, 0, st>>>(g)));
+    {
+        const size_t sm = (size_t)(32 + 64) * RL_NC * 16;
+        PSCA_K((rebuild_large<<<dim3(l.ntiles, l.ks), NT, sm, st>>>(g)));
+    }
+    PSCA_K((reduce_large<<<(l.NBLK * 32 + NT - 1) / NT, NT, 0, st>>>(g)));
+    return PSCA_OK;
+}
+
+int psca_large_factor(const psca_large_args* a, int k, void* workspace, size_t workspace_bytes,
+                      void* stream) {
+    int rc = check_large_args(a);
+    if (rc != PSCA_OK) return rc;
+    if (k < 0 || k >= a->max_iter) return PSCA_E_ARG;
+    LargeLayout l = large_layout(a, workspace);
+    if (!workspace || workspace_bytes < l.total) return PSCA_E_WORKSPACE;
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LargeArgs g = large_kargs(a, l, k);
+    ProfScope prof(st, 1);
+    PSCA_K((finalize_large<<<1, 1, 0, st>>>(g)));
+    return large_factor_chain(g, l, g.x_next, st);
+}
+
+int psca_large_flag(const psca_large_args* a, void* workspace, int* flag_dev) {
+    if (check_large_args(a) != PSCA_OK || !workspace || !flag_dev) return PSCA_E_ARG;
+    LargeLayout l = large_layout(a, workspace);
+    *reinterpret_cast<int**>(flag_dev) = l.flag;
     return PSCA_OK;
 }
 

@@ -1,0 +1,678 @@
+// psca_large.cuh -- large pilot length (80 < L <= 256) PSCA path, host-driven
+// step loop (included by psca.cu inside its anonymous namespace).
+//
+// At L = 256 (BASELINE config 4: N = 100,000, one instance) neither the P'/A'
+// fragments (1.6 MB) nor a useful S tile fit in SMEM, so the column pass is a
+// GEMM-tiled pipeline:
+//   quad_large     output tile = 32 complex rows (8 row blocks, one per warp) x
+//                  64 columns; K chunks of 16 complex rows of S and the matching
+//                  fragment blocks are cp.async double-buffered; fused epilogue
+//                  s^T T over the tile's rows -> per-row-tile partial q, r
+//   update_large   per column: q, r = fixed-order sum of the row-tile partials,
+//                  the fused per-device update, rebuild weight v, per-CTA
+//                  (dx2, min q) reductions
+//   rebuild_large  lower C-block tiles (8 row blocks x 8 column blocks) x column
+//                  splits; per 32-column chunk the moving columns (v != 0) are
+//                  ballot-compacted into SMEM and multiplied on DMMA
+//   reduce_large   fixed-order sums of the split partials (the rank-local Sigma
+//                  increment, in C-fragment form) and of the (dx2, min q)
+//                  partials -> the exchange buffer that multi-GPU column
+//                  sharding all-reduces (NCCL) between psca_large_columns and
+//                  psca_large_factor
+// and the factorisation:
+//   finalize_large one thread: q-floor guard, update norm, objective, tol stop
+//   assemble_large D_{k+1} = (1 - rho_k) D_k + increment; Sigma = D + sigma^2 I
+//   gj_cluster     Hermitian sweep Gauss-Jordan over an 8-CTA thread-block
+//                  cluster: lower 2x2 blocks in registers across 8 x 1024
+//                  threads, the pivot column broadcast into every CTA's SMEM
+//                  through DSMEM, one cluster barrier per pivot
+//   gemm_large     G = Sigma_hat P and A = P G (lower 2x2 blocks)
+//   pack_large     P'/A' fragments (same layout as the small-L path)
+
+constexpr int QL_NC = 64;    // columns per quad tile
+constexpr int QL_KC = 16;    // complex rows per K chunk (8 k-steps)
+constexpr int QL_RT = 32;    // complex rows per row tile (8 row blocks)
+constexpr int RL_NC = 32;    // columns per rebuild chunk
+constexpr int GJ_CL = 8;     // CTAs per GJ cluster
+constexpr int GJ_NT = 1024;  // threads per GJ CTA
+
+struct LargeArgs {
+    int kind, N, L, LP, NRB, T, n_antennas, record_objective, k;
+    double tol, noise;
+    const double2* pilots;      // [L][N] (this rank's columns)
+    const double* gains;        // [N]
+    const double2* emp_cov;     // [L][L]
+    const double* steps;        // [T]
+    const double* prior_lin;    // [N]
+    const double* prior_p;      // [N]
+    psca_eff_prior eff;
+    const double* x_cur;
+    double* x_next;
+    double* iterates;           // [T+1][N] or null
+    double* update_norm;        // [T]
+    double* objective;          // [T] or null
+    int* status;                // [1]
+    int* n_iter;                // [1]
+    double* cond_est;           // [1]
+    // workspace
+    double2* frags;             // [NB][24]
+    double* q_part;             // [LP/32][N]
+    double* r_part;             // [LP/32][N]
+    double* v;                  // [N]
+    double* pgrad;              // [N]
+    double* red_part;           // [n_red][2]
+    int n_red;
+    double2* dsig_part;         // [ks][NBLK][32]
+    int ks, n_rtiles_lower;
+    double2* dsig;              // [NBLK][32]   exchange buffer (all-reduced over ranks)
+    double* red;                // [4]          exchange: dx2 (sum), min q (min)
+    double2* dmat;              // [L][L] D
+    double2* Xg;                // [LP][LP] Sigma, then P
+    double2* Gg;                // [LP][LP]
+    double2* Ag;                // [LP][LP]
+    double* inst;               // [4] frob, logdet, trace, prior value
+    int* flag;                  // [1] finalize decision
+};
+
+__device__ __forceinline__ int lblock_base(int i) {   // rebuild C-block index of (i, 0)
+    int s = 0;
+    for (int t = 0; t < i; ++t) s += (4 * t + 3) / 8 + 1;
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT, 2) quad_large(LargeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* sm = reinterpret_cast<double2*>(smem_raw);
+    constexpr int SB = QL_KC * QL_NC;          // S chunk
+    constexpr int FB = 8 * 8 * FRAG_SLOTS;     // fragment chunk
+    constexpr int STAGE = SB + FB;
+    double* qr = reinterpret_cast<double*>(sm + 2 * STAGE);   // [8 warps][64][2]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const int rt = blockIdx.y, col0 = blockIdx.x * QL_NC;
+    const int i = 8 * rt + warp;              // this warp's row block
+    const int nkk = 2 * (i + 1);
+    const int nchunks = 2 * rt + 2;
+    const int fslot = frag_lane_slot(lane);
+
+    auto stage = [&](int c, double2* buf) {
+        double2* Sb = buf;
+        double2* Fb = buf + SB;
+        for (int e = tid; e < SB; e += NT) {
+            const int m = e / QL_NC, n = e % QL_NC;
+            const int gm = QL_KC * c + m, col = col0 + n;
+            const bool ok = gm < a.L && col < a.N;
+            const double2* src = ok ? a.pilots + (size_t)gm * a.N + col : a.pilots;
+            cp_async16(Sb + m * QL_NC + (n ^ swz(m)), src, ok ? 16 : 0);
+        }
+        for (int e = tid; e < FB; e += NT) {
+            const int rb = e / (8 * FRAG_SLOTS), rem = e % (8 * FRAG_SLOTS);
+            const int kl = rem / FRAG_SLOTS, sl = rem % FRAG_SLOTS;
+            const int ib = 8 * rt + rb, kk = 8 * c + kl;
+            const bool ok = ib < a.NRB && kk < 2 * (ib + 1);
+            const double2* src = ok ? a.frags + ((size_t)ib * (ib + 1) + kk) * FRAG_SLOTS + sl
+                                    : a.frags;
+            cp_async16(Fb + e, src, ok ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+
+    double T[8][2], U[8][2];
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb) T[cb][0] = T[cb][1] = U[cb][0] = U[cb][1] = 0.0;
+
+    stage(0, sm);
+    for (int c = 0; c < nchunks; ++c) {
+        double2* buf = sm + (c & 1) * STAGE;
+        if (c + 1 < nchunks) {
+            stage(c + 1, sm + ((c + 1) & 1) * STAGE);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* Sd = reinterpret_cast<const double*>(buf);
+        const double2* Fb = buf + SB + warp * 8 * FRAG_SLOTS + fslot;
+#pragma unroll
+        for (int kl = 0; kl < 8; ++kl) {
+            if (8 * c + kl < nkk) {
+                const double2 pa = Fb[kl * FRAG_SLOTS];
+                const int m = 2 * kl + (c4 >> 1);
+#pragma unroll
+                for (int cb = 0; cb < 8; ++cb) {
+                    const int n = 8 * cb + r8;
+                    const double bv = Sd[2 * (m * QL_NC + (n ^ swz(m))) + (c4 & 1)];
+                    dmma(T[cb], pa.x, bv);
+                    dmma(U[cb], pa.y, bv);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // ---- epilogue: q += sum_rows S_real * T over this tile's rows ------------
+    double2* Se = sm;   // [32][64] rows 32 rt ..
+    for (int e = tid; e < QL_RT * QL_NC; e += NT) {
+        const int m = e / QL_NC, n = e % QL_NC;
+        const int gm = QL_RT * rt + m, col = col0 + n;
+        const bool ok = gm < a.L && col < a.N;
+        const double2* src = ok ? a.pilots + (size_t)gm * a.N + col : a.pilots;
+        cp_async16(Se + m * QL_NC + (n ^ swz(m)), src, ok ? 16 : 0);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    {
+        const double* Sd = reinterpret_cast<const double*>(Se);
+        const int lr = 4 * warp + (r8 >> 1), p = r8 & 1;
+#pragma unroll
+        for (int cb = 0; cb < 8; ++cb) {
+            const int n0 = 8 * cb + 2 * c4;
+            const double s0 = Sd[2 * (lr * QL_NC + (n0 ^ swz(lr))) + p];
+            const double s1 = Sd[2 * (lr * QL_NC + ((n0 + 1) ^ swz(lr))) + p];
+            double q0 = s0 * T[cb][0], q1 = s1 * T[cb][1];
+            double r0 = s0 * U[cb][0], r1 = s1 * U[cb][1];
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                q0 += __shfl_xor_sync(0xffffffffu, q0, o);
+                q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+                r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+                r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+            }
+            if (r8 == 0) {
+                double* d = qr + (warp * QL_NC + n0) * 2;
+                d[0] = q0; d[1] = r0; d[2] = q1; d[3] = r1;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid < QL_NC) {
+        const int col = col0 + tid;
+        if (col < a.N) {
+            double q = 0.0, r = 0.0;
+            for (int w = 0; w < NWARP; ++w) {
+                q += qr[(w * QL_NC + tid) * 2];
+                r += qr[(w * QL_NC + tid) * 2 + 1];
+            }
+            a.q_part[(size_t)rt * a.N + col] = q;
+            a.r_part[(size_t)rt * a.N + col] = r;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) update_large(LargeArgs a) {
+    __shared__ double sred[2 * NWARP];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = blockIdx.x * NT + tid;
+    const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
+    const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
+    const double rho = a.steps[a.k];
+    const double omr = __dsub_rn(1.0, rho);
+    double dx2 = 0.0, mq = INFINITY;
+    if (n < a.N) {
+        double q = 0.0, r = 0.0;
+        for (int t = 0; t < a.LP / QL_RT; ++t) {
+            q += a.q_part[(size_t)t * a.N + n];
+            r += a.r_part[(size_t)t * a.N + n];
+        }
+        const double x = a.x_cur[n];
+        const double g = known ? a.gains[n] : 1.0;
+        const double diff = __dsub_rn(q, r);
+        double grad;
+        if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
+        else if (a.kind == PSCA_MAP_K) grad = __dadd_rn(__dmul_rn(g, diff), a.prior_lin[n]);
+        else if (a.kind == PSCA_ML_UD) grad = diff;
+        else grad = __dadd_rn(diff, a.pgrad[n]);
+        const double gq = known ? __dmul_rn(g, q) : q;
+        const double coef = __dmul_rn(gq, gq);
+        const double cand = np_clip(__dsub_rn(x, __ddiv_rn(grad, coef)), 0.0, hi);
+        const double rc = __dmul_rn(rho, cand);
+        const double xn = __dadd_rn(__dmul_rn(omr, x), rc);
+        a.x_next[n] = xn;
+        if (a.iterates) a.iterates[(size_t)(a.k + 1) * a.N + n] = xn;
+        a.v[n] = known ? __dmul_rn(rc, g) : rc;
+        const double d = __dsub_rn(xn, x);
+        dx2 = d * d;
+        mq = q;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        dx2 += __shfl_xor_sync(0xffffffffu, dx2, o);
+        const double t = __shfl_xor_sync(0xffffffffu, mq, o);
+        mq = (t < mq) ? t : mq;
+    }
+    if (lane == 0) {
+        sred[2 * warp] = dx2;
+        sred[2 * warp + 1] = mq;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0, m = INFINITY;
+        for (int w = 0; w < NWARP; ++w) {
+            s += sred[2 * w];
+            m = (sred[2 * w + 1] < m) ? sred[2 * w + 1] : m;
+        }
+        a.red_part[2 * blockIdx.x] = s;
+        a.red_part[2 * blockIdx.x + 1] = m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// rebuild: blockIdx.x = lower tile (row tile rt of 8 row blocks, column group
+// cg of 8 column blocks, 64 cg <= 32 rt + 31), blockIdx.y = column split
+__global__ void __launch_bounds__(NT) rebuild_large(LargeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* WS = reinterpret_cast<double2*>(smem_raw);   // [32 rows][32 slots]
+    double2* SP = WS + 32 * RL_NC;                         // [64 rows][32 slots]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    int rt = 0, cg = 0;
+    {
+        int t = blockIdx.x;
+        for (rt = 0;; ++rt) {
+            const int ncg = (32 * rt + 31) / 64 + 1;
+            if (t < ncg) { cg = t; break; }
+            t -= ncg;
+        }
+    }
+    const int i = 8 * rt + warp;
+    const int per = (a.N + gridDim.y - 1) / gridDim.y;
+    const int c_begin = blockIdx.y * per, c_end = min(a.N, c_begin + per);
+    double acc[8][2];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) acc[jj][0] = acc[jj][1] = 0.0;
+    const int p = r8 & 1, q = c4 & 1, cpr = c4 >> 1;
+    const unsigned long long wsgn = (p & q) ? 0x8000000000000000ull : 0ull;
+    const int la = 4 * warp + (r8 >> 1);   // local WS row of the A fragment
+
+    for (int c0 = c_begin; c0 < c_end; c0 += RL_NC) {
+        const int col = c0 + lane;
+        const double v = (col < c_end) ? a.v[col] : 0.0;
+        const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
+        if (mask == 0u) continue;                          // CTA-uniform (same v)
+        const int nnz = __popc(mask);
+        const int pos = __popc(mask & ((1u << lane) - 1u));
+        __syncthreads();                                   // previous chunk consumed
+        for (int r = warp; r < 32; r += NWARP) {
+            const int gl = 32 * rt + r;
+            const int o = r * RL_NC + (pos ^ (2 * (r & 3)));
+            if (v != 0.0) {
+                const double2 s = (gl < a.L) ? a.pilots[(size_t)gl * a.N + col] : make_double2(0.0, 0.0);
+                WS[o] = make_double2(v * s.x, v * s.y);
+            }
+            if (lane == 0 && (nnz & 1)) WS[r * RL_NC + (nnz ^ (2 * (r & 3)))] = make_double2(0.0, 0.0);
+        }
+        for (int r = warp; r < 64; r += NWARP) {
+            const int gm = 64 * cg + r;
+            const int o = r * RL_NC + (pos ^ (2 * (r & 3)));
+            if (v != 0.0)
+                SP[o] = (gm < a.L) ? a.pilots[(size_t)gm * a.N + col] : make_double2(0.0, 0.0);
+            if (lane == 0 && (nnz & 1)) SP[r * RL_NC + (nnz ^ (2 * (r & 3)))] = make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        const double* Wd = reinterpret_cast<const double*>(WS);
+        const double* Pd = reinterpret_cast<const double*>(SP);
+        const int nk2 = (nnz + 1) >> 1;
+        for (int k2 = 0; k2 < nk2; ++k2) {
+            const int sa = la & 3;
+            const int na = (2 * k2 + cpr) ^ (2 * sa);
+            const double av = xsign(Wd[2 * (la * RL_NC + na) + (p ^ q)], wsgn);
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int lm = 8 * jj + r8;            // local SP row (m = 64 cg + lm)
+                const int nb = (2 * k2 + cpr) ^ (2 * (lm & 3));
+                const double bv = Pd[2 * (lm * RL_NC + nb) + q];
+                dmma(acc[jj], av, bv);
+            }
+        }
+    }
+    // ---- C fragments -> dsig_part[split][block][lane] -------------------------
+    const int base = lblock_base(i);
+    const int jmax = (4 * i + 3) / 8;
+    double2* out = a.dsig_part + (size_t)blockIdx.y * rebuild_block_count(a.NRB) * 32;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * cg + jj;
+        if (i < a.NRB && j <= jmax) out[(size_t)(base + j) * 32 + lane] = make_double2(acc[jj][0], acc[jj][1]);
+    }
+}
+
+// sums of the split partials -> exchange buffers (fixed orders)
+__global__ void __launch_bounds__(NT) reduce_large(LargeArgs a) {
+    const int nblk32 = rebuild_block_count(a.NRB) * 32;
+    const int e = blockIdx.x * NT + threadIdx.x;
+    if (e < nblk32) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int sp = 0; sp < a.ks; ++sp) {
+            const double2 v = a.dsig_part[(size_t)sp * nblk32 + e];
+            s.x += v.x;
+            s.y += v.y;
+        }
+        a.dsig[e] = s;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double s = 0.0, m = INFINITY;
+        for (int b = 0; b < a.n_red; ++b) {
+            s += a.red_part[2 * b];
+            m = (a.red_part[2 * b + 1] < m) ? a.red_part[2 * b + 1] : m;
+        }
+        a.red[0] = s;
+        a.red[1] = m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// factorisation
+// ---------------------------------------------------------------------------
+__global__ void finalize_large(LargeArgs a) {
+    // flag: 0 continue, 1 stop (frozen / done)
+    const int k = a.k;
+    const double* in = a.inst;
+    int flag = 0;
+    if (a.status[0] != PSCA_RUNNING) {
+        flag = 1;
+    } else if (a.red[1] < 0.5 * a.L / in[0]) {
+        a.status[0] = PSCA_QFLOOR;
+        a.n_iter[0] = k;
+        flag = 1;
+    } else {
+        const double un = sqrt(a.red[0]);
+        a.update_norm[k] = un;
+        if (a.objective) a.objective[k] = in[1] + in[2] + in[3];
+        a.n_iter[0] = k + 1;
+        if (un < a.tol) {
+            a.status[0] = PSCA_CONVERGED;
+            flag = 1;
+        } else if (k + 1 >= a.T) {
+            flag = 1;
+        }
+    }
+    a.flag[0] = flag;
+}
+
+// D_{k+1} = (1 - rho) D_k + increment (k >= 0), Sigma = D + sigma^2 I -> Xg
+// (a.k = -1: D = 0, Sigma = sigma^2 I)
+__global__ void __launch_bounds__(NT) assemble_large(LargeArgs a) {
+    if (a.flag[0]) return;
+    const int L = a.L, LP = a.LP;
+    const int nblk32 = rebuild_block_count(a.NRB) * 32;
+    const int e = blockIdx.x * NT + threadIdx.x;
+    const double omr = (a.k >= 0) ? __dsub_rn(1.0, a.steps[a.k]) : 0.0;
+    double* Dd = reinterpret_cast<double*>(a.dmat);
+    double* Xd = reinterpret_cast<double*>(a.Xg);
+    if (e < nblk32) {
+        const int blk = e >> 5, lane = e & 31;
+        int i = 0, base = 0;
+        while (base + (4 * i + 3) / 8 + 1 <= blk) { base += (4 * i + 3) / 8 + 1; ++i; }
+        const int j = blk - base;
+        const double2 s = (a.k >= 0) ? a.dsig[e] : make_double2(0.0, 0.0);
+        const int r8 = lane >> 2, c4 = lane & 3;
+        const int l = 4 * i + (r8 >> 1), p = r8 & 1;
+        const int m0 = 8 * j + 2 * c4;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int m = m0 + h;
+            if (l < L && m <= l) {
+                const size_t o = 2 * ((size_t)l * L + m) + p;
+                const double val = (a.k >= 0) ? fma(omr, Dd[o], h ? s.y : s.x) : 0.0;
+                Dd[o] = val;
+                Xd[2 * ((size_t)l * LP + m) + p] = val;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT) finish_sigma_large(LargeArgs a) {
+    if (a.flag[0]) return;
+    const int L = a.L, LP = a.LP;
+    const int e = blockIdx.x * NT + threadIdx.x;
+    if (e >= LP * LP) return;
+    const int i = e / LP, j = e % LP;
+    double2* X = a.Xg;
+    if (i >= L || j >= L) {
+        X[e] = make_double2(0.0, 0.0);
+    } else if (i < j) {
+        const double2 v = X[(size_t)j * LP + i];
+        X[e] = make_double2(v.x, -v.y);
+    } else if (i == j) {
+        X[e] = make_double2(X[e].x + a.noise, 0.0);
+    }
+}
+
+// Frobenius norm of Sigma and (optionally) the prior terms; one CTA
+__global__ void __launch_bounds__(NT) frob_large(LargeArgs a) {
+    __shared__ double sred[NWARP + 1];
+    if (a.flag[0]) return;
+    double s = 0.0;
+    for (int e = threadIdx.x; e < a.L * a.L; e += NT) {
+        const int i = e / a.L, j = e % a.L;
+        const double2 v = a.Xg[(size_t)i * a.LP + j];
+        s = fma(v.x, v.x, fma(v.y, v.y, s));
+    }
+    s = block_sum(s, sred);
+    if (threadIdx.x == 0) a.inst[0] = sqrt(s);
+}
+
+// Sweep-operator Gauss-Jordan on an 8-CTA cluster (see header comment).
+__global__ void __cluster_dims__(GJ_CL, 1, 1) __launch_bounds__(GJ_NT, 1)
+gj_cluster(LargeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* cbuf = reinterpret_cast<double2*>(smem_raw);   // [2][LP]
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    if (a.flag[0]) return;   // uniform across the cluster
+    const int L = a.L, LP = a.LP;
+    const int rank = (int)cl.block_rank();
+    const int gtid = rank * GJ_NT + threadIdx.x;
+    constexpr int GT = GJ_CL * GJ_NT;
+    const int nbl = LP / 2, nlb = nbl * (nbl + 1) / 2;
+    constexpr int SLMAX = 2;   // LP <= 256: 8256 lower blocks <= 2 * 8192
+    int bi[SLMAX], bj[SLMAX];
+    double2 v[SLMAX][2][2];
+#pragma unroll
+    for (int u = 0; u < SLMAX; ++u) {
+        const int t = gtid + GT * u;
+        if (t < nlb) lower_block(t, bi[u], bj[u]); else { bi[u] = -1; bj[u] = 0; }
+#pragma unroll
+        for (int di = 0; di < 2; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj) {
+                const int i = 2 * bi[u] + di, j = 2 * bj[u] + dj;
+                v[u][di][dj] = (bi[u] >= 0 && i < L && j < L && i >= j) ? a.Xg[(size_t)i * LP + j]
+                                                                       : make_double2(0.0, 0.0);
+            }
+    }
+    for (int e = threadIdx.x; e < 2 * LP; e += GJ_NT)
+        cbuf[e] = (e < L) ? a.Xg[(size_t)e * LP] : make_double2(0.0, 0.0);
+    cl.sync();
+    double logdet = 0.0;
+    bool ok = true;
+    for (int k = 0; k < L; ++k) {
+        const double2* cb = cbuf + (k & 1) * LP;
+        const int nxt = ((k + 1) & 1) * LP;
+        const double d = cb[k].x;   // identical copy in every CTA: a uniform decision
+        if (!(d > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (a.record_objective) logdet += log(d);
+        const double dinv = __drcp_rn(d);
+#pragma unroll
+        for (int u = 0; u < SLMAX; ++u) {
+            if (bi[u] < 0) continue;
+            const int i0 = 2 * bi[u], j0 = 2 * bj[u];
+            const double2 ci[2] = {cb[i0], cb[i0 + 1]};
+            const double2 cj[2] = {cb[j0], cb[j0 + 1]};
+#pragma unroll
+            for (int di = 0; di < 2; ++di)
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) {
+                    const int i = i0 + di, j = j0 + dj;
+                    const double2 o = v[u][di][dj];
+                    const double pr = ci[di].x * cj[dj].x + ci[di].y * cj[dj].y;
+                    const double pim = ci[di].y * cj[dj].x - ci[di].x * cj[dj].y;
+                    double nx = o.x - pr * dinv, ny = o.y - pim * dinv;
+                    const bool onrow = (i == k) || (j == k);
+                    nx = onrow ? o.x * dinv : nx;
+                    ny = onrow ? o.y * dinv : ny;
+                    nx = (i == k && j == k) ? -dinv : nx;
+                    ny = (i == k && j == k) ? 0.0 : ny;
+                    if (i < j) { nx = 0.0; ny = 0.0; }
+                    v[u][di][dj] = make_double2(nx, ny);
+                    int dst = -1;
+                    double2 val;
+                    if (j == k + 1 && i >= j && i < L) { dst = i; val = make_double2(nx, ny); }
+                    if (i == k + 1 && j < i) { dst = j; val = make_double2(nx, -ny); }
+                    if (dst >= 0) {
+#pragma unroll
+                        for (int r = 0; r < GJ_CL; ++r) {
+                            double2* rb = cl.map_shared_rank(cbuf, r);
+                            rb[nxt + dst] = val;
+                        }
+                    }
+                }
+        }
+        cl.sync();
+    }
+    // a failed pivot is seen identically by every thread of every CTA
+    if (!ok) {
+        if (rank == 0 && threadIdx.x == 0) {
+            a.status[0] = PSCA_CHOL_FAIL;
+            if (a.cond_est) a.cond_est[0] = INFINITY;
+        }
+        return;
+    }
+    if (rank == 0 && threadIdx.x == 0) a.inst[1] = logdet;
+    // P = -(swept), full Hermitian, into Xg
+#pragma unroll
+    for (int u = 0; u < SLMAX; ++u) {
+        if (bi[u] < 0) continue;
+#pragma unroll
+        for (int di = 0; di < 2; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj) {
+                const int i = 2 * bi[u] + di, j = 2 * bj[u] + dj;
+                if (i >= j) {
+                    const double2 pv = (i < L && j < L) ? make_double2(-v[u][di][dj].x, -v[u][di][dj].y)
+                                                        : make_double2(0.0, 0.0);
+                    a.Xg[(size_t)i * LP + j] = (i == j) ? make_double2(pv.x, 0.0) : pv;
+                    if (i != j) a.Xg[(size_t)j * LP + i] = make_double2(pv.x, -pv.y);
+                }
+            }
+    }
+}
+
+// G = Sigma_hat P (all 2x2 blocks, MODE 0) or A = P G (lower 2x2 blocks, MODE 1)
+template <int MODE>
+__global__ void __launch_bounds__(NT) gemm_large(LargeArgs a) {
+    if (a.flag[0] || a.status[0] != PSCA_RUNNING) return;
+    const int L = a.L, LP = a.LP, nbl = LP / 2;
+    const int t = blockIdx.x * NT + threadIdx.x;
+    int bi, bj;
+    if (MODE == 0) {
+        if (t >= nbl * nbl) return;
+        bi = t / nbl;
+        bj = t % nbl;
+    } else {
+        if (t >= nbl * (nbl + 1) / 2) return;
+        lower_block(t, bi, bj);
+    }
+    const int i0 = 2 * bi, j0 = 2 * bj;
+    double2 c[2][2];
+#pragma unroll
+    for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) c[di][dj] = make_double2(0.0, 0.0);
+    for (int k = 0; k < L; ++k) {
+        double2 x0, x1, y0, y1;
+        if (MODE == 0) {
+            x0 = (i0 < L) ? __ldg(a.emp_cov + (size_t)i0 * L + k) : make_double2(0.0, 0.0);
+            x1 = (i0 + 1 < L) ? __ldg(a.emp_cov + (size_t)(i0 + 1) * L + k) : make_double2(0.0, 0.0);
+            y0 = a.Xg[(size_t)k * LP + j0];
+            y1 = a.Xg[(size_t)k * LP + j0 + 1];
+        } else {
+            x0 = a.Xg[(size_t)i0 * LP + k];
+            x1 = a.Xg[(size_t)(i0 + 1) * LP + k];
+            y0 = a.Gg[(size_t)k * LP + j0];
+            y1 = a.Gg[(size_t)k * LP + j0 + 1];
+        }
+        c[0][0] = cfma(x0, y0, c[0][0]);
+        c[0][1] = cfma(x0, y1, c[0][1]);
+        c[1][0] = cfma(x1, y0, c[1][0]);
+        c[1][1] = cfma(x1, y1, c[1][1]);
+    }
+    double2* out = (MODE == 0) ? a.Gg : a.Ag;
+#pragma unroll
+    for (int di = 0; di < 2; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 2; ++dj) out[(size_t)(i0 + di) * LP + j0 + dj] = c[di][dj];
+}
+
+// trace(P Sigma_hat) for the objective; one CTA
+__global__ void __launch_bounds__(NT) trace_large(LargeArgs a) {
+    __shared__ double sred[NWARP + 1];
+    if (a.flag[0] || a.status[0] != PSCA_RUNNING) return;
+    double s = 0.0;
+    for (int e = threadIdx.x; e < a.L * a.L; e += NT) {
+        const int i = e / a.L, j = e % a.L;
+        const double2 pv = a.Xg[(size_t)i * a.LP + j];
+        const double2 ev = a.emp_cov[(size_t)j * a.L + i];
+        s = fma(pv.x, ev.x, fma(-pv.y, ev.y, s));
+    }
+    s = block_sum(s, sred);
+    if (threadIdx.x == 0) a.inst[2] = s;
+}
+
+// prior terms at the new iterate (x_next of the finalised iteration, or 0)
+__global__ void __launch_bounds__(NT) prior_large(LargeArgs a, const double* xv) {
+    __shared__ double sred[NWARP + 1];
+    if (a.flag[0]) return;
+    double acc = 0.0;
+    const int n = blockIdx.x * NT + threadIdx.x;   // grid-stride not needed: one pass
+    for (int m = n; m < a.N; m += gridDim.x * NT) {
+        const double x = xv[m];
+        if (a.kind == PSCA_MAP_UR) {
+            double dens, der;
+            eff_density(x, a.prior_p[m], a.eff, dens, der);
+            const double mag = a.eff.dead_zone_grad;
+            a.pgrad[m] = (dens <= 1e-300) ? ((x <= a.eff.g_low / 2.0) ? 1.0 : -1.0) * (mag / a.n_antennas)
+                                          : -np_clip(der / dens, -mag, mag) / a.n_antennas;
+            if (a.record_objective) acc += log(dens > 1e-300 ? dens : 1e-300);
+        } else if (a.kind == PSCA_MAP_K) {
+            acc = fma(a.prior_lin[m], x, acc);
+        }
+    }
+    if (gridDim.x == 1 && a.record_objective) {
+        acc = block_sum(acc, sred);
+        if (threadIdx.x == 0)
+            a.inst[3] = (a.kind == PSCA_MAP_K) ? acc : (a.kind == PSCA_MAP_UR ? -acc / a.n_antennas : 0.0);
+    }
+}
+
+__global__ void __launch_bounds__(NT) pack_large(LargeArgs a) {
+    if (a.flag[0] || a.status[0] != PSCA_RUNNING) return;
+    const int NB = a.NRB * (a.NRB + 1);
+    const int e = blockIdx.x * NT + threadIdx.x;
+    if (e >= NB * 8) return;
+    const int blk = e >> 3, a4 = (e >> 1) & 3, cc = e & 1;
+    int i = (int)((sqrt(4.0 * blk + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) > blk) --i;
+    while ((i + 1) * (i + 2) <= blk) ++i;
+    const int kk = blk - i * (i + 1);
+    const int l = 4 * i + a4, m = 2 * kk + cc;
+    double2 pv = make_double2(0.0, 0.0), av = make_double2(0.0, 0.0);
+    if (l < a.L && m <= l) {
+        pv = a.Xg[(size_t)l * a.LP + m];
+        av = a.Ag[(size_t)l * a.LP + m];
+        if (m < l) {
+            pv.x *= 2.0; pv.y *= 2.0; av.x *= 2.0; av.y *= 2.0;
+        } else {
+            pv.y = 0.0; av.y = 0.0;
+        }
+    }
+    const int ent = a4 * 2 + cc;
+    double* o = reinterpret_cast<double*>(a.frags) + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
+    o[0] = pv.x; o[1] = av.x;
+    o[2] = pv.y; o[3] = av.y;
+    o[4] = -pv.y; o[5] = -av.y;
+}

@@ -180,7 +180,17 @@ def prior_arrays(problem, n_devices: int, n_antennas: int) -> dict:
 
 
 ABORT_COND = "Sigma is numerically singular (estimated condition number {:.3e})"
+# The compiled / generic batched kernels cover L <= 128; larger pilot lengths
+# (BASELINE config 4: L = 256) run the GEMM-tiled step loop of large.py.
+MAX_L_BATCHED = 128
+
+
 ABORT_QFLOOR = "quadratic form underflow; inverse inconsistent"
+
+
+def use_large_path(pilot_len: int) -> bool:
+    import os
+    return pilot_len > MAX_L_BATCHED or os.environ.get("PSCA_FORCE_LARGE") == "1"
 
 
 def psca_run(problem, sample, schedule: StepSchedule | None = None, max_iter: int = 30,
@@ -210,28 +220,42 @@ def psca_run(problem, sample, schedule: StepSchedule | None = None, max_iter: in
     t1 = torch.cuda.Event(enable_timing=True) if torch.cuda.is_available() else None
     if t0 is not None:
         t0.record()
-    res = device.solve(problem.kind, np.asarray(sample.pilots)[None],
-                       np.asarray(sample.emp_cov)[None], np.array([sample.noise_power], float), m,
-                       steps, gains=np.asarray(sample.gains, dtype=float)[None] if problem.known_pathloss else None,
-                       max_iter=n_steps, tol=tol, record_objective=record_objective,
-                       record_iterates=True, **kw)
+    gains = np.asarray(sample.gains, dtype=float) if problem.known_pathloss else None
+    if use_large_path(sample.pilot_len):
+        from .large import psca_run_large
+        r = psca_run_large(problem.kind, np.asarray(sample.pilots), gains,
+                           np.asarray(sample.emp_cov), sample.noise_power, m, steps,
+                           max_iter=n_steps, tol=tol, record_objective=record_objective,
+                           record_iterates=True, **kw)
+        status, k_done = r["status"], r["n_iter"]
+        its_t, un_t, obj_t, x_t, cond = (r["iterates"], r["update_norm"], r["objective"],
+                                         r["x"], r["cond_est"])
+    else:
+        res = device.solve(problem.kind, np.asarray(sample.pilots)[None],
+                           np.asarray(sample.emp_cov)[None], np.array([sample.noise_power], float),
+                           m, steps, gains=gains[None] if gains is not None else None,
+                           max_iter=n_steps, tol=tol, record_objective=record_objective,
+                           record_iterates=True, **kw)
+        status = int(res["status"][0].item())
+        k_done = int(res["n_iter"][0].item())
+        its_t, un_t = res["iterates"][0, :k_done + 1], res["update_norm"][0, :k_done]
+        obj_t = res["objective"][0, :k_done] if record_objective else None
+        x_t, cond = res["x"][0], float(res["cond_est"][0].item())
     if t1 is not None:
         t1.record()
-    status = int(res["status"][0].item())
-    k_done = int(res["n_iter"][0].item())
-    its = res["iterates"][0, :k_done + 1].cpu().numpy()
+    its = its_t.cpu().numpy()
     trace.iterates = [its[i].copy() for i in range(k_done + 1)]
-    trace.update_norm = [float(v) for v in res["update_norm"][0, :k_done].cpu().numpy()]
+    trace.update_norm = [float(v) for v in un_t.cpu().numpy()]
     if record_objective:
-        trace.objective = [float(v) for v in res["objective"][0, :k_done].cpu().numpy()]
+        trace.objective = [float(v) for v in obj_t.cpu().numpy()]
     torch.cuda.synchronize()
     per = (t0.elapsed_time(t1) * 1e-3 / max(k_done, 1)) if t0 is not None else 0.0
     trace.wall_times = [per] * k_done
     if status == device.STATUS_CHOL_FAIL:
-        trace.meta["abort"] = ABORT_COND.format(float(res["cond_est"][0].item()))
+        trace.meta["abort"] = ABORT_COND.format(cond)
     elif status == device.STATUS_QFLOOR:
         trace.meta["abort"] = ABORT_QFLOOR
-    trace.final = res["x"][0].cpu().numpy().copy()
+    trace.final = x_t.cpu().numpy().copy()
     if (status in (device.STATUS_RUNNING,) and schedule.steps is not None
             and len(schedule.steps) < max_iter):
         raise IndexError("explicit schedule shorter than max_iter")
@@ -253,10 +277,37 @@ def psca_run_batch(problem, pilots, emp_cov, noise, n_antennas: int, gains=None,
     kw = prior_arrays(problem, n, n_antennas)
     if problem.known_pathloss and gains is None:
         raise DomainError("known-pathloss problems need the gains")
+    if use_large_path(pilots.shape[-2]):
+        return _batch_via_large(problem, pilots, emp_cov, noise, n_antennas, gains, steps,
+                                max_iter, tol, record_objective, kw)
     return device.solve(problem.kind, pilots, emp_cov, noise, n_antennas, steps,
                         gains=gains if problem.known_pathloss else None, max_iter=max_iter,
                         tol=tol, record_objective=record_objective, n_chunks=n_chunks, out=out,
                         **kw)
+
+
+def _batch_via_large(problem, pilots, emp_cov, noise, n_antennas, gains, steps, max_iter, tol,
+                     record_objective, kw):
+    """Large-L batches: one step-loop solve per instance (device tensors out)."""
+    import torch
+    from .large import psca_run_large
+    B = pilots.shape[0]
+    outs = []
+    for b in range(B):
+        g = gains[b] if gains is not None else None
+        outs.append(psca_run_large(problem.kind, pilots[b], g, emp_cov[b], float(noise[b]),
+                                   n_antennas, steps, max_iter=max_iter, tol=tol,
+                                   record_objective=record_objective, **kw))
+    dev = outs[0]["x"].device
+    un = torch.zeros((B, max_iter), dtype=torch.float64, device=dev)
+    for b, o in enumerate(outs):
+        un[b, :o["n_iter"]] = o["update_norm"]
+    return {"x": torch.stack([o["x"] for o in outs]), "update_norm": un,
+            "objective": None, "iterates": None,
+            "status": torch.tensor([o["status"] for o in outs], dtype=torch.int32, device=dev),
+            "n_iter": torch.tensor([o["n_iter"] for o in outs], dtype=torch.int32, device=dev),
+            "cond_est": torch.tensor([o["cond_est"] for o in outs], dtype=torch.float64, device=dev),
+            "launches": sum(o["launches"] for o in outs), "path": "large"}
 
 
 # -- elementwise helpers kept for API parity (estimators.py:176-200); the
