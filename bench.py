@@ -57,6 +57,9 @@ def parse_args():
                     help="CPU-baseline sample budget (seconds of solve time per worker)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="c1", choices=["c1", "c4"],
+                    help="c1 (headline, default) or c4 (one N=100000, L=256 instance, "
+                         "devices column-sharded over the ranks, NCCL all-reduce per iteration)")
     return ap.parse_args()
 
 
@@ -423,10 +426,84 @@ def ours_arm(args):
     return 0
 
 
+def c4_arm(args):
+    """BASELINE config 4: one huge instance, columns sharded over the ranks."""
+    import numpy as np
+    import torch
+    world, rank, local = dist_setup(args)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        group = dist.group.WORLD
+    else:
+        torch.cuda.set_device(0)
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2503_15259_b200 import estimators, large, scenes
+    cfg = scenes.BASELINE_CONFIGS["c4"]
+    T = args.iters or cfg.n_iter
+    s = scenes.make_scene(cfg, 0)
+    sl = large.column_shard(cfg.n_devices, rank, world)
+    steps = estimators.default_steps(T)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S = torch.from_numpy(np.ascontiguousarray(s.pilots[:, sl])).to(dev)
+    g = torch.from_numpy(np.ascontiguousarray(s.gains[sl])).to(dev)
+    E = torch.from_numpy(s.emp_cov).to(dev)
+
+    def run():
+        st = large.GpuLargeStepper("ml-k", S, g, E, 1.0, cfg.n_antennas, steps, max_iter=T)
+        return large.ShardedDriver(st, group=group).run(T), st.launches
+
+    for _ in range(max(args.warmup, 1)):
+        run()
+    torch.cuda.synchronize()
+    times = []
+    launches = 0
+    for _ in range(args.steps):
+        if group is not None:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res, nl = run()
+        e1.record()
+        torch.cuda.synchronize()
+        launches += nl
+        ms = e0.elapsed_time(e1)
+        if group is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        times.append(ms)
+    ms = sum(times) / len(times)
+    if rank == 0:
+        flops = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * T
+        print(json.dumps({
+            "metric": "c4 solve time (one instance, N=100000, L=256, T=50)",
+            "value": 1e3 / ms, "unit": "instances/s", "ms_per_step": ms,
+            "ms_per_iteration": ms / T, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE c4 scene)",
+            "config": {"workload": "c4: PSCA-MLE known pathloss, N=100000, L=256, M=512, "
+                                   "K=2500, T=50; devices column-sharded, NCCL all-reduce of "
+                                   "the Sigma increment per iteration",
+                       "parallelism": f"column shards x{world}"},
+            "algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
+            "gpu_launches": launches, "status": res["status"], "n_iter": res["n_iter"]}),
+            flush=True)
+    if group is not None:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config == "c4":
+        return c4_arm(args)
     return ours_arm(args)
 
 
