@@ -347,7 +347,11 @@ def ours_arm(args):
     ms = max_over_ranks(e0.elapsed_time(e1))
     value = world * B * args.steps / (ms * 1e-3)
     col_ms = prof["column_ms"] / max(prof["column_launches"], 1)
-    flops_launch = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * B
+    # algorithmic flops of the timed region spread over the column-family launches
+    # (one per iteration, two per iteration when the batch is split over two streams,
+    # one per solve for the persistent kernel)
+    flops_total = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * B * iters * args.steps
+    flops_launch = flops_total / max(prof["column_launches"], 1)
     achieved = flops_launch / (col_ms * 1e-3) / 1e12
     x_check = out["x"]
     finite = bool(torch.isfinite(x_check).all().item())
@@ -413,6 +417,8 @@ def ours_arm(args):
                 "column_ms_per_launch": col_ms,
                 "factor_ms_per_launch": prof["factor_ms"] / max(prof["factor_launches"], 1),
                 "column_share": prof["column_ms"] / max(prof["column_ms"] + prof["factor_ms"], 1e-9),
+                "column_launches": prof["column_launches"],
+                "path": out.get("path"),
             },
             "gpu_launches": launches,
             "clocks": clk.summary(),

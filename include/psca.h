@@ -178,7 +178,8 @@ int psca_large_factor(const psca_large_args* a, int k, void* workspace, size_t w
 int psca_last_launch_count(void);
 
 /* Execution path of the last psca_solve on this thread: 0 = two kernels per
- * iteration (column chunks), 1 = one persistent launch for the whole solve. */
+ * iteration (column chunks), 1 = one persistent launch for the whole solve,
+ * 2 = two kernels per iteration for each half batch on two internal streams. */
 int psca_last_path(void);
 
 /* Device timing of every column / factor kernel launched by this thread

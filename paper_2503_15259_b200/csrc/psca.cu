@@ -1225,7 +1225,7 @@ cudaError_t launch_solve_factor(const FacArgs& fa, const Geo& g, cudaStream_t st
     return launch_factor<FAC_SOLVE>(fa, g, st);
 }
 
-thread_local int g_last_path = 0;   // 0 two-kernel, 1 persistent
+thread_local int g_last_path = 0;   // 0 two-kernel, 1 persistent, 2 two-kernel on split streams
 
 // The persistent fused kernel is opt-in (PSCA_PERSISTENT=1): measured slower
 // than the two-kernel path on B200 (profiles/README.md, round 1).
@@ -1301,6 +1301,77 @@ cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     kfn<<<fa.B, NT, sm, st>>>(fa);
     ++g_launches;
     return cudaGetLastError();
+}
+
+bool split_disabled() {
+    static const bool off = [] {
+        const char* e = getenv("PSCA_NO_SPLIT");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
+
+// two non-blocking side streams + fork/join events per device (created once)
+cudaError_t side_streams(cudaStream_t (&ss)[2], cudaEvent_t* fork, cudaEvent_t (&join)[2]) {
+    struct Side {
+        bool init = false;
+        cudaStream_t s[2];
+        cudaEvent_t f, j[2];
+    };
+    static Side sides[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    Side& sd = sides[dev & 63];
+    if (!sd.init) {
+        for (int h = 0; h < 2; ++h) {
+            if ((e = cudaStreamCreateWithFlags(&sd.s[h], cudaStreamNonBlocking)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&sd.j[h], cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
+        if ((e = cudaEventCreateWithFlags(&sd.f, cudaEventDisableTiming)) != cudaSuccess) return e;
+        sd.init = true;
+    }
+    ss[0] = sd.s[0]; ss[1] = sd.s[1];
+    *fork = sd.f;
+    join[0] = sd.j[0]; join[1] = sd.j[1];
+    return cudaSuccess;
+}
+
+// views of instances [b0, b0 + Bh) of a solve (single chunk per instance)
+ColArgs sub_col(const ColArgs& c, int b0, int Bh, const Geo& g) {
+    ColArgs r = c;
+    const size_t N = c.N, L = c.L;
+    r.B = Bh;
+    r.pilots = c.pilots + (size_t)b0 * L * N;
+    if (c.gains) r.gains = c.gains + (size_t)b0 * N;
+    if (c.iterates) r.iterates = c.iterates + (size_t)b0 * (c.T + 1) * N;
+    r.frags = c.frags + (size_t)b0 * g.NB * FRAG_SLOTS;
+    r.sig_part = c.sig_part + (size_t)b0 * c.n_chunks * g.NBLK * 32;
+    r.red_part = c.red_part + (size_t)b0 * c.n_chunks * 4;
+    r.status = c.status + b0;
+    if (c.pgrad) r.pgrad = c.pgrad + (size_t)b0 * N;
+    return r;
+}
+
+FacArgs sub_fac(const FacArgs& f, int b0, int Bh, const Geo& g) {
+    FacArgs r = f;
+    const size_t N = f.N, L = f.L;
+    r.B = Bh;
+    r.noise = f.noise + b0;
+    r.emp_cov = f.emp_cov + (size_t)b0 * L * L;
+    r.sig_part = f.sig_part + (size_t)b0 * f.n_chunks * g.NBLK * 32;
+    r.red_part = f.red_part + (size_t)b0 * f.n_chunks * 4;
+    r.frags = f.frags + (size_t)b0 * g.NB * FRAG_SLOTS;
+    r.inst = f.inst + (size_t)b0 * 4;
+    r.status = f.status + b0;
+    r.n_iter = f.n_iter + b0;
+    if (f.cond_est) r.cond_est = f.cond_est + b0;
+    r.update_norm = f.update_norm + (size_t)b0 * f.T;
+    if (f.objective) r.objective = f.objective + (size_t)b0 * f.T;
+    if (f.scratch) r.scratch = f.scratch + (size_t)b0 * 2 * g.LP * (g.LP + 1);
+    if (f.pgrad) r.pgrad = f.pgrad + (size_t)b0 * N;
+    if (f.dmat) r.dmat = f.dmat + (size_t)b0 * L * L;
+    return r;
 }
 
 struct SolveLayout {
@@ -1589,14 +1660,58 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
         if (!ok_or_record(launch_persistent(ca, fa, lay.counter, g.NRB, st))) return PSCA_E_CUDA;
         return cudaGetLastError() == cudaSuccess ? PSCA_OK : PSCA_E_CUDA;
     }
-    fa.k_new = 0; fa.x_cur = xc; fa.x_next = xn;
-    if (!ok_or_record(launch_solve_factor(fa, g, st))) return PSCA_E_CUDA;
-    for (int k = 0; k < a->max_iter; ++k) {
-        ca.k = k; ca.x_cur = xc; ca.x_next = xn;
-        if (!ok_or_record(launch_solve_column(ca, g, n_chunks, st))) return PSCA_E_CUDA;
-        fa.k_new = k + 1; fa.x_cur = xc; fa.x_next = xn;
+    // Large batches: two half-batches on two internal streams, so the
+    // latency-bound factor kernel of one half runs under the column kernel of
+    // the other (1 column CTA + 2 factor CTAs fit one SM).
+    const bool split = n_chunks == 1 && a->B >= 4 * sm_count() && !split_disabled();
+    if (split) {
+        g_last_path = 2;
+        cudaStream_t ss[2];
+        cudaEvent_t ev_fork, ev_join[2];
+        if (!ok_or_record(side_streams(ss, &ev_fork, ev_join))) return PSCA_E_CUDA;
+        const int Bh[2] = {a->B / 2, a->B - a->B / 2};
+        const int b0[2] = {0, a->B / 2};
+        ColArgs ch[2];
+        FacArgs fh[2];
+        for (int h = 0; h < 2; ++h) {
+            ch[h] = sub_col(ca, b0[h], Bh[h], g);
+            fh[h] = sub_fac(fa, b0[h], Bh[h], g);
+        }
+        cudaEventRecord(ev_fork, st);
+        for (int h = 0; h < 2; ++h) cudaStreamWaitEvent(ss[h], ev_fork, 0);
+        for (int h = 0; h < 2; ++h) {
+            FacArgs f = fh[h];
+            f.k_new = 0; f.x_cur = xc + (size_t)b0[h] * a->N; f.x_next = xn + (size_t)b0[h] * a->N;
+            if (!ok_or_record(launch_solve_factor(f, g, ss[h]))) return PSCA_E_CUDA;
+        }
+        for (int k = 0; k < a->max_iter; ++k) {
+            for (int h = 0; h < 2; ++h) {
+                ColArgs c = ch[h];
+                c.k = k; c.x_cur = xc + (size_t)b0[h] * a->N; c.x_next = xn + (size_t)b0[h] * a->N;
+                if (!ok_or_record(launch_solve_column(c, g, n_chunks, ss[h]))) return PSCA_E_CUDA;
+            }
+            for (int h = 0; h < 2; ++h) {
+                FacArgs f = fh[h];
+                f.k_new = k + 1; f.x_cur = xc + (size_t)b0[h] * a->N;
+                f.x_next = xn + (size_t)b0[h] * a->N;
+                if (!ok_or_record(launch_solve_factor(f, g, ss[h]))) return PSCA_E_CUDA;
+            }
+            double* t = xc; xc = xn; xn = t;
+        }
+        for (int h = 0; h < 2; ++h) {
+            cudaEventRecord(ev_join[h], ss[h]);
+            cudaStreamWaitEvent(st, ev_join[h], 0);
+        }
+    } else {
+        fa.k_new = 0; fa.x_cur = xc; fa.x_next = xn;
         if (!ok_or_record(launch_solve_factor(fa, g, st))) return PSCA_E_CUDA;
-        double* t = xc; xc = xn; xn = t;
+        for (int k = 0; k < a->max_iter; ++k) {
+            ca.k = k; ca.x_cur = xc; ca.x_next = xn;
+            if (!ok_or_record(launch_solve_column(ca, g, n_chunks, st))) return PSCA_E_CUDA;
+            fa.k_new = k + 1; fa.x_cur = xc; fa.x_next = xn;
+            if (!ok_or_record(launch_solve_factor(fa, g, st))) return PSCA_E_CUDA;
+            double* t = xc; xc = xn; xn = t;
+        }
     }
     if (xc != a->x_out) {
         if (cudaMemcpyAsync(a->x_out, xc, BN * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)

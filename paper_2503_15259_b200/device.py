@@ -221,7 +221,8 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
     return {"x": x, "update_norm": un[:, :T], "objective": obj[:, :T] if obj is not None else None,
             "iterates": its, "status": status, "n_iter": n_iter, "cond_est": cond, "_ws": ws,
             "launches": lib.psca_last_launch_count(),
-            "path": "persistent" if lib.psca_last_path() == 1 else "two-kernel"}
+            "path": {0: "two-kernel", 1: "persistent", 2: "two-kernel-split"}.get(
+                lib.psca_last_path(), "?")}
 
 
 # ---------------------------------------------------------------------------
