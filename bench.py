@@ -357,21 +357,16 @@ def ours_arm(args):
     finite = bool(torch.isfinite(x_check).all().item())
 
     # ---- end to end through the public API from pinned host buffers ----------
+    # psca_run_batch_host: chunked H2D on a copy stream overlapped with the solve,
+    # estimates copied back per chunk; all of it inside the timed region
     e2e = None
     if not args.no_e2e:
-        x_h = torch.empty((B, cfg.n_devices), dtype=torch.float64).pin_memory()
         h2d = pil_h.numel() * 16 + emp_h.numel() * 16 + noi_h.numel() * 8
-        d2h = x_h.numel() * 8
-        out2 = {}
-        p2, em2, n2 = (torch.empty_like(t) for t in (pil_d, emp_d, noi_d))
+        d2h = B * cfg.n_devices * 8 + 2 * B * 4
 
         def e2e_step():
-            nonlocal out2
-            p2.copy_(pil_h, non_blocking=True)
-            em2.copy_(emp_h, non_blocking=True)
-            n2.copy_(noi_h, non_blocking=True)
-            out2 = estimators.psca_run_batch(problem, p2, em2, n2, m, max_iter=iters, out=out2)
-            x_h.copy_(out2["x"], non_blocking=True)
+            return estimators.psca_run_batch_host(problem, pil_h, emp_h, noi_h, m,
+                                                  max_iter=iters, chunks=4)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -380,15 +375,17 @@ def ours_arm(args):
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(args.steps):
-            e2e_step()
+            r = e2e_step()
         f1.record()
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(f0.elapsed_time(f1))
         e2e = {"value": world * B * args.steps / (ems * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": ems / args.steps}
-        del p2, em2, n2
+               "ms_per_step": ems / args.steps,
+               "api": "paper_2503_15259_b200.psca_run_batch_host (pinned host in, host out; "
+                      "4 chunks, H2D overlapped with the solve)",
+               "x_matches_device_run": bool(torch.equal(r["x"], out["x"].cpu()))}
 
     line = None
     if rank == 0:

@@ -9,6 +9,7 @@ points (``psca_run_batch``, ``unroll.forward_batch``) are the throughput path.
 
 from .sysmodel import ActivityModel, DomainError, Sample, SystemConfig, empirical_cov
 from .estimators import (DetectorTrace, Problem, StepSchedule, psca_run, psca_run_batch,
+                         psca_run_batch_host,
                          default_schedule, default_steps, bounds_for)
 from .priors import EffPathlossPrior, IndependentPrior
 from .covlinalg import (ConditioningError, CovState, cov_known, cov_unknown, eval_objective,
@@ -16,7 +17,7 @@ from .covlinalg import (ConditioningError, CovState, cov_known, cov_unknown, eva
 
 __all__ = [
     "ActivityModel", "DomainError", "Sample", "SystemConfig", "empirical_cov",
-    "DetectorTrace", "Problem", "StepSchedule", "psca_run", "psca_run_batch",
+    "DetectorTrace", "Problem", "StepSchedule", "psca_run", "psca_run_batch", "psca_run_batch_host",
     "default_schedule", "default_steps", "bounds_for",
     "EffPathlossPrior", "IndependentPrior",
     "ConditioningError", "CovState", "cov_known", "cov_unknown", "eval_objective",

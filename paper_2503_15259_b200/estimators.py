@@ -286,6 +286,66 @@ def psca_run_batch(problem, pilots, emp_cov, noise, n_antennas: int, gains=None,
                         **kw)
 
 
+_COPY_STREAMS = {}
+
+
+def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=None,
+                        schedule: StepSchedule | None = None, max_iter: int = 30,
+                        tol: float = 0.0, chunks: int = 4) -> dict:
+    """B independent PSCA runs from HOST arrays, with H2D / compute / D2H overlap.
+
+    pilots (B,L,N) complex128, emp_cov (B,L,L), noise (B,), gains (B,N): numpy
+    arrays or CPU tensors (pinned memory for full copy/compute overlap).  The
+    batch is cut into ``chunks`` sub-batches; the host-to-device copy of chunk
+    c+1 runs on a copy stream while chunk c is solved on the current stream,
+    and each chunk's estimates are copied back as soon as it is solved.
+    Returns host tensors x (B,N), status (B,), n_iter (B,).
+    """
+    import torch
+    if schedule is None:
+        schedule = StepSchedule.default()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    as_t = lambda a: a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+    S, E, nz = as_t(pilots), as_t(emp_cov), as_t(np.asarray(noise, dtype=float))
+    G = as_t(gains) if (gains is not None and problem.known_pathloss) else None
+    B, L, N = S.shape
+    chunks = max(1, min(chunks, B))
+    bounds = [(B * c) // chunks for c in range(chunks + 1)]
+    comp = torch.cuda.current_stream()
+    copy = _COPY_STREAMS.setdefault(dev.index, torch.cuda.Stream(device=dev))
+    pin = S.is_pinned()
+    x_h = torch.empty((B, N), dtype=torch.float64, pin_memory=pin)
+    st_h = torch.empty(B, dtype=torch.int32, pin_memory=pin)
+    ni_h = torch.empty(B, dtype=torch.int32, pin_memory=pin)
+    bufs = [None, None]
+    free = [torch.cuda.Event(), torch.cuda.Event()]
+    outs = [{}, {}]
+    for c in range(chunks):
+        lo, hi = bounds[c], bounds[c + 1]
+        k = c % 2
+        with torch.cuda.stream(copy):
+            if c >= 2:
+                copy.wait_event(free[k])           # chunk c-2 finished with this buffer
+            bufs[k] = [t[lo:hi].to(dev, non_blocking=True) if t is not None else None
+                       for t in (S, E, nz, G)]
+            copied = torch.cuda.Event()
+            copied.record(copy)
+        comp.wait_event(copied)
+        Sd, Ed, nd, gd = bufs[k]
+        for t in (Sd, Ed, nd, gd):
+            if t is not None:
+                t.record_stream(comp)
+        res = psca_run_batch(problem, Sd, Ed, nd, n_antennas, gains=gd, schedule=schedule,
+                             max_iter=max_iter, tol=tol, out=outs[k])
+        outs[k] = {"x": res["x"], "_ws": res.get("_ws")}
+        x_h[lo:hi].copy_(res["x"], non_blocking=True)
+        st_h[lo:hi].copy_(res["status"], non_blocking=True)
+        ni_h[lo:hi].copy_(res["n_iter"], non_blocking=True)
+        free[k].record(comp)
+    comp.synchronize()
+    return {"x": x_h, "status": st_h, "n_iter": ni_h}
+
+
 def _batch_via_large(problem, pilots, emp_cov, noise, n_antennas, gains, steps, max_iter, tol,
                      record_objective, kw):
     """Large-L batches: one step-loop solve per instance (device tensors out)."""
