@@ -34,7 +34,7 @@ struct TG {
     static constexpr size_t S_BYTES = (size_t)LP8 * NCT * 16;
     static constexpr size_t W_BYTES = (size_t)LP8 * WCAP * 16;
     static constexpr size_t F_BYTES = (size_t)NB * FRAG_SLOTS * 16;
-    static constexpr size_t SMALL = 2 * NCT * 2 * 8 + NWARP * 4 * 8;
+    static constexpr size_t SMALL = 4 * NCT * 2 * 8 + NWARP * 4 * 8;
     static constexpr size_t TILE_BYTES = 2 * S_BYTES + 2 * W_BYTES;
     // fragments staged in SMEM when they fit beside the tile buffers (NRB <= 16);
     // otherwise col_pass reads them through L1 from global
@@ -88,13 +88,17 @@ __device__ __forceinline__ void rebuild_slots(int (&slot)[TG<NRB>::MAXBW], int& 
 // warp 0 holds the per-lane partial sum of (x_next - x)^2 and min q, all
 // cp.async groups are retired and the CTA is synchronised.
 // ---------------------------------------------------------------------------
-#ifndef PSCA_QCH
-#define PSCA_QCH 1
+// Quad-stage shape, chosen by A/B measurement on B200 (profiles/README.md):
+// one DMMA accumulator chain per matrix and the B fragments loaded from SMEM
+// per k-step (2.42 ms vs 3.05 ms per launch with two chains and
+// register-resident B fragments: register pressure, not the ~32-cycle DMMA
+// latency, was the limit), one 8-column block per warp (2.42 vs 2.55 ms with
+// two blocks and four row-block groups).
+#ifndef PSCA_QCB
+#define PSCA_QCB 1
 #endif
-#ifndef PSCA_BQREG
-#define PSCA_BQREG 0
-#endif
-constexpr int QCH = PSCA_QCH;   // independent DMMA chains per matrix in the quad stage
+constexpr int QCB = PSCA_QCB;                // 8-column blocks per warp in the quad stage
+constexpr int QPARTS = NWARP / (NCB / QCB);  // row-block groups (LPT-balanced)
 
 template <int NRB>
 __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
@@ -113,15 +117,17 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
 
     // ---- per-lane constants --------------------------------------------------
     const int cp_dst = warp * NCT + (lane ^ swz(warp));   // tile slot (+ s*8*NCT)
-    const int cb = warp & (NCB - 1);
-    const int half = warp / NCB;
+    const int cb = (warp % (NCB / QCB)) * QCB;   // first of this warp's column blocks
+    const int half = warp / (NCB / QCB);         // row-block group
     unsigned long long rowmask = 0ull;
     {
-        int load0 = 0, load1 = 0;
+        int load[QPARTS];
+        for (int h = 0; h < QPARTS; ++h) load[h] = 0;
         for (int i = NRB - 1; i >= 0; --i) {
-            const int cost = 2 * (i + 1);
-            const int h = (load1 < load0) ? 1 : 0;
-            if (h) load1 += cost; else load0 += cost;
+            int h = 0;
+            for (int u = 1; u < QPARTS; ++u)
+                if (load[u] < load[h]) h = u;
+            load[h] += 2 * (i + 1);
             if (h == half) rowmask |= (1ull << i);
         }
     }
@@ -236,56 +242,54 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         // ---- phase A: deferred rebuild of tile t-1, quad forms of tile t -----
         if (pend > 0) rebuild(pend);
         {
-#if PSCA_BQREG
-            double bq[2 * NRB];
+            double qa[QCB][2], ra[QCB][2];
 #pragma unroll
-            for (int kk = 0; kk < 2 * NRB; ++kk) bq[kk] = Sd[qoff[kk & 1] + kk * 4 * NCT];
-#define PSCA_BQ(kk) bq[kk]
-#else
-#define PSCA_BQ(kk) Sd[qoff[(kk) & 1] + (kk) * 4 * NCT]
-#endif
-            double qa0 = 0.0, qa1 = 0.0, ra0 = 0.0, ra1 = 0.0;
+            for (int j = 0; j < QCB; ++j) qa[j][0] = qa[j][1] = ra[j][0] = ra[j][1] = 0.0;
 #pragma unroll
             for (int i = 0; i < NRB; ++i) {
                 if ((rowmask >> i) & 1ull) {
-                    double tc[QCH][2], uc[QCH][2];
+                    double tc[QCB][2], uc[QCB][2];
 #pragma unroll
-                    for (int c = 0; c < QCH; ++c) tc[c][0] = tc[c][1] = uc[c][0] = uc[c][1] = 0.0;
+                    for (int j = 0; j < QCB; ++j) tc[j][0] = tc[j][1] = uc[j][0] = uc[j][1] = 0.0;
                     const double2* f = FR + i * (i + 1) * FRAG_SLOTS + fslot;
 #pragma unroll
                     for (int kk = 0; kk < 2 * (i + 1); ++kk) {
                         const double2 pa = f[kk * FRAG_SLOTS];
-                        const double bv = PSCA_BQ(kk);
-                        dmma(tc[kk % QCH], pa.x, bv);
-                        dmma(uc[kk % QCH], pa.y, bv);
+#pragma unroll
+                        for (int j = 0; j < QCB; ++j) {
+                            const double bv = Sd[qoff[kk & 1] + kk * 4 * NCT + 16 * j];
+                            dmma(tc[j], pa.x, bv);
+                            dmma(uc[j], pa.y, bv);
+                        }
                     }
 #pragma unroll
-                    for (int c = 1; c < QCH; ++c) {
-                        tc[0][0] += tc[c][0]; tc[0][1] += tc[c][1];
-                        uc[0][0] += uc[c][0]; uc[0][1] += uc[c][1];
+                    for (int j = 0; j < QCB; ++j) {
+                        const double s0 = Sd[epoff[0] + i * 8 * NCT + 16 * j];
+                        const double s1 = Sd[epoff[1] + i * 8 * NCT + 16 * j];
+                        qa[j][0] = fma(s0, tc[j][0], qa[j][0]);
+                        qa[j][1] = fma(s1, tc[j][1], qa[j][1]);
+                        ra[j][0] = fma(s0, uc[j][0], ra[j][0]);
+                        ra[j][1] = fma(s1, uc[j][1], ra[j][1]);
                     }
-                    const double s0 = Sd[epoff[0] + i * 8 * NCT];
-                    const double s1 = Sd[epoff[1] + i * 8 * NCT];
-                    qa0 = fma(s0, tc[0][0], qa0);
-                    qa1 = fma(s1, tc[0][1], qa1);
-                    ra0 = fma(s0, uc[0][0], ra0);
-                    ra1 = fma(s1, uc[0][1], ra1);
                 }
             }
 #pragma unroll
-            for (int o = 4; o < 32; o <<= 1) {
-                qa0 += __shfl_xor_sync(0xffffffffu, qa0, o);
-                qa1 += __shfl_xor_sync(0xffffffffu, qa1, o);
-                ra0 += __shfl_xor_sync(0xffffffffu, ra0, o);
-                ra1 += __shfl_xor_sync(0xffffffffu, ra1, o);
-            }
-            if (r8 == 0) {
-                const int n0 = cb * 8 + 2 * c4;
-                double* d = qr_s + half * NCT * 2;
-                d[2 * n0] = qa0;
-                d[2 * n0 + 1] = ra0;
-                d[2 * (n0 + 1)] = qa1;
-                d[2 * (n0 + 1) + 1] = ra1;
+            for (int j = 0; j < QCB; ++j) {
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) {
+                    qa[j][0] += __shfl_xor_sync(0xffffffffu, qa[j][0], o);
+                    qa[j][1] += __shfl_xor_sync(0xffffffffu, qa[j][1], o);
+                    ra[j][0] += __shfl_xor_sync(0xffffffffu, ra[j][0], o);
+                    ra[j][1] += __shfl_xor_sync(0xffffffffu, ra[j][1], o);
+                }
+                if (r8 == 0) {
+                    const int n0 = (cb + j) * 8 + 2 * c4;
+                    double* d = qr_s + half * NCT * 2;
+                    d[2 * n0] = qa[j][0];
+                    d[2 * n0 + 1] = ra[j][0];
+                    d[2 * (n0 + 1)] = qa[j][1];
+                    d[2 * (n0 + 1) + 1] = ra[j][1];
+                }
             }
         }
         __syncthreads();
@@ -294,8 +298,12 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         {
             double v = 0.0;
             if (cvalid) {
-                const double q = qr_s[2 * lane] + qr_s[NCT * 2 + 2 * lane];
-                const double r = qr_s[2 * lane + 1] + qr_s[NCT * 2 + 2 * lane + 1];
+                double q = qr_s[2 * lane], r = qr_s[2 * lane + 1];
+#pragma unroll
+                for (int h = 1; h < QPARTS; ++h) {
+                    q += qr_s[h * NCT * 2 + 2 * lane];
+                    r += qr_s[h * NCT * 2 + 2 * lane + 1];
+                }
                 const double diff = __dsub_rn(q, r);
                 double grad;
                 if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
