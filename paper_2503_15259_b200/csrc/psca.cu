@@ -1198,7 +1198,7 @@ cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
     ProfScope prof(st, 1);
-    kfn<<<fa.B, NT_FAC, sm, st>>>(fa);
+    kfn<<<fa.B, fac_threads<NRB>(), sm, st>>>(fa);
     ++g_launches;
     return cudaGetLastError();
 }

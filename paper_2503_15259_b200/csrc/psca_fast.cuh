@@ -21,6 +21,18 @@
 //                                      overlaps the DMMA work of the other
 //                                      resident CTA.
 
+// Quad-stage shape, chosen by A/B measurement on B200 (profiles/README.md):
+// one DMMA accumulator chain per matrix and the B fragments loaded from SMEM
+// per k-step (2.42 ms vs 3.05 ms per launch with two chains and
+// register-resident B fragments: register pressure, not the ~32-cycle DMMA
+// latency, was the limit), one 8-column block per warp (2.42 vs 2.55 ms with
+// two blocks and four row-block groups).
+#ifndef PSCA_QCB
+#define PSCA_QCB 1
+#endif
+constexpr int QCB = PSCA_QCB;                // 8-column blocks per warp in the quad stage
+constexpr int QPARTS = NWARP / (NCB / QCB);  // row-block groups (LPT-balanced)
+
 template <int NRB>
 struct TG {
     static constexpr int LP = 4 * NRB;
@@ -34,12 +46,19 @@ struct TG {
     static constexpr size_t S_BYTES = (size_t)LP8 * NCT * 16;
     static constexpr size_t W_BYTES = (size_t)LP8 * WCAP * 16;
     static constexpr size_t F_BYTES = (size_t)NB * FRAG_SLOTS * 16;
-    static constexpr size_t SMALL = 4 * NCT * 2 * 8 + NWARP * 4 * 8;
+    static constexpr size_t SMALL = (size_t)QPARTS * NCT * 2 * 8;   // quad partials
     static constexpr size_t TILE_BYTES = 2 * S_BYTES + 2 * W_BYTES;
-    // fragments staged in SMEM when they fit beside the tile buffers (NRB <= 16);
-    // otherwise col_pass reads them through L1 from global
-    static constexpr bool FR_SMEM = TILE_BYTES + F_BYTES + SMALL <= 227 * 1024;
-    static constexpr size_t COL_SMEM = TILE_BYTES + (FR_SMEM ? F_BYTES : 0) + SMALL;
+    // Fragments are staged in SMEM beside the tile buffers: lane-ready
+    // (FRAG_SLOTS = 24 per block, {re, im, -im}) when that fits (NRB <= 16),
+    // else compacted to {re, im} (16 per block; the -im lanes flip the sign
+    // bit after the load), which still fits at NRB = 20 (L = 80).
+    static constexpr bool FIT24 = TILE_BYTES + F_BYTES + SMALL <= 227 * 1024;
+    static constexpr size_t F16_BYTES = (size_t)NB * 16 * 16;
+    static constexpr bool FIT16 = TILE_BYTES + F16_BYTES + SMALL <= 227 * 1024;
+    static constexpr bool FR_SMEM = FIT24 || FIT16;
+    static constexpr int FR_SLOTS = FIT24 ? FRAG_SLOTS : (FIT16 ? 16 : FRAG_SLOTS);
+    static constexpr size_t COL_SMEM =
+        TILE_BYTES + (FR_SMEM ? (size_t)NB * FR_SLOTS * 16 : 0) + SMALL;
     static constexpr size_t FAC_BYTES = (size_t)4 * LP * 16 + (size_t)2 * LP * (LP + 1) * 16;
     static constexpr size_t UNION = (TILE_BYTES > FAC_BYTES) ? TILE_BYTES : FAC_BYTES;
     static constexpr size_t PERSIST_SMEM = F_BYTES + UNION + SMALL;
@@ -88,19 +107,8 @@ __device__ __forceinline__ void rebuild_slots(int (&slot)[TG<NRB>::MAXBW], int& 
 // warp 0 holds the per-lane partial sum of (x_next - x)^2 and min q, all
 // cp.async groups are retired and the CTA is synchronised.
 // ---------------------------------------------------------------------------
-// Quad-stage shape, chosen by A/B measurement on B200 (profiles/README.md):
-// one DMMA accumulator chain per matrix and the B fragments loaded from SMEM
-// per k-step (2.42 ms vs 3.05 ms per launch with two chains and
-// register-resident B fragments: register pressure, not the ~32-cycle DMMA
-// latency, was the limit), one 8-column block per warp (2.42 vs 2.55 ms with
-// two blocks and four row-block groups).
-#ifndef PSCA_QCB
-#define PSCA_QCB 1
-#endif
-constexpr int QCB = PSCA_QCB;                // 8-column blocks per warp in the quad stage
-constexpr int QPARTS = NWARP / (NCB / QCB);  // row-block groups (LPT-balanced)
 
-template <int NRB>
+template <int NRB, int FS = FRAG_SLOTS>
 __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
                                          const double* __restrict__ x_cur,
                                          double* __restrict__ x_next, int n_begin, int n_end,
@@ -145,7 +153,13 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         for (int j = 0; j < 2; ++j)
             epoff[j] = 2 * ((r8 >> 1) * NCT + cb * 8 + ((2 * c4 + j) ^ se)) + (r8 & 1);
     }
-    const int fslot = frag_lane_slot(lane);
+    // lane's fragment slot; with the compact 16-slot layout the -im lanes
+    // (row parity 0, k parity 1) read im and flip its sign
+    const int fslot = (FS == FRAG_SLOTS)
+                          ? frag_lane_slot(lane)
+                          : 2 * (2 * (r8 >> 1) + (c4 >> 1)) + ((r8 & 1) != (c4 & 1));
+    const unsigned long long fsgn =
+        (FS != FRAG_SLOTS && (r8 & 1) == 0 && (c4 & 1) == 1) ? 0x8000000000000000ull : 0ull;
     // rebuild fragments over the packed slots (WS / SP rows of WCAP = 16 slots,
     // slot swizzle 2*(row & 3)), k-step k2 = 4 g + h, slot n = 2 k2 + (c4>>1):
     //   A (WS):  l = 4i + (r8>>1), component p^q, sign p&q
@@ -251,15 +265,17 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
                     double tc[QCB][2], uc[QCB][2];
 #pragma unroll
                     for (int j = 0; j < QCB; ++j) tc[j][0] = tc[j][1] = uc[j][0] = uc[j][1] = 0.0;
-                    const double2* f = FR + i * (i + 1) * FRAG_SLOTS + fslot;
+                    const double2* f = FR + i * (i + 1) * FS + fslot;
 #pragma unroll
                     for (int kk = 0; kk < 2 * (i + 1); ++kk) {
-                        const double2 pa = f[kk * FRAG_SLOTS];
+                        const double2 pa = f[kk * FS];
+                        const double pv = (FS == FRAG_SLOTS) ? pa.x : xsign(pa.x, fsgn);
+                        const double av = (FS == FRAG_SLOTS) ? pa.y : xsign(pa.y, fsgn);
 #pragma unroll
                         for (int j = 0; j < QCB; ++j) {
                             const double bv = Sd[qoff[kk & 1] + kk * 4 * NCT + 16 * j];
-                            dmma(tc[j], pa.x, bv);
-                            dmma(uc[j], pa.y, bv);
+                            dmma(tc[j], pv, bv);
+                            dmma(uc[j], av, bv);
                         }
                     }
 #pragma unroll
@@ -460,6 +476,13 @@ struct TF {
 // factor CTA size of the two-kernel path: 128 threads, Sigma_hat read from L2,
 // so four instances share an SM and hide each other's pivot-barrier latency
 constexpr int NT_FAC = 128;
+// L >= 64: the register-tiled products need more threads (128 spill at L = 80)
+// and the CTA is alone on its SM anyway (SMEM), so use all of NT.
+#ifndef PSCA_FAC_WIDE
+#define PSCA_FAC_WIDE 256
+#endif
+template <int NRB>
+__host__ __device__ constexpr int fac_threads() { return NRB >= 16 ? PSCA_FAC_WIDE : NT_FAC; }
 
 // (bi, bj), bi >= bj, of lower 2x2 block number t (row-major)
 __device__ __forceinline__ void lower_block(int t, int& bi, int& bj) {
@@ -729,11 +752,16 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColAr
     double2* WS = S1 + G::LP8 * NCT;
     double2* SP = WS + G::LP8 * G::WCAP;
     double2* FRs = SP + G::LP8 * G::WCAP;                            // [NB][24] if staged
-    double* qr_s = reinterpret_cast<double*>(FRs + (G::FR_SMEM ? G::NB * FRAG_SLOTS : 0));
+    constexpr int FS = G::FR_SLOTS;
+    double* qr_s = reinterpret_cast<double*>(FRs + (G::FR_SMEM ? G::NB * FS : 0));
     const double2* FR;
     if (G::FR_SMEM) {   // stage the instance's P'/A' fragments (one cp.async group)
         const double2* src = a.frags + (size_t)b * G::NB * FRAG_SLOTS;
-        for (int e = tid; e < G::NB * FRAG_SLOTS; e += NT) cp_async16(FRs + e, src + e, 16);
+        for (int e = tid; e < G::NB * FS; e += NT) {
+            // compact layout: slot 2 ent + var of a block <- 3 ent + var (var < 2)
+            const int se = (FS == FRAG_SLOTS) ? e : (e >> 4) * FRAG_SLOTS + 3 * ((e & 15) >> 1) + (e & 1);
+            cp_async16(FRs + e, src + se, 16);
+        }
         cp_async_commit();
         FR = FRs;
     } else {
@@ -745,8 +773,8 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColAr
     if (a.dbg_delay_ns > 0 && (b & 1)) __nanosleep(a.dbg_delay_ns);
     double acc[G::MAXBW][2];
     double dx2, minq;
-    col_pass<NRB>(a, b, a.k, a.x_cur + bN, a.x_next + bN, n_begin, n_end, S0, S1, WS, SP, FR,
-                  qr_s, acc, slot, nbw, dx2, minq);
+    col_pass<NRB, FS>(a, b, a.k, a.x_cur + bN, a.x_next + bN, n_begin, n_end, S0, S1, WS, SP,
+                      FR, qr_s, acc, slot, nbw, dx2, minq);
 
     {
         double2* sp = a.sig_part + ((size_t)b * a.n_chunks + chunk) * G::NBLK * 32;
@@ -774,7 +802,7 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColAr
 }
 
 template <int NRB>
-__global__ void __launch_bounds__(NT_FAC, (NRB <= 10) ? 4 : 1) factor_solve_t(FacArgs a) {
+__global__ void __launch_bounds__(fac_threads<NRB>(), (NRB <= 10) ? 4 : 1) factor_solve_t(FacArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double sred[NWARP + 1];
     __shared__ int s_flag;
@@ -797,7 +825,7 @@ __global__ void __launch_bounds__(NT_FAC, (NRB <= 10) ? 4 : 1) factor_solve_t(Fa
     assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
     double frob, logdet, trace;
     double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
-    if (!factor_pass<NRB, NT_FAC>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet,
+    if (!factor_pass<NRB, fac_threads<NRB>()>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet,
                                   trace)) {
         if (tid == 0) {
             a.status[b] = PSCA_CHOL_FAIL;

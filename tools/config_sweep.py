@@ -43,17 +43,33 @@ def batched(name, net=False):
         out = estimators.psca_run_batch(prob, P, E, Nz, cfg.n_antennas, gains=G, schedule=sched,
                                         max_iter=T, out=out)
     ms = timed(run)
+    prof = None
+    if os.environ.get("SWEEP_PROFILE"):
+        from paper_2503_15259_b200 import device
+        device.profile_begin()
+        run()
+        torch.cuda.synchronize()
+        p = device.profile_end()
+        prof = {"column_ms_per_launch": p["column_ms"] / max(1, p["column_launches"]),
+                "factor_ms_per_launch": p["factor_ms"] / max(1, p["factor_launches"]),
+                "column_ms": p["column_ms"], "factor_ms": p["factor_ms"]}
     flops = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * B * T
     return {"config": name + ("_net" if net else ""), "kind": cfg.kind, "B": B, "N": cfg.n_devices,
             "L": cfg.pilot_len, "T": T, "ms_per_solve": ms, "instances_per_s": B / (ms * 1e-3),
             "psca_iters_per_s": B * T / (ms * 1e-3), "algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
-            "path": out.get("path")}
+            "path": out.get("path"), "profile": prof}
 
 
-rows = [batched("c0")]
-for n in ("c1", "c2", "c3_l20", "c3_l40", "c3_l80"):
-    rows.append(batched(n))
-rows.append(batched("c2", net=True))
+only = set(sys.argv[1:])
+want = lambda n: not only or n in only   # noqa: E731
+rows = [batched(n) for n in ("c0", "c1", "c2", "c3_l20", "c3_l40", "c3_l80") if want(n)]
+if want("c2_net"):
+    rows.append(batched("c2", net=True))
+for r in rows:
+    print(json.dumps(r), flush=True)
+if not want("c4"):
+    sys.exit(0)
+rows = []
 cfg = scenes.BASELINE_CONFIGS["c4"]
 s = scenes.make_scene(cfg, 0)
 S = torch.from_numpy(s.pilots).to(dev)
