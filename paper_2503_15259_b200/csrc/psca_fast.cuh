@@ -626,103 +626,103 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         }
         trace = block_sum(s, sred);
     }
-    // ---- G = Sigma_hat P (all 2x2 blocks) ----------------------------------------
+    // ---- G = Sigma_hat P and A = P G on DMMA ----------------------------------
+    // Complex products in the real 2x2 expansion, first real column of each
+    // complex column only: C^[2l+p][m] = sum_{kc,q} A^[2l+p][2kc+q] Bc[2kc+q][m]
+    // with A^ = [[re,-im],[im,re]] and Bc[2kc+q][m] = component q of B(kc,m),
+    // so C^[2l+p][m] = component p of (A B)(l,m).  Tile = 8 real rows (4
+    // complex rows, ri) x 8 complex columns (cj), k-step = 2 complex columns.
+    // A warp owns a row tile and keeps one accumulator chain per column tile
+    // (the A fragment is shared), reading A^ from Sigma_hat (L2) or P (SMEM)
+    // and Bc from SMEM.
     {
-        int gi[F::SG], gj[F::SG];
-        double2 gacc[F::SG][2][2];
+        constexpr int NCJ = (LP + 7) / 8;
+        constexpr int NKS = LP / 2;
+        constexpr int NWF = NTH / 32;
+        const int lane = tid & 31, warp = tid >> 5;
+        const int r8 = lane >> 2, c4 = lane & 3;
+        const int p = r8 & 1, q = c4 & 1;
+        const unsigned long long sg = (p == 0 && q == 1) ? 0x8000000000000000ull : 0ull;
+        const double* Xd = reinterpret_cast<const double*>(X);
+        double* Gd = reinterpret_cast<double*>(G);
+        // G = Sigma_hat P, all tiles
+        for (int ri = warp; ri < NRB; ri += NWF) {
+            const int l = 4 * ri + (r8 >> 1);
+            double acc[NCJ][2];
 #pragma unroll
-        for (int u = 0; u < F::SG; ++u) {
-            const int t = tid + NTH * u;
-            gi[u] = (t < F::NFB) ? t / F::NBL : -1;
-            gj[u] = (t < F::NFB) ? t % F::NBL : 0;
+            for (int j = 0; j < NCJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+            const double* erow = reinterpret_cast<const double*>(Eg + (size_t)l * L);
+#pragma unroll 4
+            for (int ks = 0; ks < NKS; ++ks) {
+                const int kc = 2 * ks + (c4 >> 1);
+                const double av = (l < L && kc < L) ? xsign(__ldg(erow + 2 * kc + (p ^ q)), sg) : 0.0;
+                const double* brow = Xd + 2 * (kc * ld) + q;
 #pragma unroll
-            for (int di = 0; di < 2; ++di)
-#pragma unroll
-                for (int dj = 0; dj < 2; ++dj) gacc[u][di][dj] = make_double2(0.0, 0.0);
-        }
-        for (int c = 0; c < L; ++c) {
-#pragma unroll
-            for (int u = 0; u < F::SG; ++u) {
-                if (gi[u] < 0) continue;
-                const int i0 = 2 * gi[u], j0 = 2 * gj[u];
-                const double2 e0 = (i0 < L) ? Ev(i0, c) : make_double2(0.0, 0.0);
-                const double2 e1 = (i0 + 1 < L) ? Ev(i0 + 1, c) : make_double2(0.0, 0.0);
-                const double2 x0 = X[c * ld + j0], x1 = X[c * ld + j0 + 1];
-                gacc[u][0][0] = cfma(e0, x0, gacc[u][0][0]);
-                gacc[u][0][1] = cfma(e0, x1, gacc[u][0][1]);
-                gacc[u][1][0] = cfma(e1, x0, gacc[u][1][0]);
-                gacc[u][1][1] = cfma(e1, x1, gacc[u][1][1]);
+                for (int j = 0; j < NCJ; ++j) {
+                    const int m = 8 * j + r8;
+                    const double bv = (m < LP) ? brow[2 * m] : 0.0;
+                    dmma(acc[j], av, bv);
+                }
             }
-        }
 #pragma unroll
-        for (int u = 0; u < F::SG; ++u) {
-            if (gi[u] < 0) continue;
+            for (int j = 0; j < NCJ; ++j)
 #pragma unroll
-            for (int di = 0; di < 2; ++di)
-#pragma unroll
-                for (int dj = 0; dj < 2; ++dj)
-                    G[(2 * gi[u] + di) * ld + 2 * gj[u] + dj] = gacc[u][di][dj];
-        }
-    }
-    __syncthreads();
-    // ---- A = P G (lower 2x2 blocks) and the fragment pack ------------------------
-    {
-        double2 aacc[F::SL][2][2];
-#pragma unroll
-        for (int u = 0; u < F::SL; ++u)
-#pragma unroll
-            for (int di = 0; di < 2; ++di)
-#pragma unroll
-                for (int dj = 0; dj < 2; ++dj) aacc[u][di][dj] = make_double2(0.0, 0.0);
-        for (int t = 0; t < L; ++t) {
-#pragma unroll
-            for (int u = 0; u < F::SL; ++u) {
-                if (bi[u] < 0) continue;
-                const int l0 = 2 * bi[u], m0 = 2 * bj[u];
-                const double2 p0 = X[l0 * ld + t], p1 = X[(l0 + 1) * ld + t];
-                const double2 g0 = G[t * ld + m0], g1 = G[t * ld + m0 + 1];
-                aacc[u][0][0] = cfma(p0, g0, aacc[u][0][0]);
-                aacc[u][0][1] = cfma(p0, g1, aacc[u][0][1]);
-                aacc[u][1][0] = cfma(p1, g0, aacc[u][1][0]);
-                aacc[u][1][1] = cfma(p1, g1, aacc[u][1][1]);
-            }
-        }
-        auto put = [&](int l, int m, double2 pv, double2 av) {
-            const int i4 = l >> 2;
-            const int blk = i4 * (i4 + 1) + (m >> 1);
-            const int ent = (l & 3) * 2 + (m & 1);
-            double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
-            o[0] = pv.x; o[1] = av.x;
-            o[2] = pv.y; o[3] = av.y;
-            o[4] = -pv.y; o[5] = -av.y;
-        };
-#pragma unroll
-        for (int u = 0; u < F::SL; ++u) {
-            if (bi[u] < 0) continue;
-#pragma unroll
-            for (int di = 0; di < 2; ++di)
-#pragma unroll
-                for (int dj = 0; dj < 2; ++dj) {
-                    const int l = 2 * bi[u] + di, m = 2 * bj[u] + dj;
-                    double2 pv = make_double2(0.0, 0.0), av = make_double2(0.0, 0.0);
-                    if (l < L && m <= l) {
-                        pv = X[l * ld + m];
-                        av = aacc[u][di][dj];
-                        if (m < l) {
-                            pv.x *= 2.0; pv.y *= 2.0; av.x *= 2.0; av.y *= 2.0;
-                        } else {
-                            pv.y = 0.0; av.y = 0.0;
-                        }
-                    }
-                    put(l, m, pv, av);
+                for (int h = 0; h < 2; ++h) {
+                    const int m = 8 * j + 2 * c4 + h;
+                    if (m < LP) Gd[2 * (l * ld + m) + p] = acc[j][h];
                 }
         }
-        // upper 2x2 blocks inside the diagonal 4x4 fragment groups are zero
-        if (tid < NRB) {
-            const int l0 = 4 * tid, m0 = 4 * tid + 2;
-            const double2 z = make_double2(0.0, 0.0);
-            put(l0, m0, z, z); put(l0, m0 + 1, z, z);
-            put(l0 + 1, m0, z, z); put(l0 + 1, m0 + 1, z, z);
+        __syncthreads();
+        // A = P G, lower tiles only (column tiles cj with 8 cj <= 4 ri + 3), and
+        // the fragment pack: entry (l, m), m <= 4 ri + 3, gets P'/A' = 2x the
+        // lower values, the real diagonal, zero above the diagonal
+        const double* Gc = reinterpret_cast<const double*>(G);
+        for (int t = warp; t < NRB; t += NWF) {
+            const int ri = NRB - 1 - t;             // longest rows first
+            const int ncj = (4 * ri + 3) / 8 + 1;
+            const int l = 4 * ri + (r8 >> 1);
+            double acc[NCJ][2];
+#pragma unroll
+            for (int j = 0; j < NCJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+            const double* prow = Xd + 2 * (l * ld);
+#pragma unroll 4
+            for (int ks = 0; ks < NKS; ++ks) {
+                const int kc = 2 * ks + (c4 >> 1);
+                const double av = xsign(prow[2 * kc + (p ^ q)], sg);
+                const double* brow = Gc + 2 * (kc * ld) + q;
+#pragma unroll
+                for (int j = 0; j < NCJ; ++j) {
+                    if (j < ncj) {
+                        const int m = 8 * j + r8;
+                        const double bv = (m < LP) ? brow[2 * m] : 0.0;
+                        dmma(acc[j], av, bv);
+                    }
+                }
+            }
+            const int i4 = l >> 2;
+#pragma unroll
+            for (int j = 0; j < NCJ; ++j) {
+                if (j < ncj) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int m = 8 * j + 2 * c4 + h;
+                        if (m <= 4 * ri + 3) {
+                            const double f = (m < l) ? 2.0 : ((m == l && p == 0) ? 1.0 : 0.0);
+                            const double pv = f * Xd[2 * (l * ld + m) + p];
+                            const double avv = f * acc[j][h];
+                            const int blk = i4 * (i4 + 1) + (m >> 1);
+                            const int ent = (l & 3) * 2 + (m & 1);
+                            double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
+                            if (p == 0) {
+                                o[0] = pv; o[1] = avv;
+                            } else {
+                                o[2] = pv; o[3] = avv;
+                                o[4] = -pv; o[5] = -avv;
+                            }
+                        }
+                    }
+                }
+            }
         }
     }
     __syncthreads();
