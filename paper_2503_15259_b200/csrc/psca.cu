@@ -193,7 +193,8 @@ __device__ __forceinline__ double np_clip(double v, double lo, double hi) {
 }
 
 // deterministic CTA reductions (fixed shuffle + fixed warp order)
-// (any CTA size up to NT; sred holds NWARP + 1 doubles)
+// (any CTA size up to 1024; sred holds SRED doubles)
+constexpr int SRED = 33;
 __device__ double block_sum(double v, double* sred) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -203,10 +204,10 @@ __device__ double block_sum(double v, double* sred) {
     double t = 0.0;
     if (threadIdx.x == 0) {
         for (int i = 0; i < nw; ++i) t += sred[i];
-        sred[NWARP] = t;
+        sred[SRED - 1] = t;
     }
     __syncthreads();
-    return sred[NWARP];
+    return sred[SRED - 1];
 }
 
 // ---------------------------------------------------------------------------
@@ -720,8 +721,21 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
             int j = blk - base;
             double2 s = make_double2(0.0, 0.0);
             if (!zero_weights) {
-                for (int c = 0; c < a.n_chunks; ++c) {
-                    double2 v = sp[(size_t)c * geo.NBLK * 32 + e];
+                // loads in batches of 8 (memory-level parallelism), adds in chunk order
+                const size_t cs = (size_t)geo.NBLK * 32;
+                int c = 0;
+                for (; c + 8 <= a.n_chunks; c += 8) {
+                    double2 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = sp[(size_t)(c + u) * cs + e];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        s.x += v[u].x;
+                        s.y += v[u].y;
+                    }
+                }
+                for (; c < a.n_chunks; ++c) {
+                    const double2 v = sp[(size_t)c * cs + e];
                     s.x += v.x;
                     s.y += v.y;
                 }
@@ -791,7 +805,18 @@ __device__ bool fac_finalize(const FacArgs& a, int b, int* s_flag) {
     if (tid == 0) {
         double dx2 = 0.0, minq = INFINITY;
         const double* rp = a.red_part + (size_t)b * a.n_chunks * 4;
-        for (int c = 0; c < a.n_chunks; ++c) {
+        int c = 0;
+        for (; c + 8 <= a.n_chunks; c += 8) {   // batched loads, chunk-order adds
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = *reinterpret_cast<const double2*>(rp + 4 * (c + u));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                dx2 += v[u].x;
+                minq = (v[u].y < minq) ? v[u].y : minq;
+            }
+        }
+        for (; c < a.n_chunks; ++c) {
             dx2 += rp[4 * c];
             minq = (rp[4 * c + 1] < minq) ? rp[4 * c + 1] : minq;
         }
@@ -850,7 +875,7 @@ __device__ double fac_prior_terms(const FacArgs& a, int b, double* sred) {
 template <int MODE>
 __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double sred[NWARP + 1];
+    __shared__ double sred[SRED];
     __shared__ int s_flag;
     const Geo geo = make_geo(a.L, a.nrb);
     const int b = blockIdx.x;
@@ -1190,17 +1215,46 @@ cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, c
     return launch_column<COL_SOLVE>(ca, g, n_chunks, st);
 }
 
-template <int NRB>
-cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
-    const size_t sm = (size_t)4 * g.LP * 16 + (size_t)2 * g.LP * (g.LP + 1) * 16;
-    auto kfn = factor_solve_t<NRB>;
+template <int NRB, int NTH>
+cudaError_t launch_factor_nt(const FacArgs& fa, const Geo& g, cudaStream_t st) {
+    const size_t sm = fac_smem<NRB>();
+    auto kfn = factor_solve_t<NRB, NTH>;
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
     ProfScope prof(st, 1);
-    kfn<<<fa.B, fac_threads<NRB>(), sm, st>>>(fa);
+    kfn<<<fa.B, NTH, sm, st>>>(fa);
     ++g_launches;
     return cudaGetLastError();
+}
+
+int sm_count();
+
+// Few instances (B < SM count): one wide CTA per instance, so the pivot
+// sweeps, the DMMA products and the chunk-partial sums of a lone instance
+// spread over 16 warps instead of 4 (c0: B = 1).  PSCA_FAC_SMALL_NT
+// overrides the width (128 / 256 / 512) for measurements.
+int small_factor_threads() {
+    static const int nt = [] {
+        const char* e = getenv("PSCA_FAC_SMALL_NT");
+        const int v = e ? atoi(e) : 512;
+        return (v == 128 || v == 256 || v == 512) ? v : 512;
+    }();
+    return nt;
+}
+
+template <int NRB>
+cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
+    if (fa.B < sm_count()) {
+        switch (small_factor_threads()) {
+            case 512: return launch_factor_nt<NRB, 512>(fa, g, st);
+            case 256: return launch_factor_nt<NRB, 256>(fa, g, st);
+            default: break;
+        }
+        if (fac_threads<NRB>() != 128) return launch_factor_nt<NRB, fac_threads<NRB>()>(fa, g, st);
+        return launch_factor_nt<NRB, 128>(fa, g, st);
+    }
+    return launch_factor_nt<NRB, fac_threads<NRB>()>(fa, g, st);
 }
 
 template <int MODE>

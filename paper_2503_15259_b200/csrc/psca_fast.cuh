@@ -483,6 +483,11 @@ constexpr int NT_FAC = 128;
 #endif
 template <int NRB>
 __host__ __device__ constexpr int fac_threads() { return NRB >= 16 ? PSCA_FAC_WIDE : NT_FAC; }
+// dynamic SMEM of factor_solve_t: pivot buffers, X, G
+template <int NRB>
+__host__ __device__ constexpr size_t fac_smem() {
+    return (size_t)4 * (4 * NRB) * 16 + (size_t)2 * (4 * NRB) * (4 * NRB + 1) * 16;
+}
 
 // (bi, bj), bi >= bj, of lower 2x2 block number t (row-major)
 __device__ __forceinline__ void lower_block(int t, int& bi, int& bj) {
@@ -651,11 +656,12 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
             double acc[NCJ][2];
 #pragma unroll
             for (int j = 0; j < NCJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-            const double* erow = reinterpret_cast<const double*>(Eg + (size_t)l * L);
+            const double* erow = Es ? reinterpret_cast<const double*>(Es + (size_t)l * ld)
+                                    : reinterpret_cast<const double*>(Eg + (size_t)l * L);
 #pragma unroll 4
             for (int ks = 0; ks < NKS; ++ks) {
                 const int kc = 2 * ks + (c4 >> 1);
-                const double av = (l < L && kc < L) ? xsign(__ldg(erow + 2 * kc + (p ^ q)), sg) : 0.0;
+                const double av = (l < L && kc < L) ? xsign(erow[2 * kc + (p ^ q)], sg) : 0.0;
                 const double* brow = Xd + 2 * (kc * ld) + q;
 #pragma unroll
                 for (int j = 0; j < NCJ; ++j) {
@@ -801,10 +807,10 @@ __global__ void __launch_bounds__(NT, (NRB <= 12) ? 2 : 1) column_kernel_t(ColAr
     }
 }
 
-template <int NRB>
-__global__ void __launch_bounds__(fac_threads<NRB>(), (NRB <= 10) ? 4 : 1) factor_solve_t(FacArgs a) {
+template <int NRB, int NTH>
+__global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor_solve_t(FacArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double sred[NWARP + 1];
+    __shared__ double sred[SRED];
     __shared__ int s_flag;
     const Geo geo = make_geo(a.L, a.nrb);
     const int b = blockIdx.x;
@@ -821,11 +827,11 @@ __global__ void __launch_bounds__(fac_threads<NRB>(), (NRB <= 10) ? 4 : 1) facto
     double2* colb = sm + 2 * LP;    // (unused)
     double2* X = sm + 4 * LP;       // [LP][ld]
     double2* G = X + (size_t)LP * ld;
-    const double2* Es = nullptr;   // Sigma_hat read through L1/L2
+    const double2* Es = nullptr;   // Sigma_hat read through L1/L2 (staging it in SMEM for the wide variants measured no gain)
     assemble_sigma(a, geo, b, X, ld, a.k_new == 0);
     double frob, logdet, trace;
     double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
-    if (!factor_pass<NRB, fac_threads<NRB>()>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet,
+    if (!factor_pass<NRB, NTH>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet,
                                   trace)) {
         if (tid == 0) {
             a.status[b] = PSCA_CHOL_FAIL;
@@ -849,7 +855,7 @@ template <int NRB>
 __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs fa, int* counter) {
     using G = TG<NRB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ double sred[NWARP + 1];
+    __shared__ double sred[SRED];
     __shared__ double s_inst[4];
     __shared__ int s_b, s_flag;
     const Geo geo = make_geo(fa.L, fa.nrb);

@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(NT) finish_sigma_large(LargeArgs a) {
 
 // Frobenius norm of Sigma and (optionally) the prior terms; one CTA
 __global__ void __launch_bounds__(NT) frob_large(LargeArgs a) {
-    __shared__ double sred[NWARP + 1];
+    __shared__ double sred[SRED];
     if (a.flag[0]) return;
     double s = 0.0;
     for (int e = threadIdx.x; e < a.L * a.L; e += NT) {
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(NT) gemm_large(LargeArgs a) {
 
 // trace(P Sigma_hat) for the objective; one CTA
 __global__ void __launch_bounds__(NT) trace_large(LargeArgs a) {
-    __shared__ double sred[NWARP + 1];
+    __shared__ double sred[SRED];
     if (a.flag[0] || a.status[0] != PSCA_RUNNING) return;
     double s = 0.0;
     for (int e = threadIdx.x; e < a.L * a.L; e += NT) {
@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(NT) trace_large(LargeArgs a) {
 
 // prior terms at the new iterate (x_next of the finalised iteration, or 0)
 __global__ void __launch_bounds__(NT) prior_large(LargeArgs a, const double* xv) {
-    __shared__ double sred[NWARP + 1];
+    __shared__ double sred[SRED];
     if (a.flag[0]) return;
     double acc = 0.0;
     const int n = blockIdx.x * NT + threadIdx.x;   // grid-stride not needed: one pass

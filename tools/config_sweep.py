@@ -40,8 +40,9 @@ def batched(name, net=False):
 
     def run():
         nonlocal out
+        kw = {"n_chunks": int(os.environ["SWEEP_CHUNKS"])} if os.environ.get("SWEEP_CHUNKS") else {}
         out = estimators.psca_run_batch(prob, P, E, Nz, cfg.n_antennas, gains=G, schedule=sched,
-                                        max_iter=T, out=out)
+                                        max_iter=T, out=out, **kw)
     ms = timed(run)
     prof = None
     if os.environ.get("SWEEP_PROFILE"):
