@@ -73,6 +73,15 @@ typedef struct {
     const double* prior_lin;/* map-k: [N] = -log(p/(1-p))/M  (priors.py:154-158) */
     const double* prior_p;  /* map-ur: [N] activation probabilities p_n      */
     psca_eff_prior eff;     /* map-ur prior scalars                            */
+    /* map-k with a pairwise MVB prior (priors.py:56-151, group activity): the
+     * gradient term is -(c1 + c2 x)/M at every iterate (priors.py:154-159)
+     * instead of the constant prior_lin.  c2 is the symmetric N x N
+     * interaction matrix in CSR form (zero diagonal).  All four null for the
+     * independent prior. */
+    const double* prior_c1;       /* [N]                                      */
+    const int* prior_c2_indptr;   /* [N+1]                                    */
+    const int* prior_c2_indices;  /* [nnz]                                    */
+    const double* prior_c2_data;  /* [nnz]                                    */
     double* x_out;          /* [B][N]  final estimate (trace.final)            */
     double* update_norm;    /* [B][max_iter]                                    */
     double* objective;      /* [B][max_iter] or 0                              */

@@ -218,6 +218,25 @@ def indep_prior_value(p: np.ndarray, alpha: np.ndarray, m: int) -> float:
 # Step schedules (estimators.py:66-128)
 # ---------------------------------------------------------------------------
 
+def pairwise_prior_grad(c1: np.ndarray, c2, alpha: np.ndarray, m: int) -> np.ndarray:
+    """Pairwise MVB gradient -(c1 + c2 alpha)/M (priors.py:154-159); c2 = (indptr,
+    indices, data) CSR, each row summed in index order like scipy's csr matvec."""
+    indptr, indices, data = c2
+    s = np.zeros(alpha.shape[0])
+    for n in range(alpha.shape[0]):
+        acc = 0.0
+        for j in range(indptr[n], indptr[n + 1]):
+            acc += data[j] * alpha[indices[j]]
+        s[n] = acc
+    return -(c1 + s) / m
+
+
+def pairwise_prior_value(c1: np.ndarray, c2, alpha: np.ndarray, m: int) -> float:
+    """-(c1.alpha + alpha.(c2 alpha)/2)/M (priors.py:146-151)."""
+    cs = -pairwise_prior_grad(np.zeros_like(c1), c2, alpha, 1)
+    return -(float(c1 @ alpha) + 0.5 * float(alpha @ cs)) / m
+
+
 def default_steps(n: int) -> np.ndarray:
     """rho_0 = 1/2, rho <- rho (1 - rho/2)  (estimators.py:66-83)."""
     out = np.empty(n)
@@ -240,12 +259,14 @@ def polynomial_steps(n: int, offset: float = 4.0, exponent: float = 0.8) -> np.n
 def psca(kind: str, pilots: np.ndarray, gains: np.ndarray, emp: np.ndarray, noise: float,
          n_antennas: int, steps: np.ndarray, max_iter: int, tol: float = 0.0,
          indep_p: np.ndarray | None = None, eff: EffPrior | None = None,
-         record_objective: bool = False) -> dict:
+         record_objective: bool = False, pairwise=None) -> dict:
     """One PSCA run from x = 0; returns the trace fields of DetectorTrace.
 
     kind in KINDS; ``steps`` holds rho_k for k < max_iter (explicit schedule).
     Known-pathloss kinds estimate activities in [0,1]; unknown-pathloss kinds
     estimate gamma in [0, inf) (ml-ud) or [0, g_high] (map-ur).
+    ``pairwise`` = (c1, (indptr, indices, data)) selects the pairwise MAP-K
+    prior instead of ``indep_p``.
     """
     assert kind in KINDS
     n = pilots.shape[1]
@@ -255,7 +276,8 @@ def psca(kind: str, pilots: np.ndarray, gains: np.ndarray, emp: np.ndarray, nois
     x = np.zeros(n)
     pc = pilots.conj()
     out = {"iterates": [x.copy()], "update_norm": [], "objective": [], "abort": None}
-    prior_const = indep_prior_grad(indep_p, n_antennas, n) if kind == "map-k" else None
+    prior_const = (indep_prior_grad(indep_p, n_antennas, n)
+                   if kind == "map-k" and pairwise is None else None)
     for k in range(max_iter):
         w = x * gains if known else x
         sigma = model_cov(pilots, w, noise, pc)
@@ -272,7 +294,8 @@ def psca(kind: str, pilots: np.ndarray, gains: np.ndarray, emp: np.ndarray, nois
         if kind == "ml-k":
             grad = gains * d
         elif kind == "map-k":
-            grad = gains * d + prior_const
+            pg = prior_const if pairwise is None else pairwise_prior_grad(*pairwise, x, n_antennas)
+            grad = gains * d + pg
         elif kind == "ml-ud":
             grad = d
         else:
@@ -283,7 +306,9 @@ def psca(kind: str, pilots: np.ndarray, gains: np.ndarray, emp: np.ndarray, nois
         x_new = (1.0 - rho) * x + rho * cand
         if record_objective:
             val = objective_cov(sigma, p, emp)
-            if kind == "map-k":
+            if kind == "map-k" and pairwise is not None:
+                val += pairwise_prior_value(*pairwise, x, n_antennas)
+            elif kind == "map-k":
                 val += indep_prior_value(indep_p, x, n_antennas)
             elif kind == "map-ur":
                 val += eff_prior_value(x, eff, n_antennas)

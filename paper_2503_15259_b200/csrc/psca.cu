@@ -266,6 +266,7 @@ struct ColArgs {
     const double* steps;        // [T]
     const double* prior_lin;    // [N]
     const double* prior_p;      // [N]
+    int pairwise;               // map-k with a pairwise prior: gradient term from pgrad
     const double* pgrad;        // map-ur: [B][N] prior gradient at x_cur (factor_kernel)
     psca_eff_prior eff;
     double* q_out;              // COL_QUAD: [B][N]
@@ -448,7 +449,8 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
                     if (a.kind == PSCA_ML_K) {
                         grad = __dmul_rn(g, diff);
                     } else if (a.kind == PSCA_MAP_K) {
-                        grad = __dadd_rn(__dmul_rn(g, diff), a.prior_lin[n]);
+                        grad = __dadd_rn(__dmul_rn(g, diff),
+                                         a.pairwise ? a.pgrad[bN + n] : a.prior_lin[n]);
                     } else if (a.kind == PSCA_ML_UD) {
                         grad = diff;
                     } else {
@@ -562,7 +564,11 @@ struct FacArgs {
     const double* prior_lin;    // map-k [N]
     const double* prior_p;      // map-ur [N]
     psca_eff_prior eff;
-    double* pgrad;              // map-ur [B][N]: prior gradient at the new iterate
+    double* pgrad;              // map-ur / pairwise map-k [B][N]: prior gradient at the new iterate
+    const double* c1;           // pairwise map-k: [N] first-order coefficients
+    const int* c2_ptr;          //   CSR of c2: [N+1], [nnz], [nnz]
+    const int* c2_idx;
+    const double* c2_val;
     int* status;
     int* n_iter;
     double* cond_est;
@@ -837,6 +843,29 @@ __device__ bool fac_finalize(const FacArgs& a, int b, int* s_flag) {
 __device__ double fac_prior_terms_at(const FacArgs& a, int b, const double* xv, double* sred) {
     const int tid = threadIdx.x;
     double prior_value = 0.0;
+    if (a.kind == PSCA_MAP_K && a.c2_ptr) {
+        // pairwise MVB prior: gradient -(c1 + c2 x)/M, the CSR product in
+        // index order as scipy's csr matvec (priors.py:154-159); value
+        // -(c1.x + x.(c2 x)/2)/M (priors.py:146-151)
+        const size_t bN = (size_t)b * a.N;
+        double lin = 0.0, quad = 0.0;
+        for (int n = tid; n < a.N; n += blockDim.x) {
+            double s = 0.0;
+            for (int j = a.c2_ptr[n]; j < a.c2_ptr[n + 1]; ++j)
+                s = __dadd_rn(s, __dmul_rn(a.c2_val[j], xv[a.c2_idx[j]]));
+            a.pgrad[bN + n] = __ddiv_rn(-__dadd_rn(a.c1[n], s), (double)a.n_antennas);
+            if (a.record_objective) {
+                lin = fma(a.c1[n], xv[n], lin);
+                quad = fma(xv[n], s, quad);
+            }
+        }
+        if (a.record_objective) {
+            lin = block_sum(lin, sred);
+            quad = block_sum(quad, sred);
+            prior_value = -(lin + 0.5 * quad) / a.n_antennas;
+        }
+        return prior_value;
+    }
     if ((a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.record_objective))) {
         const size_t bN = (size_t)b * a.N;
         double acc = 0.0;
@@ -1449,7 +1478,8 @@ SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, v
     s.red_part = cv.take<double>((size_t)a->B * n_chunks * 4 * 8);
     s.x_alt = cv.take<double>((size_t)a->B * a->N * 8);
     s.inst = cv.take<double>((size_t)a->B * 4 * 8);
-    s.pgrad = cv.take<double>(a->kind == PSCA_MAP_UR ? (size_t)a->B * a->N * 8 : 0);
+    const bool pg = a->kind == PSCA_MAP_UR || (a->kind == PSCA_MAP_K && a->prior_c2_indptr);
+    s.pgrad = cv.take<double>(pg ? (size_t)a->B * a->N * 8 : 0);
     s.counter = cv.take<int>(sizeof(int));
     s.dmat = cv.take<double2>((size_t)a->B * a->L * a->L * 16);
     s.scratch = cv.take<double2>(fac_scratch_bytes(g, a->B));
@@ -1465,7 +1495,14 @@ int check_solve_args(const psca_solve_args* a) {
     if (!a->pilots || !a->emp_cov || !a->noise || !a->x_out || !a->status || !a->n_iter)
         return PSCA_E_ARG;
     if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
-    if (a->kind == PSCA_MAP_K && !a->prior_lin) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_K) {
+        const bool pair = a->prior_c2_indptr || a->prior_c2_indices || a->prior_c2_data ||
+                          a->prior_c1;
+        if (pair && !(a->prior_c2_indptr && a->prior_c2_indices && a->prior_c2_data &&
+                      a->prior_c1))
+            return PSCA_E_ARG;
+        if (!pair && !a->prior_lin) return PSCA_E_ARG;
+    }
     if (a->kind == PSCA_MAP_UR && !a->prior_p) return PSCA_E_ARG;
     if (a->max_iter > 0 && (!a->steps || !a->update_norm)) return PSCA_E_ARG;
     return PSCA_OK;
@@ -1678,6 +1715,7 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     ca.sig_part = lay.sig_part; ca.red_part = lay.red_part; ca.status = a->status;
     ca.steps = a->steps; ca.prior_lin = a->prior_lin; ca.prior_p = a->prior_p; ca.eff = a->eff;
     ca.pgrad = lay.pgrad;
+    ca.pairwise = (a->kind == PSCA_MAP_K && a->prior_c2_indptr) ? 1 : 0;
     // incremental rebuild needs the compiled column kernel (psca_fast.cuh)
     const bool fast_col = !generic_forced() && g.NRB <= 20 &&
                           (g.NRB == 2 || g.NRB == 3 || g.NRB == 4 || g.NRB == 5 || g.NRB == 6 ||
@@ -1692,6 +1730,10 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     fa.B = a->B; fa.N = a->N; fa.L = a->L; fa.nrb = g.NRB; fa.T = a->max_iter;
     fa.n_chunks = n_chunks;
     fa.prior_lin = a->prior_lin; fa.prior_p = a->prior_p; fa.eff = a->eff; fa.pgrad = lay.pgrad;
+    if (ca.pairwise) {
+        fa.c1 = a->prior_c1; fa.c2_ptr = a->prior_c2_indptr; fa.c2_idx = a->prior_c2_indices;
+        fa.c2_val = a->prior_c2_data;
+    }
     fa.incremental = ca.incremental; fa.steps = a->steps; fa.dmat = lay.dmat;
     fa.kind = a->kind; fa.n_antennas = a->n_antennas;
     fa.record_objective = ca.record_objective; fa.tol = a->tol;

@@ -245,8 +245,9 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         if (cvalid) {
             x = x_cur[ncol];
             if (known) g = a.gains[bN + ncol];
-            if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
-            else if (a.kind == PSCA_MAP_UR) pg = a.pgrad[bN + ncol];
+            if (a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.pairwise))
+                pg = a.pgrad[bN + ncol];
+            else if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
         }
         cp_async_wait<0>();
         __syncthreads();

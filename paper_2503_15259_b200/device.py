@@ -42,6 +42,8 @@ class SolveArgsC(ctypes.Structure):
         ("pilots", ctypes.c_void_p), ("gains", ctypes.c_void_p), ("emp_cov", ctypes.c_void_p),
         ("noise", ctypes.c_void_p), ("steps", ctypes.c_void_p), ("prior_lin", ctypes.c_void_p),
         ("prior_p", ctypes.c_void_p), ("eff", EffPriorC),
+        ("prior_c1", ctypes.c_void_p), ("prior_c2_indptr", ctypes.c_void_p),
+        ("prior_c2_indices", ctypes.c_void_p), ("prior_c2_data", ctypes.c_void_p),
         ("x_out", ctypes.c_void_p), ("update_norm", ctypes.c_void_p),
         ("objective", ctypes.c_void_p), ("iterates", ctypes.c_void_p),
         ("status", ctypes.c_void_p), ("n_iter", ctypes.c_void_p), ("cond_est", ctypes.c_void_p),
@@ -158,13 +160,15 @@ def eff_prior_struct(prior) -> EffPriorC:
 
 
 def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=None,
-          prior_lin=None, prior_p=None, eff_prior=None, max_iter: int | None = None,
-          tol: float = 0.0, record_objective: bool = False, record_iterates: bool = False,
-          n_chunks: int = 0, out=None):
+          prior_lin=None, prior_p=None, eff_prior=None, prior_c1=None, prior_c2=None,
+          max_iter: int | None = None, tol: float = 0.0, record_objective: bool = False,
+          record_iterates: bool = False, n_chunks: int = 0, out=None):
     """Run the batched PSCA solve on the current CUDA device / stream.
 
     pilots (B,L,N) complex128, emp_cov (B,L,L) complex128, noise (B,) float64,
     gains (B,N) float64 for known-pathloss kinds, steps (T,) float64.
+    A pairwise MAP-K prior passes prior_c1 (N,) and prior_c2 = (indptr,
+    indices, data) of its CSR interaction matrix instead of prior_lin.
     Inputs may be numpy arrays or torch tensors (moved to the device if
     needed).  Returns a dict of device tensors: x (B,N), update_norm (B,T),
     objective (B,T) or None, iterates (B,T+1,N) or None, status (B,) int32,
@@ -188,6 +192,16 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
     g = _dev(torch, gains, torch.float64, dev) if gains is not None else None
     pl = _dev(torch, prior_lin, torch.float64, dev) if prior_lin is not None else None
     pp = _dev(torch, prior_p, torch.float64, dev) if prior_p is not None else None
+    c1 = _dev(torch, prior_c1, torch.float64, dev) if prior_c1 is not None else None
+    c2 = None
+    if prior_c2 is not None:
+        indptr, indices, data = prior_c2
+        c2 = (_dev(torch, np.asarray(indptr, dtype=np.int32), torch.int32, dev),
+              _dev(torch, np.asarray(indices, dtype=np.int32), torch.int32, dev),
+              _dev(torch, np.asarray(data, dtype=np.float64), torch.float64, dev))
+        if c2[1].numel() == 0:   # keep valid pointers for an empty interaction
+            c2 = (c2[0], torch.zeros(1, dtype=torch.int32, device=dev),
+                  torch.zeros(1, dtype=torch.float64, device=dev))
     if out is None:
         out = {}
     x = out.get("x")
@@ -206,7 +220,12 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
         noise=sig2.data_ptr(), steps=st.data_ptr(),
         prior_lin=pl.data_ptr() if pl is not None else 0,
         prior_p=pp.data_ptr() if pp is not None else 0,
-        eff=eff_prior_struct(eff_prior), x_out=x.data_ptr(), update_norm=un.data_ptr(),
+        eff=eff_prior_struct(eff_prior),
+        prior_c1=c1.data_ptr() if c1 is not None else 0,
+        prior_c2_indptr=c2[0].data_ptr() if c2 is not None else 0,
+        prior_c2_indices=c2[1].data_ptr() if c2 is not None else 0,
+        prior_c2_data=c2[2].data_ptr() if c2 is not None else 0,
+        x_out=x.data_ptr(), update_norm=un.data_ptr(),
         objective=obj.data_ptr() if obj is not None else 0,
         iterates=its.data_ptr() if its is not None else 0, status=status.data_ptr(),
         n_iter=n_iter.data_ptr(), cond_est=cond.data_ptr())

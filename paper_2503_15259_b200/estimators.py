@@ -172,6 +172,12 @@ def bounds_for(problem, sample=None) -> tuple[float, float]:
 def prior_arrays(problem, n_devices: int, n_antennas: int) -> dict:
     """Device-side prior inputs for ``device.solve`` from a Problem."""
     if problem.kind == "map-k":
+        if hasattr(problem.prior, "c2"):   # pairwise MVB (priors.py:56-106)
+            pr = problem.prior
+            if not isinstance(pr, priors.PairwiseMvbPrior):
+                pr = priors.PairwiseMvbPrior(pr.c1, pr.c2)
+            return {"prior_c1": np.broadcast_to(pr.c1, (n_devices,)).astype(float),
+                    "prior_c2": pr.csr_arrays()}
         return {"prior_lin": priors.known_prior_gradient(problem.prior, n_antennas, n_devices)}
     if problem.kind == "map-ur":
         p = np.broadcast_to(np.asarray(problem.prior.p, dtype=float), (n_devices,)).copy()

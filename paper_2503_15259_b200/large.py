@@ -204,8 +204,10 @@ def column_shard(n_devices: int, rank: int, world: int) -> slice:
 
 def psca_run_large(kind, pilots, gains, emp_cov, noise, n_antennas, steps, *, max_iter, tol=0.0,
                    prior_lin=None, prior_p=None, eff_prior=None, record_objective=False,
-                   record_iterates=False, group=None) -> dict:
+                   record_iterates=False, group=None, prior_c1=None, prior_c2=None) -> dict:
     """Solve one instance with the large-L step loop (columns = this rank's shard)."""
+    if prior_c1 is not None or prior_c2 is not None:
+        raise NotImplementedError("pairwise MAP-K prior on the large-L path (L > 128)")
     st = GpuLargeStepper(kind, pilots, gains, emp_cov, noise, n_antennas, steps,
                          max_iter=max_iter, tol=tol, prior_lin=prior_lin, prior_p=prior_p,
                          eff_prior=eff_prior, record_objective=record_objective,

@@ -35,6 +35,93 @@ class IndependentPrior:
         return np.log(self.p / (1.0 - self.p))
 
 
+@dataclass
+class PairwiseMvbPrior:
+    """Order-2 multivariate-Bernoulli prior exp(c1.a + sum_{n<m} c2_nm a_n a_m)/Z
+    (priors.py:56-106).  c2 is kept as a symmetric CSR matrix with zero
+    diagonal; one given triangle is mirrored.  On the GPU path the MAP-K
+    gradient -(c1 + c2 x)/M is evaluated at every iterate by the factor kernel
+    (CSR passed through ``psca_solve_args.prior_c2_*``)."""
+
+    c1: np.ndarray
+    c2: object
+
+    def __post_init__(self):
+        import scipy.sparse as sp
+        self.c1 = np.asarray(self.c1, dtype=float)
+        c2 = sp.csr_matrix(self.c2)
+        c2.setdiag(0.0)
+        c2.eliminate_zeros()
+        if (c2 != c2.T).nnz:
+            upper = sp.triu(c2, k=1)
+            c2 = upper + upper.T
+        self.c2 = sp.csr_matrix(c2)
+
+    def scaled(self, s: float) -> "PairwiseMvbPrior":
+        return PairwiseMvbPrior(self.c1 * s, self.c2 * s)
+
+    @classmethod
+    def from_independent(cls, prior: IndependentPrior) -> "PairwiseMvbPrior":
+        import scipy.sparse as sp
+        n = prior.p.shape[0]
+        return cls(prior.log_odds, sp.csr_matrix((n, n)))
+
+    @classmethod
+    def from_group_model(cls, n_devices: int, group_size: int, p_group: float,
+                         coeff_cap: float = 12.0) -> "PairwiseMvbPrior":
+        """Coefficients for contiguous groups of ``group_size`` devices that are
+        active together with probability p_group (priors.py:84-106)."""
+        import scipy.sparse as sp
+        if n_devices % group_size:
+            raise DomainError("group_size must divide n_devices")
+        a, b = fit_group_coefficients(group_size, p_group, coeff_cap)
+        c1 = np.full(n_devices, a)
+        if group_size == 1:
+            return cls(c1, sp.csr_matrix((n_devices, n_devices)))
+        block = b * (np.ones((group_size, group_size)) - np.eye(group_size))
+        c2 = sp.block_diag([sp.csr_matrix(block)] * (n_devices // group_size), format="csr")
+        return cls(c1, c2)
+
+    def csr_arrays(self):
+        """(indptr, indices, data) of c2, int32 / float64, rows in index order."""
+        c2 = self.c2.tocsr()
+        c2.sort_indices()
+        return (c2.indptr.astype(np.int32), c2.indices.astype(np.int32),
+                c2.data.astype(np.float64))
+
+
+def fit_group_coefficients(group_size: int, p: float, cap: float) -> tuple[float, float]:
+    """Exchangeable pairwise fit of the group law (priors.py:109-139): within a
+    group the model p.m.f. depends on the active count k only,
+    P(k) ~ C(G,k) exp(a k + b k(k-1)/2); (a, b) maximise the expected
+    log-likelihood G p a + C(G,2) p b - log Z(a, b) under the true law
+    (E a_n = E a_n a_m = p), box-constrained by the cap."""
+    import scipy.optimize
+    import scipy.special
+    g = group_size
+    if g == 1:
+        return float(np.clip(math.log(p / (1.0 - p)), -cap, cap)), 0.0
+    k = np.arange(g + 1)
+    log_binom = np.array([math.lgamma(g + 1) - math.lgamma(i + 1) - math.lgamma(g - i + 1)
+                          for i in k])
+    pairs = k * (k - 1) / 2.0
+    n_pairs = g * (g - 1) / 2.0
+
+    def objective(theta):
+        a, b = theta
+        logits = log_binom + a * k + b * pairs
+        logz = scipy.special.logsumexp(logits)
+        w = np.exp(logits - logz)
+        val = -(g * p * a + n_pairs * p * b - logz)
+        grad = -np.array([g * p - float(w @ k), n_pairs * p - float(w @ pairs)])
+        return val, grad
+
+    res = scipy.optimize.minimize(objective, x0=np.array([math.log(p / (1 - p)), 0.0]),
+                                  jac=True, method="L-BFGS-B",
+                                  bounds=[(-cap, cap), (-2 * cap - 8, 2 * cap + 8)])
+    return float(res.x[0]), float(res.x[1])
+
+
 def known_prior_gradient(prior, n_antennas: int, n: int) -> np.ndarray:
     """Constant MAP-K gradient term -log(p/(1-p))/M (priors.py:154-158).
 
@@ -42,8 +129,7 @@ def known_prior_gradient(prior, n_antennas: int, n: int) -> np.ndarray:
     the value the kernel adds is bitwise the reference's.
     """
     if hasattr(prior, "c2"):
-        raise NotImplementedError(
-            "PairwiseMvbPrior (group activity) is not on the GPU path yet (SURVEY.md 8(f) item 4)")
+        raise DomainError("a pairwise prior has an iterate-dependent gradient (prior_c1/prior_c2)")
     log_odds = np.log(prior.p / (1.0 - prior.p))
     return np.broadcast_to(-log_odds / n_antennas, (n,)).copy()
 

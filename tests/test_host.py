@@ -24,18 +24,38 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(str(device.LIB_PATH))
     for name in sorted(declared):
         assert hasattr(lib, name), f"{name} declared in psca.h but not exported"
-    assert declared <= set(device.EXPORTED_SYMBOLS) | {"psca_last_path"}
+    from paper_2503_15259_b200 import large
+    assert declared <= set(device.EXPORTED_SYMBOLS) | set(large.EXPORTED_SYMBOLS) | {"psca_last_path"}
     assert device.load().psca_version().decode().startswith("psca-b200")
 
 
-def test_solve_args_struct_matches_header_layout():
+def _c_offsets(struct: str, fields, tmp_path) -> dict:
+    """offsetof / sizeof of a psca.h struct as the C compiler lays it out."""
+    import subprocess
+    src = tmp_path / f"{struct}.c"
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "psca.h"', "int main(void) {"]
+    for f in fields:
+        lines.append(f'  printf("{f} %zu\\n", offsetof({struct}, {f}));')
+    lines.append(f'  printf("__size__ %zu\\n", sizeof({struct}));')
+    lines.append("  return 0; }")
+    src.write_text("\n".join(lines))
+    exe = tmp_path / struct
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), "-o", str(exe), str(src)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    return {k: int(v) for k, v in (ln.split() for ln in out.strip().splitlines())}
+
+
+def test_solve_args_struct_matches_header_layout(tmp_path):
+    """The ctypes mirrors match the C compiler's layout of include/psca.h field by field."""
     from paper_2503_15259_b200.device import EffPriorC, SolveArgsC
+    from paper_2503_15259_b200.large import LargeArgsC
     assert ctypes.sizeof(EffPriorC) == 10 * 8
-    # ints (6) + tol + 2 ints -> 40 bytes before the pointer block, 7 pointers,
-    # the prior struct, 7 more pointers
-    assert SolveArgsC.pilots.offset == 40
-    assert SolveArgsC.eff.offset == 40 + 7 * 8
-    assert ctypes.sizeof(SolveArgsC) == 40 + 7 * 8 + 80 + 7 * 8
+    for cls, name in ((SolveArgsC, "psca_solve_args"), (LargeArgsC, "psca_large_args")):
+        fields = [f[0] for f in cls._fields_]
+        c = _c_offsets(name, fields, tmp_path)
+        for f in fields:
+            assert getattr(cls, f).offset == c[f], (name, f)
+        assert ctypes.sizeof(cls) == c["__size__"], name
 
 
 def test_workspace_query_rejects_bad_arguments():
