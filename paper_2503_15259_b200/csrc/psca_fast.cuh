@@ -30,6 +30,9 @@
 #ifndef PSCA_QCB
 #define PSCA_QCB 1
 #endif
+#ifndef PSCA_UPD_ONE
+#define PSCA_UPD_ONE 1
+#endif
 constexpr int QCB = PSCA_QCB;                // 8-column blocks per warp in the quad stage
 constexpr int QPARTS = NWARP / (NCB / QCB);  // row-block groups (LPT-balanced)
 
@@ -46,7 +49,7 @@ struct TG {
     static constexpr size_t S_BYTES = (size_t)LP8 * NCT * 16;
     static constexpr size_t W_BYTES = (size_t)LP8 * WCAP * 16;
     static constexpr size_t F_BYTES = (size_t)NB * FRAG_SLOTS * 16;
-    static constexpr size_t SMALL = (size_t)QPARTS * NCT * 2 * 8;   // quad partials
+    static constexpr size_t SMALL = (size_t)QPARTS * NCT * 2 * 8 + NCT * 8;   // quad partials, v
     static constexpr size_t TILE_BYTES = 2 * S_BYTES + 2 * W_BYTES;
     // Fragments are staged in SMEM beside the tile buffers: lane-ready
     // (FRAG_SLOTS = 24 per block, {re, im, -im}) when that fits (NRB <= 16),
@@ -242,7 +245,7 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         const int ncol = col0 + lane;
         const bool cvalid = ncol < n_end;
         double x = 0.0, g = 1.0, pg = 0.0;
-        if (cvalid) {
+        if (cvalid && (!PSCA_UPD_ONE || warp == 0)) {
             x = x_cur[ncol];
             if (known) g = a.gains[bN + ncol];
             if (a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.pairwise))
@@ -312,8 +315,15 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
         __syncthreads();
 
         // ---- phase B: update (estimators.py:272-276) + packed WS / SP --------
+        // The per-device update runs in warp 0 only (lane = column) and is
+        // broadcast through SMEM: its DDIV/DMUL chain shares the FP64 pipe
+        // with the other CTA's DMMAs, so it is not replicated per warp.
         {
             double v = 0.0;
+#if PSCA_UPD_ONE
+            double* v_s = qr_s + QPARTS * NCT * 2;
+            if (warp == 0) {
+#endif
             if (cvalid) {
                 double q = qr_s[2 * lane], r = qr_s[2 * lane + 1];
 #pragma unroll
@@ -343,6 +353,12 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
                     p_minq = (q < p_minq) ? q : p_minq;
                 }
             }
+#if PSCA_UPD_ONE
+                v_s[lane] = v;
+            }
+            __syncthreads();
+            v = v_s[lane];
+#endif
             const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
             const int nnz = __popc(mask);
             const int pos = __popc(mask & ((1u << lane) - 1u));
