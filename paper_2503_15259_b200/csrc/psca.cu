@@ -700,81 +700,83 @@ __device__ void pack_frags(const double2* X, const double2* G, int ld, int L, co
     }
 }
 
-// Sigma (lower + mirrored) from the chunk partial C fragments + sigma^2 I
-// Sigma (lower + mirrored) from the chunk partial C fragments + sigma^2 I.
-// Incremental mode: the partials are the increment S diag(rho_k cand g) S^H,
-// and D_{k+1} = (1 - rho_k) D_k + increment is kept per instance in a.dmat
-// (D_0 = 0); Sigma = D + sigma^2 I.  Full mode: the partials are D itself.
+// Per-instance stride (double2) of the incremental D store: the two-kernel
+// path keeps D in the rebuild C-fragment layout ([NBLK][32]), the persistent
+// path as a dense L x L lower triangle.
+__host__ __device__ inline size_t dmat_stride(const Geo& g, int L) {
+    const size_t frag = (size_t)g.NBLK * 32, dense = (size_t)L * L;
+    return frag > dense ? frag : dense;
+}
+
+// Sigma from the chunk partial C fragments + sigma^2 I, in one pass: each
+// fragment element gives one component of a lower entry (l, m), written with
+// its conjugate mirror and sigma^2 on the diagonal.  Incremental mode: the
+// partials are the increment S diag(rho_k cand g) S^H and
+// D_{k+1} = (1 - rho_k) D_k + increment is kept per instance in a.dmat in the
+// same fragment layout (D_0 = 0); Sigma = D + sigma^2 I.  Full mode: the
+// partials are D itself.  Entries with a row or column in [L, LP) are left
+// undefined (the factor reads rows / columns < L only).
 __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2* X, int ld,
                                bool zero_weights) {
     const int L = a.L;
-    for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
-        int i = e / L, j = e - i * L;
-        X[i * ld + j] = make_double2(0.0, 0.0);
-    }
-    __syncthreads();
     double* Xd = reinterpret_cast<double*>(X);
-    double* Dd = a.incremental ? reinterpret_cast<double*>(a.dmat + (size_t)b * L * L) : nullptr;
+    double2* D = a.incremental ? a.dmat + (size_t)b * dmat_stride(geo, L) : nullptr;
     const double omr = (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[a.k_new - 1]) : 0.0;
-    {
-        const int total = geo.NBLK * 32;
-        const double2* sp = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
-        for (int e = threadIdx.x; e < total; e += blockDim.x) {
-            int blk = e >> 5, lane = e & 31;
-            // decode (i, j) of rebuild block blk
-            int i = 0, base = 0;
-            while (base + (4 * i + 3) / 8 + 1 <= blk) { base += (4 * i + 3) / 8 + 1; ++i; }
-            int j = blk - base;
-            double2 s = make_double2(0.0, 0.0);
-            if (!zero_weights) {
-                // loads in batches of 8 (memory-level parallelism), adds in chunk order
-                const size_t cs = (size_t)geo.NBLK * 32;
-                int c = 0;
-                for (; c + 8 <= a.n_chunks; c += 8) {
-                    double2 v[8];
+    const double s2 = a.noise[b];
+    const double2* sp = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
+    const size_t cs = (size_t)geo.NBLK * 32;
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    int i = 0, base = 0;   // row block of blk, index of its first block (monotone walk)
+    for (int blk = threadIdx.x >> 5; blk < geo.NBLK; blk += nw) {
+        while (base + (4 * i + 3) / 8 + 1 <= blk) {
+            base += (4 * i + 3) / 8 + 1;
+            ++i;
+        }
+        const int j = blk - base;
+        const int e = blk * 32 + lane;
+        double2 s = make_double2(0.0, 0.0);
+        if (!zero_weights) {
+            // loads in batches of 8 (memory-level parallelism), adds in chunk order
+            int c = 0;
+            for (; c + 8 <= a.n_chunks; c += 8) {
+                double2 v[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) v[u] = sp[(size_t)(c + u) * cs + e];
+                for (int u = 0; u < 8; ++u) v[u] = sp[(size_t)(c + u) * cs + e];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        s.x += v[u].x;
-                        s.y += v[u].y;
-                    }
-                }
-                for (; c < a.n_chunks; ++c) {
-                    const double2 v = sp[(size_t)c * cs + e];
-                    s.x += v.x;
-                    s.y += v.y;
+                for (int u = 0; u < 8; ++u) {
+                    s.x += v[u].x;
+                    s.y += v[u].y;
                 }
             }
-            int r8 = lane >> 2, c4 = lane & 3;
-            int l = 4 * i + (r8 >> 1), p = r8 & 1;
-            int m0 = 8 * j + 2 * c4;
-            if (l < L) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int m = m0 + h;
-                    if (m <= l) {
-                        const size_t o = 2 * ((size_t)l * L + m) + p;
-                        double val = h ? s.y : s.x;
-                        if (Dd) {
-                            val = zero_weights ? 0.0 : fma(omr, Dd[o], val);
-                            Dd[o] = val;
-                        }
-                        Xd[2 * (l * ld + m) + p] = val;
-                    }
-                }
+            for (; c < a.n_chunks; ++c) {
+                const double2 v = sp[(size_t)c * cs + e];
+                s.x += v.x;
+                s.y += v.y;
             }
         }
-    }
-    __syncthreads();
-    const double s2 = a.noise[b];
-    for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
-        int i = e / L, j = e - i * L;
-        if (i < j) {
-            double2 v = X[j * ld + i];
-            X[i * ld + j] = make_double2(v.x, -v.y);
-        } else if (i == j) {
-            X[i * ld + i] = make_double2(X[i * ld + i].x + s2, 0.0);
+        if (D) {
+            if (zero_weights) {
+                s = make_double2(0.0, 0.0);
+            } else {
+                const double2 d = D[e];
+                s = make_double2(fma(omr, d.x, s.x), fma(omr, d.y, s.y));
+            }
+            D[e] = s;
+        }
+        const int l = 4 * i + (r8 >> 1), p = r8 & 1;
+        if (l < L) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int m = 8 * j + 2 * c4 + h;
+                const double v = h ? s.y : s.x;
+                if (m < l) {
+                    Xd[2 * (l * ld + m) + p] = v;
+                    Xd[2 * (m * ld + l) + p] = p ? -v : v;
+                } else if (m == l) {
+                    Xd[2 * (l * ld + l) + p] = p ? 0.0 : v + s2;
+                }
+            }
         }
     }
     __syncthreads();
@@ -1453,7 +1455,7 @@ FacArgs sub_fac(const FacArgs& f, int b0, int Bh, const Geo& g) {
     if (f.objective) r.objective = f.objective + (size_t)b0 * f.T;
     if (f.scratch) r.scratch = f.scratch + (size_t)b0 * 2 * g.LP * (g.LP + 1);
     if (f.pgrad) r.pgrad = f.pgrad + (size_t)b0 * N;
-    if (f.dmat) r.dmat = f.dmat + (size_t)b0 * L * L;
+    if (f.dmat) r.dmat = f.dmat + (size_t)b0 * dmat_stride(g, L);
     return r;
 }
 
@@ -1481,7 +1483,7 @@ SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, v
     const bool pg = a->kind == PSCA_MAP_UR || (a->kind == PSCA_MAP_K && a->prior_c2_indptr);
     s.pgrad = cv.take<double>(pg ? (size_t)a->B * a->N * 8 : 0);
     s.counter = cv.take<int>(sizeof(int));
-    s.dmat = cv.take<double2>((size_t)a->B * a->L * a->L * 16);
+    s.dmat = cv.take<double2>((size_t)a->B * dmat_stride(g, a->L) * 16);
     s.scratch = cv.take<double2>(fac_scratch_bytes(g, a->B));
     s.total = cv.off;
     return s;

@@ -908,7 +908,7 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
 
         // ---- iterate 0: prior terms at x = 0, Sigma_0 = sigma^2 I, D_0 = 0 --
         if (fa.incremental) {
-            double2* D = fa.dmat + (size_t)b * L * L;
+            double2* D = fa.dmat + (size_t)b * dmat_stride(geo, L);
             for (int e = tid; e < L * L; e += NT) D[e] = make_double2(0.0, 0.0);
         }
         double pv = fac_prior_terms_at(fa, b, xc, sred);
@@ -947,7 +947,7 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
                 // ---- factorisation at x_{k+1} ---------------------------------
                 pv = fac_prior_terms_at(fa, b, xn, sred);
                 acc_to_sigma<NRB>(acc, slot, nbw, X, ld, L,
-                                  fa.incremental ? reinterpret_cast<double*>(fa.dmat + (size_t)b * L * L)
+                                  fa.incremental ? reinterpret_cast<double*>(fa.dmat + (size_t)b * dmat_stride(geo, L))
                                                  : nullptr,
                                   __dsub_rn(1.0, fa.steps[k]));
                 finish_sigma(X, ld, L, fa.noise[b]);
