@@ -587,19 +587,29 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
             const int i0 = 2 * bi[u], j0 = 2 * bj[u];
             const double2 ci[2] = {cb[i0], cb[i0 + 1]};
             const double2 cj[2] = {cb[j0], cb[j0 + 1]};
+            // u_j = conj(c_j) / d (also the new row-k entries a_kj / d, since
+            // a_kj = conj(c_j)); w_i = c_i / d (new column-k entries), only for
+            // the blocks holding column k
+            double2 uj[2], wi[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj) uj[dj] = make_double2(cj[dj].x * dinv, -cj[dj].y * dinv);
+            if (j0 == (k & ~1)) {
+#pragma unroll
+                for (int di = 0; di < 2; ++di) wi[di] = make_double2(ci[di].x * dinv, ci[di].y * dinv);
+            }
 #pragma unroll
             for (int di = 0; di < 2; ++di)
 #pragma unroll
                 for (int dj = 0; dj < 2; ++dj) {
                     const int i = i0 + di, j = j0 + dj;
                     const double2 o = v[u][di][dj];
-                    // c_i conj(c_j)
-                    const double pr = ci[di].x * cj[dj].x + ci[di].y * cj[dj].y;
-                    const double pim = ci[di].y * cj[dj].x - ci[di].x * cj[dj].y;
-                    double nx = o.x - pr * dinv, ny = o.y - pim * dinv;
-                    const bool onrow = (i == k) || (j == k);
-                    nx = onrow ? o.x * dinv : nx;
-                    ny = onrow ? o.y * dinv : ny;
+                    // a_ij - c_i u_j
+                    double nx = fma(-ci[di].x, uj[dj].x, fma(ci[di].y, uj[dj].y, o.x));
+                    double ny = fma(-ci[di].x, uj[dj].y, fma(-ci[di].y, uj[dj].x, o.y));
+                    nx = (i == k) ? uj[dj].x : nx;
+                    ny = (i == k) ? uj[dj].y : ny;
+                    nx = (j == k) ? wi[di].x : nx;
+                    ny = (j == k) ? wi[di].y : ny;
                     nx = (i == k && j == k) ? -dinv : nx;
                     ny = (i == k && j == k) ? 0.0 : ny;
                     if (i < j) { nx = 0.0; ny = 0.0; }
