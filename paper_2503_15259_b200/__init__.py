@@ -6,7 +6,8 @@ meanings and error behaviour, with the PSCA iteration running as hand-written
 sm_100a CUDA kernels behind the C ABI in include/psca.h.  Batched entry
 points (``psca_run_batch``, ``unroll.forward_batch``) are the throughput path;
 ``harness`` runs the reference's experiment grid on GPU batches and
-``unroll.train`` tunes PSCA-Nets with batched device forwards.
+``unroll.train`` tunes PSCA-Nets with batched device forwards;
+``baselines.pg_ml_batch`` is the projected-gradient comparison detector.
 """
 
 from .sysmodel import (ActivityModel, DomainError, Sample, SystemConfig, empirical_cov,

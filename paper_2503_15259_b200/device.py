@@ -267,59 +267,93 @@ def empirical_cov(y, n_antennas: int):
     return res[0] if single else res
 
 
-def cov_unknown(pilots, weights, noise):
+def cov_unknown_t(S, W, Nz):
+    """Sigma = S diag(W) S^H + sigma^2 I for device tensors S (B,L,N) c128, W (B,N), Nz (B,)."""
     torch = _torch()
     lib = load()
+    B, L, N = S.shape
+    out = torch.empty((B, L, L), dtype=torch.complex128, device=S.device)
+    ws = _workspace(torch, lib.psca_cov_workspace_bytes(B, N, L), S.device)
+    _check(lib.psca_cov_unknown(_ptr(S), _ptr(W), _ptr(Nz), B, N, L, _ptr(out), _ptr(ws),
+                                ctypes.c_size_t(ws.numel()), _stream(torch)), "psca_cov_unknown")
+    return out
+
+
+def hpd_inverse_t(X):
+    """(inverse, status, cond_est, logdet) device tensors for Hermitian PD X (B,L,L)."""
+    torch = _torch()
+    lib = load()
+    B, L, _ = X.shape
+    out = torch.empty_like(X)
+    status = torch.empty(B, dtype=torch.int32, device=X.device)
+    cond = torch.empty(B, dtype=torch.float64, device=X.device)
+    logdet = torch.empty(B, dtype=torch.float64, device=X.device)
+    ws = _workspace(torch, lib.psca_inverse_workspace_bytes(B, L), X.device)
+    _check(lib.psca_hpd_inverse(_ptr(X), B, L, _ptr(out), _ptr(status), _ptr(cond), _ptr(logdet),
+                                _ptr(ws), ctypes.c_size_t(ws.numel()), _stream(torch)),
+           "psca_hpd_inverse")
+    return out, status, cond, logdet
+
+
+def quad_forms_t(S, P, E):
+    """(q, r) device tensors (B,N) for S (B,L,N), P = Sigma^-1 and E = Sigma_hat (B,L,L)."""
+    torch = _torch()
+    lib = load()
+    B, L, N = S.shape
+    q = torch.empty((B, N), dtype=torch.float64, device=S.device)
+    r = torch.empty((B, N), dtype=torch.float64, device=S.device)
+    ws = _workspace(torch, lib.psca_quad_workspace_bytes(B, N, L), S.device)
+    _check(lib.psca_quad_forms(_ptr(S), _ptr(P), _ptr(E), B, N, L, _ptr(q), _ptr(r), _ptr(ws),
+                               ctypes.c_size_t(ws.numel()), _stream(torch)), "psca_quad_forms")
+    return q, r
+
+
+def eval_objective_t(X, P, E):
+    """(value, status) device tensors (B,) of log|Sigma| + tr(Sigma^-1 Sigma_hat)."""
+    torch = _torch()
+    lib = load()
+    B, L, _ = X.shape
+    out = torch.empty(B, dtype=torch.float64, device=X.device)
+    status = torch.empty(B, dtype=torch.int32, device=X.device)
+    ws = _workspace(torch, lib.psca_objective_workspace_bytes(B, L), X.device)
+    _check(lib.psca_eval_objective(_ptr(X), _ptr(P), _ptr(E), B, L, _ptr(out), _ptr(status),
+                                   _ptr(ws), ctypes.c_size_t(ws.numel()), _stream(torch)),
+           "psca_eval_objective")
+    return out, status
+
+
+def _cdev(torch):
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def cov_unknown(pilots, weights, noise):
+    torch = _torch()
     pa, single = _batched(pilots, 2)
     wa = np.asarray(weights, dtype=float).reshape(pa.shape[0], pa.shape[2])
     na = np.broadcast_to(np.asarray(noise, dtype=float), (pa.shape[0],)).copy()
-    dev = torch.device("cuda", torch.cuda.current_device())
-    S = _dev(torch, pa, torch.complex128, dev)
-    W = _dev(torch, wa, torch.float64, dev)
-    Nz = _dev(torch, na, torch.float64, dev)
-    B, L, N = S.shape
-    out = torch.empty((B, L, L), dtype=torch.complex128, device=dev)
-    ws = _workspace(torch, lib.psca_cov_workspace_bytes(B, N, L), dev)
-    _check(lib.psca_cov_unknown(_ptr(S), _ptr(W), _ptr(Nz), B, N, L, _ptr(out), _ptr(ws),
-                                ctypes.c_size_t(ws.numel()), _stream(torch)), "psca_cov_unknown")
-    res = out.cpu().numpy()
+    dev = _cdev(torch)
+    res = cov_unknown_t(_dev(torch, pa, torch.complex128, dev), _dev(torch, wa, torch.float64, dev),
+                        _dev(torch, na, torch.float64, dev)).cpu().numpy()
     return res[0] if single else res
 
 
 def hpd_inverse(sigma):
     """Returns (inverse, status, cond_est, logdet) as numpy arrays."""
     torch = _torch()
-    lib = load()
     sa, single = _batched(sigma, 2)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    X = _dev(torch, sa, torch.complex128, dev)
-    B, L, _ = X.shape
-    out = torch.empty_like(X)
-    status = torch.empty(B, dtype=torch.int32, device=dev)
-    cond = torch.empty(B, dtype=torch.float64, device=dev)
-    logdet = torch.empty(B, dtype=torch.float64, device=dev)
-    ws = _workspace(torch, lib.psca_inverse_workspace_bytes(B, L), dev)
-    _check(lib.psca_hpd_inverse(_ptr(X), B, L, _ptr(out), _ptr(status), _ptr(cond), _ptr(logdet),
-                                _ptr(ws), ctypes.c_size_t(ws.numel()), _stream(torch)),
-           "psca_hpd_inverse")
-    res = (out.cpu().numpy(), status.cpu().numpy(), cond.cpu().numpy(), logdet.cpu().numpy())
+    res = tuple(t.cpu().numpy()
+                for t in hpd_inverse_t(_dev(torch, sa, torch.complex128, _cdev(torch))))
     return tuple(r[0] for r in res) if single else res
 
 
 def quad_forms(pilots, sigma_inv, emp_cov):
     torch = _torch()
-    lib = load()
     pa, single = _batched(pilots, 2)
     B, L, N = pa.shape
-    dev = torch.device("cuda", torch.cuda.current_device())
-    S = _dev(torch, pa, torch.complex128, dev)
-    P = _dev(torch, np.asarray(sigma_inv).reshape(B, L, L), torch.complex128, dev)
-    E = _dev(torch, np.asarray(emp_cov).reshape(B, L, L), torch.complex128, dev)
-    q = torch.empty((B, N), dtype=torch.float64, device=dev)
-    r = torch.empty((B, N), dtype=torch.float64, device=dev)
-    ws = _workspace(torch, lib.psca_quad_workspace_bytes(B, N, L), dev)
-    _check(lib.psca_quad_forms(_ptr(S), _ptr(P), _ptr(E), B, N, L, _ptr(q), _ptr(r), _ptr(ws),
-                               ctypes.c_size_t(ws.numel()), _stream(torch)), "psca_quad_forms")
+    dev = _cdev(torch)
+    q, r = quad_forms_t(_dev(torch, pa, torch.complex128, dev),
+                        _dev(torch, np.asarray(sigma_inv).reshape(B, L, L), torch.complex128, dev),
+                        _dev(torch, np.asarray(emp_cov).reshape(B, L, L), torch.complex128, dev))
     qn, rn = q.cpu().numpy(), r.cpu().numpy()
     return (qn[0], rn[0]) if single else (qn, rn)
 
@@ -327,20 +361,15 @@ def quad_forms(pilots, sigma_inv, emp_cov):
 def eval_objective(sigma, sigma_inv, emp_cov):
     """Returns (value, status) numpy arrays."""
     torch = _torch()
-    lib = load()
     sa, single = _batched(sigma, 2)
     B, L, _ = sa.shape
-    dev = torch.device("cuda", torch.cuda.current_device())
-    X = _dev(torch, sa, torch.complex128, dev)
-    P = _dev(torch, np.asarray(sigma_inv).reshape(B, L, L), torch.complex128, dev)
-    E = _dev(torch, np.asarray(emp_cov).reshape(B, L, L), torch.complex128, dev)
-    out = torch.empty(B, dtype=torch.float64, device=dev)
-    status = torch.empty(B, dtype=torch.int32, device=dev)
-    ws = _workspace(torch, lib.psca_objective_workspace_bytes(B, L), dev)
-    _check(lib.psca_eval_objective(_ptr(X), _ptr(P), _ptr(E), B, L, _ptr(out), _ptr(status),
-                                   _ptr(ws), ctypes.c_size_t(ws.numel()), _stream(torch)),
-           "psca_eval_objective")
-    v, s = out.cpu().numpy(), status.cpu().numpy()
+    dev = _cdev(torch)
+    v, s = eval_objective_t(_dev(torch, sa, torch.complex128, dev),
+                            _dev(torch, np.asarray(sigma_inv).reshape(B, L, L), torch.complex128,
+                                 dev),
+                            _dev(torch, np.asarray(emp_cov).reshape(B, L, L), torch.complex128,
+                                 dev))
+    v, s = v.cpu().numpy(), s.cpu().numpy()
     return (v[0], s[0]) if single else (v, s)
 
 
