@@ -1494,6 +1494,7 @@ int check_solve_args(const psca_solve_args* a) {
     if (a->kind < PSCA_ML_K || a->kind > PSCA_MAP_UR) return PSCA_E_ARG;
     if (a->L > MAX_L_TILE) return PSCA_E_UNSUPPORTED;
     if (a->n_antennas < 1) return PSCA_E_ARG;
+    if (a->B == 0) return PSCA_OK;   // empty batch: nothing is read or written
     if (!a->pilots || !a->emp_cov || !a->noise || !a->x_out || !a->status || !a->n_iter)
         return PSCA_E_ARG;
     if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
