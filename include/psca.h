@@ -182,6 +182,34 @@ int psca_large_columns(const psca_large_args* a, int k, void* workspace, size_t 
 int psca_large_factor(const psca_large_args* a, int k, void* workspace, size_t workspace_bytes,
                       void* stream);
 
+/* One block-coordinate-descent sweep over all devices of every instance
+ * (baselines.py:54-150 bcd_ml / bcd_map_k, the sequential comparison
+ * detector): per device the exact coordinate minimiser on the current
+ * Sigma^-1, then a Sherman-Morrison rank-1 update of Sigma^-1
+ * (covlinalg.py:118-131).  x and sigma_inv carry the state between sweeps;
+ * init = 1 starts from x = 0, Sigma^-1 = I / sigma^2.  status[b] = 1 when a
+ * rank-1 denominator falls below 1e-14 (the reference's SingularUpdateError).
+ * L <= 128 and the per-instance state must fit one SM's shared memory. */
+typedef struct {
+    int kind;               /* PSCA_ML_K, PSCA_MAP_K or PSCA_ML_UD               */
+    int B, N, L, n_antennas;
+    int init;
+    const double* pilots;   /* [B][L][N] complex128                            */
+    const double* gains;    /* [B][N] (known-pathloss kinds)                   */
+    const double* emp_cov;  /* [B][L][L] complex128                            */
+    const double* noise;    /* [B]                                             */
+    const double* prior_lin;/* map-k, independent prior: [N] = -log(p/(1-p))/M */
+    const double* prior_c1; /* map-k, pairwise prior (CSR c2), else 0          */
+    const int* prior_c2_indptr;
+    const int* prior_c2_indices;
+    const double* prior_c2_data;
+    double* x;              /* [B][N] in / out                                 */
+    double* sigma_inv;      /* [B][L][L] complex128 in / out                   */
+    int* status;            /* [B] in / out, 0 = running                       */
+} psca_bcd_args;
+
+int psca_bcd_sweep(const psca_bcd_args* a, void* stream);
+
 /* Number of kernel launches the last psca_solve on this thread issued
  * (reported as bench.py's gpu_launches). */
 int psca_last_launch_count(void);

@@ -12,18 +12,22 @@ objective of the samples that have not accepted yet, in one batched call.
 The per-sample scalars (BB step, Grippo reference value, acceptance) are
 device-tensor arithmetic between those calls.
 
-BCD (sequential rank-1 Woodbury sweeps, baselines.py:54-150) is not
-provided: it is inherently sequential per device and outside the PSCA path.
+BCD (baselines.py:54-150) sweeps the devices in order with exact coordinate
+minimisers and Sherman-Morrison updates of Sigma^-1: one CTA per instance
+runs a whole sweep in the ``psca_bcd_sweep`` kernel (csrc/psca_bcd.cuh), the
+per-sweep trace objective comes from the batched covariance / objective
+kernels.
 """
 
 from __future__ import annotations
 
+import ctypes
 import time
 
 import numpy as np
 
 from . import device
-from .covlinalg import ConditioningError
+from .covlinalg import ConditioningError, SingularUpdateError
 from .estimators import DetectorTrace, Problem
 from .sysmodel import DomainError
 
@@ -158,3 +162,100 @@ def pg_ml(sample, known: bool = True, max_iter: int = 30, step_mode: str = "nonm
           d0: float | None = None, window: int = 10) -> DetectorTrace:
     """Projected gradient on one sample (baselines.py:156-223)."""
     return pg_ml_batch([sample], known, max_iter, step_mode, d0, window)[0]
+
+
+# ---------------------------------------------------------------------------
+# block coordinate descent (baselines.py:54-150)
+# ---------------------------------------------------------------------------
+
+def _bcd_batch(problem: Problem, samples, max_iter: int) -> list:
+    from .estimators import prior_arrays
+    torch = device._torch()
+    lib = device.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S, E, G, noise = _stack(samples, torch, dev)
+    B, L, N = S.shape
+    m = samples[0].received.shape[1]
+    known = problem.known_pathloss
+    kw = prior_arrays(problem, N, m)
+    keep = []
+
+    def put(v, dt):
+        if v is None:
+            return 0
+        t = torch.as_tensor(np.ascontiguousarray(v), device=dev).to(dt)
+        keep.append(t)
+        return t.data_ptr()
+
+    c2 = kw.get("prior_c2")
+    x = torch.zeros((B, N), dtype=torch.float64, device=dev)
+    pinv = torch.zeros((B, L, L), dtype=torch.complex128, device=dev)
+    status = torch.zeros(B, dtype=torch.int32, device=dev)
+    args = device.BcdArgsC(
+        kind=device.KIND_CODES[problem.kind], B=B, N=N, L=L, n_antennas=m, init=1,
+        pilots=S.data_ptr(), gains=G.data_ptr() if known else 0, emp_cov=E.data_ptr(),
+        noise=noise.data_ptr(), prior_lin=put(kw.get("prior_lin"), torch.float64),
+        prior_c1=put(kw.get("prior_c1"), torch.float64),
+        prior_c2_indptr=put(c2[0], torch.int32) if c2 is not None else 0,
+        prior_c2_indices=put(c2[1] if c2[1].size else np.zeros(1, np.int32), torch.int32)
+        if c2 is not None else 0,
+        prior_c2_data=put(c2[2] if c2[2].size else np.zeros(1), torch.float64)
+        if c2 is not None else 0,
+        x=x.data_ptr(), sigma_inv=pinv.data_ptr(), status=status.data_ptr())
+    traces = [DetectorTrace(meta={"kind": problem.kind, "algorithm": "bcd"}) for _ in range(B)]
+    prev = np.zeros((B, N))
+    for b in range(B):
+        traces[b].iterates.append(prev[b].copy())
+    w_gain = G if known else torch.ones_like(G)
+    for sweep in range(max_iter):
+        t0 = time.perf_counter()
+        args.init = 1 if sweep == 0 else 0
+        device._check(lib.psca_bcd_sweep(ctypes.byref(args), device._stream(torch)),
+                      "psca_bcd_sweep")
+        st = status.cpu().numpy()
+        if st.any():
+            raise SingularUpdateError("rank-1 update denominator below tolerance")
+        elapsed = (time.perf_counter() - t0) / B
+        sig = device.cov_unknown_t(S, (x * w_gain).contiguous(), noise)
+        obj, _ = device.eval_objective_t(sig, pinv, E)
+        obj = obj.cpu().numpy()
+        xh = x.cpu().numpy()
+        if problem.kind == "map-k":
+            obj = obj + _known_prior_value(problem.prior, xh, m)
+        for b in range(B):
+            traces[b].wall_times.append(elapsed)
+            traces[b].update_norm.append(float(np.linalg.norm(xh[b] - prev[b])))
+            traces[b].objective.append(float(obj[b]))
+            traces[b].iterates.append(xh[b].copy())
+        prev = xh
+    for b in range(B):
+        traces[b].final = prev[b].copy()
+    return traces
+
+
+def _known_prior_value(prior, xh, m) -> np.ndarray:
+    """Per-sample -(1/M) log p(alpha) (priors.py:146-151)."""
+    if hasattr(prior, "c2"):
+        c2 = prior.c2
+        return np.array([-(float(prior.c1 @ a) + 0.5 * float(a @ (c2 @ a))) / m for a in xh])
+    lo = np.log(prior.p / (1.0 - prior.p))
+    return np.array([-float(lo @ a) / m for a in xh])
+
+
+def bcd_ml_batch(samples, known: bool = True, max_iter: int = 5) -> list:
+    """Sequential exact coordinate descent on the covariance-fit objective for a
+    batch of same-shape samples (baselines.py:54-63); one trace per sample."""
+    return _bcd_batch(Problem.ml_k() if known else Problem.ml_ud(), samples, max_iter)
+
+
+def bcd_map_k_batch(samples, prior, max_iter: int = 5) -> list:
+    """Coordinate descent on the known-pathloss MAP objective (baselines.py:66-71)."""
+    return _bcd_batch(Problem.map_k(prior), samples, max_iter)
+
+
+def bcd_ml(sample, known: bool = True, max_iter: int = 5) -> DetectorTrace:
+    return bcd_ml_batch([sample], known, max_iter)[0]
+
+
+def bcd_map_k(sample, prior, max_iter: int = 5) -> DetectorTrace:
+    return bcd_map_k_batch([sample], prior, max_iter)[0]

@@ -35,6 +35,10 @@ class ConditioningError(np.linalg.LinAlgError):
         self.cond_estimate = cond_estimate
 
 
+class SingularUpdateError(np.linalg.LinAlgError):
+    """Rank-1 inverse update denominator fell below tolerance (covlinalg.py:39-40)."""
+
+
 def cov_unknown(pilots: np.ndarray, gamma: np.ndarray, noise_power: float,
                 pilots_conj: np.ndarray | None = None) -> np.ndarray:
     """S diag(gamma) S^H + sigma^2 I (covlinalg.py:43-57); ``pilots_conj`` is accepted and unused."""

@@ -1074,6 +1074,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
 
 #include "psca_fast.cuh"
 #include "psca_large.cuh"
+#include "psca_bcd.cuh"
 
 // ---------------------------------------------------------------------------
 // empirical covariance (HERK): Sigma_hat = Y Y^H / M
@@ -1876,6 +1877,30 @@ int psca_cov_unknown(const double* pilots, const double* w, const double* noise,
 size_t psca_inverse_workspace_bytes(int B, int L) {
     if (B < 0 || L < 1) return 0;
     return fac_scratch_bytes(make_geo(L), B);
+}
+
+int psca_bcd_sweep(const psca_bcd_args* a, void* stream) {
+    if (!a || a->B < 0 || a->N < 1 || a->L < 1 || a->n_antennas < 1) return PSCA_E_ARG;
+    if (a->kind != PSCA_ML_K && a->kind != PSCA_MAP_K && a->kind != PSCA_ML_UD)
+        return PSCA_E_ARG;
+    if (a->L > 128) return PSCA_E_UNSUPPORTED;
+    if (a->B == 0) return PSCA_OK;
+    if (!a->pilots || !a->emp_cov || !a->noise || !a->x || !a->sigma_inv || !a->status)
+        return PSCA_E_ARG;
+    if (a->kind != PSCA_ML_UD && !a->gains) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_K && !a->prior_lin &&
+        !(a->prior_c1 && a->prior_c2_indptr && a->prior_c2_indices && a->prior_c2_data))
+        return PSCA_E_ARG;
+    const size_t sm = bcd_smem_bytes(a->L, a->N);
+    if (sm > 227 * 1024) return PSCA_E_UNSUPPORTED;
+    g_launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!ok_or_record(cudaFuncSetAttribute(bcd_sweep_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)))
+        return PSCA_E_CUDA;
+    bcd_sweep_kernel<<<a->B, BCD_NT, sm, st>>>(*a);
+    ++g_launches;
+    return ok_or_record(cudaGetLastError()) ? PSCA_OK : PSCA_E_CUDA;
 }
 
 int psca_hpd_inverse(const double* sigma, int B, int L, double* out, int* status,

@@ -51,6 +51,19 @@ class SolveArgsC(ctypes.Structure):
 
 
 # exported symbols and their signatures (must match include/psca.h)
+class BcdArgsC(ctypes.Structure):
+    """psca_bcd_args (include/psca.h)."""
+    _fields_ = [
+        ("kind", ctypes.c_int), ("B", ctypes.c_int), ("N", ctypes.c_int), ("L", ctypes.c_int),
+        ("n_antennas", ctypes.c_int), ("init", ctypes.c_int),
+        ("pilots", ctypes.c_void_p), ("gains", ctypes.c_void_p), ("emp_cov", ctypes.c_void_p),
+        ("noise", ctypes.c_void_p), ("prior_lin", ctypes.c_void_p), ("prior_c1", ctypes.c_void_p),
+        ("prior_c2_indptr", ctypes.c_void_p), ("prior_c2_indices", ctypes.c_void_p),
+        ("prior_c2_data", ctypes.c_void_p), ("x", ctypes.c_void_p), ("sigma_inv", ctypes.c_void_p),
+        ("status", ctypes.c_void_p),
+    ]
+
+
 _SIGS = {
     "psca_version": (ctypes.c_char_p, []),
     "psca_last_error": (ctypes.c_char_p, []),
@@ -79,6 +92,7 @@ _SIGS = {
                                        ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p]),
+    "psca_bcd_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
     "psca_objective_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int]),
     "psca_eval_objective": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p,

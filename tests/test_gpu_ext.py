@@ -97,14 +97,27 @@ def test_group_prior_grid_matches_reference(cuda_device, ext):
                   str(ext["ggrid_csv"]))
 
 
-def test_bcd_methods_are_reported_as_row_errors(cuda_device):
-    from paper_2503_15259_b200 import harness as h, sysmodel as sm
-    grid = h.ExperimentGrid(methods=["bcd-ml-k", "bcd-map-k"], sweep_name="L", sweep_values=[8],
-                            base=sm.SystemConfig(n_devices=40, pilot_len=8, n_antennas=8),
-                            n_val=2, n_test=2)
-    rows = h.run_grid(grid)
-    assert [r["error"].split(":")[0] for r in rows] == ["NotImplementedError"] * 2
-    assert all(r["error_rate"] == "" for r in rows)
+@pytest.mark.parametrize("kind", ["ml-k", "ml-ud", "map-k", "map-k-pair"])
+def test_bcd_baseline_matches_reference(cuda_device, ext, kind):
+    """Block coordinate descent sweeps (baselines.py:54-150) against the reference."""
+    from paper_2503_15259_b200 import baselines, priors
+    smp = _pg_samples(ext)
+    if kind == "map-k":
+        trs = baselines.bcd_map_k_batch(smp, priors.IndependentPrior(np.full(40, 0.1)), 5)
+    elif kind == "map-k-pair":
+        trs = baselines.bcd_map_k_batch(smp, priors.PairwiseMvbPrior.from_group_model(40, 4, 0.1),
+                                        5)
+    else:
+        trs = baselines.bcd_ml_batch(smp, known=kind == "ml-k", max_iter=5)
+    key = "bcd_" + kind.replace("-", "_")
+    for b, t in enumerate(trs):
+        assert max_rel(t.final, ext[key + "_final"][b]) <= 1e-9
+        np.testing.assert_allclose(t.objective, ext[key + "_objective"][b], rtol=1e-10)
+        np.testing.assert_allclose(t.update_norm, ext[key + "_update_norm"][b], rtol=1e-8)
+        assert len(t.iterates) == 6
+    one = baselines.bcd_ml(smp[2], known=True, max_iter=5) if kind == "ml-k" else None
+    if one is not None:
+        np.testing.assert_allclose(one.final, trs[2].final, rtol=1e-13, atol=1e-15)
 
 
 def _pg_samples(ext):
@@ -134,10 +147,11 @@ def test_pg_baseline_matches_reference(cuda_device, ext, known, mode):
     np.testing.assert_allclose(one.final, trs[1].final, rtol=1e-12, atol=1e-15)
 
 
-def test_pg_grid_matches_reference(cuda_device, ext):
+def test_baseline_grid_matches_reference(cuda_device, ext):
+    """PG and BCD rows of run_grid (bench.py:244-281) against the reference."""
     from paper_2503_15259_b200 import harness as h, sysmodel as sm
     grid = h.ExperimentGrid(
-        methods=["pg-ml-k", "pg-ml-ud"], sweep_name="L", sweep_values=[8],
+        methods=["pg-ml-k", "pg-ml-ud", "bcd-ml-k", "bcd-map-k", "bcd-ml-ud"], sweep_name="L", sweep_values=[8],
         base=sm.SystemConfig(n_devices=64, pilot_len=8, n_antennas=16, tx_power_dbm=5.0,
                              activity=sm.ActivityModel.iid(0.15)),
         n_val=6, n_test=8, seeds=[0])
