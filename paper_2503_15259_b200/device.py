@@ -219,7 +219,7 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
     if out is None:
         out = {}
     x = out.get("x")
-    if x is None:
+    if x is None or tuple(x.shape) != (B, N) or x.device != dev:
         x = torch.empty((B, N), dtype=torch.float64, device=dev)
     un = torch.empty((B, max(T, 1)), dtype=torch.float64, device=dev)
     obj = torch.empty((B, max(T, 1)), dtype=torch.float64, device=dev) if record_objective else None
@@ -334,6 +334,18 @@ def eval_objective_t(X, P, E):
                                    _ptr(ws), ctypes.c_size_t(ws.numel()), _stream(torch)),
            "psca_eval_objective")
     return out, status
+
+
+_SM_COUNT = {}
+
+
+def sm_count() -> int:
+    """Multiprocessors of the current CUDA device."""
+    torch = _torch()
+    d = torch.cuda.current_device()
+    if d not in _SM_COUNT:
+        _SM_COUNT[d] = torch.cuda.get_device_properties(d).multi_processor_count
+    return _SM_COUNT[d]
 
 
 def _cdev(torch):

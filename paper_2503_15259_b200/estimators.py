@@ -295,16 +295,30 @@ def psca_run_batch(problem, pilots, emp_cov, noise, n_antennas: int, gains=None,
 _COPY_STREAMS = {}
 
 
+def _host_chunk_bounds(B: int, chunks: int) -> list:
+    if chunks <= 0:
+        wave = 2 * device.sm_count()           # column CTAs resident at once
+        if B >= 8 * wave:
+            return [0, wave, 7 * wave, B]
+        chunks = 4 if B >= 4 * wave else (2 if B >= 2 * wave else 1)
+    chunks = max(1, min(chunks, B))
+    return [(B * c) // chunks for c in range(chunks + 1)]
+
+
 def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=None,
                         schedule: StepSchedule | None = None, max_iter: int = 30,
-                        tol: float = 0.0, chunks: int = 4) -> dict:
+                        tol: float = 0.0, chunks: int = 0) -> dict:
     """B independent PSCA runs from HOST arrays, with H2D / compute / D2H overlap.
 
     pilots (B,L,N) complex128, emp_cov (B,L,L), noise (B,), gains (B,N): numpy
     arrays or CPU tensors (pinned memory for full copy/compute overlap).  The
-    batch is cut into ``chunks`` sub-batches; the host-to-device copy of chunk
-    c+1 runs on a copy stream while chunk c is solved on the current stream,
-    and each chunk's estimates are copied back as soon as it is solved.
+    batch is cut into sub-batches; the host-to-device copy of chunk c+1 runs
+    on a copy stream while chunk c is solved on the current stream, and each
+    chunk's estimates are copied back as soon as it is solved.  ``chunks`` = 0
+    picks growing chunks: one wave of column CTAs first (its upload is the only
+    copy not hidden), then six waves (uploaded while the first solves; the
+    upload runs ~6x faster than the solve consumes instances at L = 40), then
+    the rest; ``chunks`` > 0 cuts equal chunks.
     Returns host tensors x (B,N), status (B,), n_iter (B,).
     """
     import torch
@@ -315,10 +329,18 @@ def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=
     S, E, nz = as_t(pilots), as_t(emp_cov), as_t(np.asarray(noise, dtype=float))
     G = as_t(gains) if (gains is not None and problem.known_pathloss) else None
     B, L, N = S.shape
-    chunks = max(1, min(chunks, B))
-    bounds = [(B * c) // chunks for c in range(chunks + 1)]
-    comp = torch.cuda.current_stream()
+    bounds = _host_chunk_bounds(B, chunks)
+    chunks = len(bounds) - 1
+    user = torch.cuda.current_stream()
     copy = _COPY_STREAMS.setdefault(dev.index, torch.cuda.Stream(device=dev))
+    # consecutive chunks solve on alternating streams, so the next chunk's
+    # launches fill the SMs while the previous chunk drains its last wave
+    alt = _COPY_STREAMS.setdefault(("alt", dev.index), torch.cuda.Stream(device=dev))
+    start = torch.cuda.Event()
+    start.record(user)
+    alt.wait_event(start)
+    copy.wait_event(start)
+    comps = [user, alt]
     pin = S.is_pinned()
     x_h = torch.empty((B, N), dtype=torch.float64, pin_memory=pin)
     st_h = torch.empty(B, dtype=torch.int32, pin_memory=pin)
@@ -329,6 +351,7 @@ def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=
     for c in range(chunks):
         lo, hi = bounds[c], bounds[c + 1]
         k = c % 2
+        comp = comps[k]
         with torch.cuda.stream(copy):
             if c >= 2:
                 copy.wait_event(free[k])           # chunk c-2 finished with this buffer
@@ -341,14 +364,21 @@ def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=
         for t in (Sd, Ed, nd, gd):
             if t is not None:
                 t.record_stream(comp)
-        res = psca_run_batch(problem, Sd, Ed, nd, n_antennas, gains=gd, schedule=schedule,
-                             max_iter=max_iter, tol=tol, out=outs[k])
-        outs[k] = {"x": res["x"], "_ws": res.get("_ws")}
-        x_h[lo:hi].copy_(res["x"], non_blocking=True)
-        st_h[lo:hi].copy_(res["status"], non_blocking=True)
-        ni_h[lo:hi].copy_(res["n_iter"], non_blocking=True)
+        # one column chunk per instance once a chunk fills a wave, so results do
+        # not depend on how the batch was cut
+        nck = 1 if hi - lo >= 2 * device.sm_count() else 0
+        with torch.cuda.stream(comp):
+            res = psca_run_batch(problem, Sd, Ed, nd, n_antennas, gains=gd, schedule=schedule,
+                                 max_iter=max_iter, tol=tol, n_chunks=nck, out=outs[k])
+            outs[k] = {"x": res["x"], "_ws": res.get("_ws")}
+            x_h[lo:hi].copy_(res["x"], non_blocking=True)
+            st_h[lo:hi].copy_(res["status"], non_blocking=True)
+            ni_h[lo:hi].copy_(res["n_iter"], non_blocking=True)
         free[k].record(comp)
-    comp.synchronize()
+    done = torch.cuda.Event()
+    done.record(alt)
+    user.wait_event(done)
+    user.synchronize()
     return {"x": x_h, "status": st_h, "n_iter": ni_h}
 
 

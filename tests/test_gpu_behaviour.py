@@ -204,3 +204,34 @@ def test_empty_batch(cuda_device):
     out = psca_run_batch(Problem.ml_ud(), np.zeros((0, 4, 10), complex), np.zeros((0, 4, 4), complex),
                          np.zeros(0), 8, max_iter=5)
     assert tuple(out["x"].shape) == (0, 10)
+
+
+@pytest.mark.parametrize("B,chunks", [(2400, 0), (700, 0), (5, 0), (9, 3)])
+def test_host_batch_api_matches_device_batch(cuda_device, B, chunks):
+    """psca_run_batch_host (pinned host in / out, chunked uploads overlapped with
+    the solves on alternating streams) returns the device batch's estimates."""
+    import torch
+    from paper_2503_15259_b200 import Problem, psca_run_batch, psca_run_batch_host
+    cfg = unit_cfg(40, 6, 16)
+    from paper_2503_15259_b200 import sysmodel as sm
+    base = sm.draw_dataset(cfg, 7, [77])
+    idx = np.arange(B) % 7
+    pil = np.stack([base[i]["pilots"] for i in idx])
+    gains = np.stack([base[i]["gains"] for i in idx])
+    rec = np.stack([base[i]["received"] for i in idx])
+    emp = np.einsum("blm,bkm->blk", rec, rec.conj()) / 16
+    noise = np.ones(B)
+    host = psca_run_batch_host(Problem.ml_k(), torch.from_numpy(pil).pin_memory(),
+                               torch.from_numpy(emp).pin_memory(), noise, 16,
+                               gains=torch.from_numpy(gains).pin_memory(), max_iter=10,
+                               chunks=chunks)
+    dev = psca_run_batch(Problem.ml_k(), pil, emp, noise, 16, gains=gains, max_iter=10,
+                         n_chunks=1)
+    xd = dev["x"].cpu().numpy()
+    xh = host["x"].numpy()
+    assert xh.shape == (B, 40) and np.all(host["status"].numpy() == 0)
+    assert np.all(host["n_iter"].numpy() == 10)
+    if B >= 2 * torch.cuda.get_device_properties(0).multi_processor_count:
+        np.testing.assert_array_equal(xh, xd)
+    else:
+        assert np.max(np.abs(xh - xd)) <= 1e-12 * np.max(np.abs(xd))
