@@ -426,6 +426,9 @@ def ours_arm(args):
                 "executed_note": "DMMA flops of the quadratic forms alone (a lower bound on "
                                  "what the kernel executes) over the same launch time; ncu "
                                  "measures the DMMA sub-pipe ~73 % busy (profiles/README.md)",
+                "overlap_note": "on the split-stream path the column launches of one half "
+                                "batch run concurrently with the other half's factor launches, "
+                                "so each CUDA-event launch duration includes that SM sharing",
                 "column_ms_per_launch": col_ms,
                 "factor_ms_per_launch": prof["factor_ms"] / max(prof["factor_launches"], 1),
                 "column_share": prof["column_ms"] / max(prof["column_ms"] + prof["factor_ms"], 1e-9),
