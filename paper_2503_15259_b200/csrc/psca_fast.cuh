@@ -495,6 +495,9 @@ struct TF {
 constexpr int NT_FAC = 128;
 // L >= 64: the register-tiled products need more threads (128 spill at L = 80)
 // and the CTA is alone on its SM anyway (SMEM), so use all of NT.
+#ifndef PSCA_FAC_PREFETCH
+#define PSCA_FAC_PREFETCH 1
+#endif
 #ifndef PSCA_FAC_WIDE
 #define PSCA_FAC_WIDE 256
 #endif
@@ -845,6 +848,17 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
     const int LP = geo.LP;
     const int ld = LP + 1;
     if (a.status[b] != PSCA_RUNNING) return;
+#if PSCA_FAC_PREFETCH
+    {
+        // Sigma_hat is read in the G product, after the assembly and the pivot
+        // sweep: ask L2 for its lines now (the column kernel's pilot stream
+        // evicts it between iterations, so it comes from DRAM)
+        const char* e = reinterpret_cast<const char*>(a.emp_cov + (size_t)b * a.L * a.L);
+        const int lines = (a.L * a.L * 16 + 127) / 128;
+        for (int i = tid; i < lines; i += NTH)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(e + (size_t)i * 128));
+    }
+#endif
     if (a.k_new > 0) {
         if (fac_finalize(a, b, &s_flag)) return;
     }
