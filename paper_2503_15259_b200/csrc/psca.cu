@@ -1073,6 +1073,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
 }
 
 #include "psca_fast.cuh"
+#include "psca_wcol.cuh"
 #include "psca_large.cuh"
 #include "psca_bcd.cuh"
 
@@ -1199,6 +1200,31 @@ cudaError_t launch_column_t(const ColArgs& ca, int n_chunks, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// The warp-streamed column kernel (psca_wcol.cuh) is the default for
+// NRB <= 10; PSCA_TILE_COLUMN=1 selects the tile-pipelined column_kernel_t
+// for A/B measurements.
+bool tile_column_forced() {
+    static const bool on = [] {
+        const char* e = getenv("PSCA_TILE_COLUMN");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+template <int NRB>
+cudaError_t launch_column_w(const ColArgs& ca, int n_chunks, cudaStream_t st) {
+    if (tile_column_forced()) return launch_column_t<NRB>(ca, n_chunks, st);
+    auto kfn = column_kernel_w<NRB>;
+    const size_t sm = TWC<NRB>::smem(ca.chunk_cols);
+    cudaError_t err =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (err != cudaSuccess) return err;
+    ProfScope prof(st, 0);
+    kfn<<<dim3(n_chunks, ca.B), NT, sm, st>>>(ca);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStream_t st);
 
 template <int MODE>
@@ -1231,13 +1257,13 @@ cudaError_t launch_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStr
 cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, cudaStream_t st) {
     if (!generic_forced()) {
         switch (g.NRB) {
-            case 2: return launch_column_t<2>(ca, n_chunks, st);
-            case 3: return launch_column_t<3>(ca, n_chunks, st);
-            case 4: return launch_column_t<4>(ca, n_chunks, st);
-            case 5: return launch_column_t<5>(ca, n_chunks, st);
-            case 6: return launch_column_t<6>(ca, n_chunks, st);
-            case 8: return launch_column_t<8>(ca, n_chunks, st);
-            case 10: return launch_column_t<10>(ca, n_chunks, st);
+            case 2: return launch_column_w<2>(ca, n_chunks, st);
+            case 3: return launch_column_w<3>(ca, n_chunks, st);
+            case 4: return launch_column_w<4>(ca, n_chunks, st);
+            case 5: return launch_column_w<5>(ca, n_chunks, st);
+            case 6: return launch_column_w<6>(ca, n_chunks, st);
+            case 8: return launch_column_w<8>(ca, n_chunks, st);
+            case 10: return launch_column_w<10>(ca, n_chunks, st);
             case 12: return launch_column_t<12>(ca, n_chunks, st);
             case 16: return launch_column_t<16>(ca, n_chunks, st);
             case 20: return launch_column_t<20>(ca, n_chunks, st);

@@ -1,0 +1,338 @@
+// psca_wcol.cuh -- warp-streamed column kernel (sm_100a), compiled shapes NRB <= 10
+// (L <= 40).  Included by psca.cu after psca_fast.cuh (uses TG, rebuild_slots,
+// ColArgs, dmma, the fragment layout and the packed rebuild layout).
+//
+// One CTA owns one (instance, column chunk) like column_kernel_t, but the
+// column pass (estimators.py:262-276 for the chunk's devices) runs without
+// CTA barriers: every warp streams its own 8-column blocks (w, w + 8, ...)
+//
+//   B fragments   the block's pilot columns go straight from HBM into
+//                 registers (2 NRB doubles per lane, one LDG.64 per k-step:
+//                 two 128-byte lines per instruction); the next block's
+//                 fragments are loaded while this block computes
+//   quad forms    q_n = s^H P s and r_n = s^H A s on DMMA over the lower
+//                 block triangle (A = P' / A' fragments from SMEM, the
+//                 same packed layout the factor kernel writes); the whole
+//                 triangle per warp, so q and r are complete in the warp
+//   epilogue      S at the C-fragment positions comes from the B registers
+//                 by shuffles; the 8 column updates (gradient, surrogate,
+//                 clip, relaxed step) run on lanes 0..7
+//   moving list   columns with a non-zero rebuild weight are appended to the
+//                 warp's list in SMEM (column, weight)
+//
+// and only the covariance rebuild, Sigma += S diag(v) S^H over the listed
+// columns (covlinalg.py:55; incremental weights), is a CTA
+// phase at the end of the pass: the listed columns are gathered 16 at a time
+// from HBM / L2 into the packed WS / SP layout and summed on DMMA into the
+// same C fragments column_kernel_t produces, so the factor kernel is shared.
+// Reduction orders are fixed (rows in descending block order, the shuffle
+// tree, lists in warp order), so reruns are bit-identical.
+
+template <int NRB>
+struct TWC {
+    using G = TG<NRB>;
+    static constexpr int NKK = 2 * NRB;   // k-steps = B fragments per lane per block
+    static constexpr size_t FR_BYTES = (size_t)G::NB * FRAG_SLOTS * 16;
+    static constexpr size_t W_BYTES = (size_t)G::LP8 * G::WCAP * 16;
+    // dynamic SMEM: fragments, WS, SP, per-warp partials, then the lists
+    static constexpr size_t FIXED = FR_BYTES + 2 * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
+    static __host__ __device__ constexpr int list_cap(int chunk_cols) {
+        return ((chunk_cols / 8 + NWARP - 1) / NWARP) * 8;
+    }
+    static __host__ __device__ constexpr size_t smem(int chunk_cols) {
+        return FIXED + (size_t)NWARP * list_cap(chunk_cols) * 12;
+    }
+};
+
+// B fragments of one 8-column block: lane (r8, c4) holds component (c4 & 1)
+// of S[2 kk + (c4 >> 1)][col0 + r8] for k-step kk
+template <int NRB>
+__device__ __forceinline__ void wc_load_b(double (&bf)[2 * NRB], const double* __restrict__ sbd,
+                                          size_t row2, int L, bool ok, int c4) {
+#pragma unroll
+    for (int kk = 0; kk < 2 * NRB; ++kk) {
+        const int m = 2 * kk + (c4 >> 1);
+        bf[kk] = (ok && m < L) ? __ldg(sbd + (size_t)m * row2) : 0.0;
+    }
+}
+
+// Quadratic forms of one block; on return every lane holds, for the columns
+// 2 c4 and 2 c4 + 1 of the block, q (qa) and r (ra) summed over all rows.
+template <int NRB>
+__device__ __forceinline__ void wc_quad(const double (&bf)[2 * NRB], const double2* __restrict__ FRl,
+                                        double (&qa)[2], double (&ra)[2], int r8, int c4) {
+    qa[0] = qa[1] = ra[0] = ra[1] = 0.0;
+    const int src0 = 8 * c4 + (r8 & 3);
+    const bool hi = (r8 >> 2) != 0;
+#pragma unroll
+    for (int i = NRB - 1; i >= 0; --i) {
+        double tc[2] = {0.0, 0.0}, uc[2] = {0.0, 0.0};
+        const double2* f = FRl + i * (i + 1) * FRAG_SLOTS;
+#pragma unroll
+        for (int kk = 0; kk < 2 * (i + 1); ++kk) {
+            const double2 pa = f[kk * FRAG_SLOTS];
+            dmma(tc, pa.x, bf[kk]);
+            dmma(uc, pa.y, bf[kk]);
+        }
+        // S[4i + (r8 >> 1)][2 c4 + h], component r8 & 1, lives in B fragment
+        // 2i + (r8 >> 2) of lane (2 c4 + h) * 4 + (r8 & 3)
+        const double a0 = __shfl_sync(0xffffffffu, bf[2 * i], src0);
+        const double a1 = __shfl_sync(0xffffffffu, bf[2 * i + 1], src0);
+        const double b0 = __shfl_sync(0xffffffffu, bf[2 * i], src0 + 4);
+        const double b1 = __shfl_sync(0xffffffffu, bf[2 * i + 1], src0 + 4);
+        const double s0 = hi ? a1 : a0;
+        const double s1 = hi ? b1 : b0;
+        qa[0] = fma(s0, tc[0], qa[0]);
+        qa[1] = fma(s1, tc[1], qa[1]);
+        ra[0] = fma(s0, uc[0], ra[0]);
+        ra[1] = fma(s1, uc[1], ra[1]);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        qa[0] += __shfl_xor_sync(0xffffffffu, qa[0], o);
+        qa[1] += __shfl_xor_sync(0xffffffffu, qa[1], o);
+        ra[0] += __shfl_xor_sync(0xffffffffu, ra[0], o);
+        ra[1] += __shfl_xor_sync(0xffffffffu, ra[1], o);
+    }
+}
+
+// rebuild over packed slots [0, cnt) of WS / SP into this warp's C blocks
+// (same operand layout as col_pass's rebuild)
+template <int NRB>
+__device__ __forceinline__ void wc_rebuild(const double2* WS, const double2* SP, int cnt,
+                                           double (&acc)[TG<NRB>::MAXBW][2],
+                                           const int (&slot)[TG<NRB>::MAXBW], int nbw, int lane) {
+    using G = TG<NRB>;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const int p = r8 & 1, q = c4 & 1, cpr = c4 >> 1;
+    const int sa = r8 >> 1, sbb = r8 & 3;
+    int wa_lane[4], b_lane[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        wa_lane[h] = 4 * (h ^ sa) + 2 * cpr + (p ^ q);
+        b_lane[h] = 4 * (h ^ sbb) + 2 * cpr + q;
+    }
+    const unsigned long long wsgn = (p & q) ? 0x8000000000000000ull : 0ull;
+    const double* Wd = reinterpret_cast<const double*>(WS);
+    const double* Pd = reinterpret_cast<const double*>(SP);
+    const int nk2 = (cnt + 1) >> 1;
+#pragma unroll
+    for (int t2 = 0; t2 < G::MAXBW; ++t2) {
+        if (t2 < nbw) {
+            const int bi = slot[t2] >> 8, bj = slot[t2] & 0xff;
+            const int abase = 2 * (4 * bi + (r8 >> 1)) * G::WCAP;
+            const int bbase = 2 * (8 * bj + r8) * G::WCAP;
+            double e1[2] = {0.0, 0.0};
+#pragma unroll
+            for (int k2 = 0; k2 < G::WCAP / 2; ++k2) {
+                if (k2 < nk2) {
+                    const int h = k2 & 3, g8 = 16 * (k2 >> 2);
+                    const double av = xsign(Wd[abase + wa_lane[h] + g8], wsgn);
+                    const double bv = Pd[bbase + b_lane[h] + g8];
+                    if (k2 & 1) dmma(e1, av, bv);
+                    else dmma(acc[t2], av, bv);
+                }
+            }
+            acc[t2][0] += e1[0];
+            acc[t2][1] += e1[1];
+        }
+    }
+}
+
+template <int NRB>
+__global__ void __launch_bounds__(NT, 2) column_kernel_w(ColArgs a) {
+    using G = TG<NRB>;
+    using W = TWC<NRB>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b = blockIdx.y;
+    const int chunk = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const size_t bN = (size_t)b * a.N;
+    const int n_begin = chunk * a.chunk_cols;
+    const int n_end = min(a.N, n_begin + a.chunk_cols);
+
+    if (a.status[b] != PSCA_RUNNING) {
+        for (int n = n_begin + tid; n < n_end; n += NT) a.x_next[bN + n] = a.x_cur[bN + n];
+        return;
+    }
+    double2* FR = reinterpret_cast<double2*>(smem_raw);
+    double2* WS = FR + G::NB * FRAG_SLOTS;
+    double2* SP = WS + G::LP8 * G::WCAP;
+    double* wpart = reinterpret_cast<double*>(SP + G::LP8 * G::WCAP);   // [NWARP][2]
+    int* s_cnt = reinterpret_cast<int*>(wpart + 2 * NWARP);               // [NWARP + 1] prefix
+    const int cap = W::list_cap(a.chunk_cols);
+    double* lv = wpart + 2 * NWARP + 16;                                  // [NWARP][cap]
+    int* lcol = reinterpret_cast<int*>(lv + (size_t)NWARP * cap);          // [NWARP][cap]
+
+    {   // stage the instance's P'/A' fragments (one cp.async group)
+        const double2* src = a.frags + (size_t)b * G::NB * FRAG_SLOTS;
+        for (int e = tid; e < G::NB * FRAG_SLOTS; e += NT) cp_async16(FR + e, src + e, 16);
+        cp_async_commit();
+    }
+
+    const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
+    const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
+    const int k = a.k;
+    const double rho = a.steps[k];
+    const double omr = __dsub_rn(1.0, rho);
+    const double* x_cur = a.x_cur + bN;
+    double* x_next = a.x_next + bN;
+    const double2* sb = a.pilots + (size_t)b * a.L * a.N;
+    const double* sbd = reinterpret_cast<const double*>(sb);
+    const size_t row2 = (size_t)2 * a.N;   // doubles per pilot row
+    const double2* FRl = FR + frag_lane_slot(lane);
+
+    const int nblk = (n_end - n_begin + 7) >> 3;
+    double p_dx2 = 0.0, p_minq = INFINITY;
+    int cnt = 0;
+    double* my_v = lv + (size_t)warp * cap;
+    int* my_c = lcol + (size_t)warp * cap;
+
+    double bA[2 * NRB], bB[2 * NRB];
+    auto load_block = [&](double (&bf)[2 * NRB], int jb) {
+        const int n = n_begin + 8 * jb + r8;
+        wc_load_b<NRB>(bf, sbd + 2 * (size_t)n + (c4 & 1), row2, a.L, n < n_end, c4);
+    };
+    // one block: quad forms, update of its 8 columns (lane j -> column j), list
+    auto do_block = [&](const double (&bf)[2 * NRB], int jb) {
+        const int ncol = n_begin + 8 * jb + lane;
+        const bool cvalid = lane < 8 && ncol < n_end;
+        double x = 0.0, g = 1.0, pg = 0.0;
+        if (cvalid) {
+            x = x_cur[ncol];
+            if (known) g = a.gains[bN + ncol];
+            if (a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.pairwise))
+                pg = a.pgrad[bN + ncol];
+            else if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
+        }
+        double qa[2], ra[2];
+        wc_quad<NRB>(bf, FRl, qa, ra, r8, c4);
+        // lane j (< 8) takes column j = 2 c4' + h from lane c4' = j >> 1
+        const int srcl = (lane >> 1) & 3;
+        const double q0 = __shfl_sync(0xffffffffu, qa[0], srcl);
+        const double q1 = __shfl_sync(0xffffffffu, qa[1], srcl);
+        const double r0 = __shfl_sync(0xffffffffu, ra[0], srcl);
+        const double r1 = __shfl_sync(0xffffffffu, ra[1], srcl);
+        double v = 0.0;
+        if (cvalid) {
+            const double q = (lane & 1) ? q1 : q0;
+            const double r = (lane & 1) ? r1 : r0;
+            const double diff = __dsub_rn(q, r);
+            double grad;
+            if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
+            else if (a.kind == PSCA_MAP_K) grad = __dadd_rn(__dmul_rn(g, diff), pg);
+            else if (a.kind == PSCA_ML_UD) grad = diff;
+            else grad = __dadd_rn(diff, pg);
+            const double gq = known ? __dmul_rn(g, q) : q;
+            const double coef = __dmul_rn(gq, gq);
+            const double cand = np_clip(__dsub_rn(x, __ddiv_rn(grad, coef)), 0.0, hi);
+            const double rc = __dmul_rn(rho, cand);
+            const double xn = __dadd_rn(__dmul_rn(omr, x), rc);
+            if (a.incremental) v = known ? __dmul_rn(rc, g) : rc;
+            else v = known ? __dmul_rn(xn, g) : xn;
+            x_next[ncol] = xn;
+            if (a.iterates) a.iterates[((size_t)b * (a.T + 1) + k + 1) * a.N + ncol] = xn;
+            const double dx = __dsub_rn(xn, x);
+            p_dx2 = fma(dx, dx, p_dx2);
+            p_minq = (q < p_minq) ? q : p_minq;
+        }
+        const unsigned mv = __ballot_sync(0xffffffffu, v != 0.0);
+        if (v != 0.0) {
+            const int pos = cnt + __popc(mv & ((1u << lane) - 1u));
+            my_v[pos] = v;
+            my_c[pos] = ncol;
+        }
+        cnt += __popc(mv);
+    };
+
+    int jb = warp;
+    if (jb < nblk) load_block(bA, jb);
+    cp_async_wait<0>();
+    __syncthreads();   // fragments staged
+    while (jb < nblk) {
+        if (jb + NWARP < nblk) load_block(bB, jb + NWARP);
+        do_block(bA, jb);
+        jb += NWARP;
+        if (jb >= nblk) break;
+        if (jb + NWARP < nblk) load_block(bA, jb + NWARP);
+        do_block(bB, jb);
+        jb += NWARP;
+    }
+
+    // ---- per-warp partials of (sum dx^2, min q), list counts -----------------
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        p_dx2 += __shfl_xor_sync(0xffffffffu, p_dx2, o);
+        const double mq = __shfl_xor_sync(0xffffffffu, p_minq, o);
+        p_minq = (mq < p_minq) ? mq : p_minq;
+    }
+    if (lane == 0) {
+        wpart[2 * warp] = p_dx2;
+        wpart[2 * warp + 1] = p_minq;
+        s_cnt[warp + 1] = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        s_cnt[0] = 0;
+        double dx2 = 0.0, minq = INFINITY;
+        for (int w = 0; w < NWARP; ++w) {
+            s_cnt[w + 1] += s_cnt[w];
+            dx2 += wpart[2 * w];
+            minq = (wpart[2 * w + 1] < minq) ? wpart[2 * w + 1] : minq;
+        }
+        double* rp = a.red_part + ((size_t)b * a.n_chunks + chunk) * 4;
+        rp[0] = dx2;
+        rp[1] = minq;
+        rp[2] = 0.0;
+        rp[3] = 0.0;
+    }
+    __syncthreads();
+
+    // ---- rebuild over the moving columns, 16 per round -----------------------
+    int slot[G::MAXBW];
+    int nbw;
+    rebuild_slots<NRB>(slot, nbw);
+    double acc[G::MAXBW][2];
+#pragma unroll
+    for (int t = 0; t < G::MAXBW; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const int total = s_cnt[NWARP];
+    for (int base = 0; base < total; base += G::WCAP) {
+        const int rc = min(total - base, G::WCAP);
+        for (int e = tid; e < G::LP8 * G::WCAP; e += NT) {
+            const int l = e / G::WCAP, s = e - l * G::WCAP;
+            double2 sv = make_double2(0.0, 0.0), wv = make_double2(0.0, 0.0);
+            if (s < rc && l < a.L) {
+                const int gi = base + s;
+                int w = 0;
+                while (gi >= s_cnt[w + 1]) ++w;
+                const int li = gi - s_cnt[w];
+                const double v = lv[(size_t)w * cap + li];
+                const int col = lcol[(size_t)w * cap + li];
+                sv = __ldg(sb + (size_t)l * a.N + col);
+                wv = make_double2(v * sv.x, v * sv.y);
+            }
+            const int o = l * G::WCAP + (s ^ (2 * (l & 3)));
+            WS[o] = wv;
+            SP[o] = sv;
+        }
+        __syncthreads();
+        wc_rebuild<NRB>(WS, SP, rc, acc, slot, nbw, lane);
+        __syncthreads();
+    }
+    {
+        double2* sp = a.sig_part + ((size_t)b * a.n_chunks + chunk) * G::NBLK * 32;
+        int idx = 0, t2 = 0;
+        for (int i = 0; i < NRB; ++i) {
+            const int jmax = (4 * i + 3) / 8;
+            for (int j = 0; j <= jmax; ++j, ++idx) {
+                if ((idx % NWARP) == warp) {
+#pragma unroll
+                    for (int u = 0; u < G::MAXBW; ++u)
+                        if (u == t2) sp[(size_t)idx * 32 + lane] = make_double2(acc[u][0], acc[u][1]);
+                    ++t2;
+                }
+            }
+        }
+    }
+}

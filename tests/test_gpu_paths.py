@@ -57,11 +57,24 @@ def test_generic_and_compiled_kernels_agree(cuda_device):
         assert max_rel(np.array(fast[key]["obj"]), np.array(slow[key]["obj"])) <= 1e-10, key
 
 
+def test_warp_streamed_and_tile_column_kernels_agree(cuda_device):
+    """The warp-streamed column kernel (default, L <= 40) and the tile-pipelined one
+    compute the same pass with different summation orders: rounding-level agreement."""
+    warp = run_script({"PSCA_TILE_COLUMN": "0"})
+    tile = run_script({"PSCA_TILE_COLUMN": "1"})
+    for key in warp:
+        xw, xt = np.array(warp[key]["x"]), np.array(tile[key]["x"])
+        tol = 1e-10 if "map-ur" not in key else 1e-7
+        assert max_rel(xw, xt) <= tol, key
+        assert max_rel(np.array(warp[key]["obj"]), np.array(tile[key]["obj"])) <= 1e-11, key
+
+
 def test_persistent_equals_two_kernel_bitwise(cuda_device):
-    """One chunk per instance: the persistent kernel and the two-kernel path run the
-    same device functions, so the iterates are bit-identical."""
-    pers = run_script({"PSCA_PERSISTENT": "1"})
-    two = run_script({"PSCA_PERSISTENT": "0"})
+    """One chunk per instance: the persistent kernel and the two-kernel path with the
+    tile-pipelined column kernel run the same device functions, so the iterates are
+    bit-identical."""
+    pers = run_script({"PSCA_PERSISTENT": "1", "PSCA_TILE_COLUMN": "1"})
+    two = run_script({"PSCA_PERSISTENT": "0", "PSCA_TILE_COLUMN": "1"})
     assert any(v["path"] == "persistent" for v in pers.values())
     assert all(v["path"] == "two-kernel" for v in two.values())
     for key in pers:
