@@ -28,14 +28,19 @@
 // Reduction orders are fixed (rows in descending block order, the shuffle
 // tree, lists in warp order), so reruns are bit-identical.
 
+#ifndef PSCA_WCOL_MINB
+#define PSCA_WCOL_MINB 2
+#endif
+
 template <int NRB>
 struct TWC {
     using G = TG<NRB>;
     static constexpr int NKK = 2 * NRB;   // k-steps = B fragments per lane per block
     static constexpr size_t FR_BYTES = (size_t)G::NB * FRAG_SLOTS * 16;
     static constexpr size_t W_BYTES = (size_t)G::LP8 * G::WCAP * 16;
-    // dynamic SMEM: fragments, WS, SP, per-warp partials, then the lists
-    static constexpr size_t FIXED = FR_BYTES + 2 * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
+    static constexpr int GPT = (G::LP8 * G::WCAP + NT - 1) / NT;   // gather elements per thread
+    // dynamic SMEM: fragments, 2 x (WS, SP), per-warp partials, then the lists
+    static constexpr size_t FIXED = FR_BYTES + 4 * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
     static __host__ __device__ constexpr int list_cap(int chunk_cols) {
         return ((chunk_cols / 8 + NWARP - 1) / NWARP) * 8;
     }
@@ -58,9 +63,14 @@ __device__ __forceinline__ void wc_load_b(double (&bf)[2 * NRB], const double* _
 
 // Quadratic forms of one block; on return every lane holds, for the columns
 // 2 c4 and 2 c4 + 1 of the block, q (qa) and r (ra) summed over all rows.
-template <int NRB>
-__device__ __forceinline__ void wc_quad(const double (&bf)[2 * NRB], const double2* __restrict__ FRl,
-                                        double (&qa)[2], double (&ra)[2], int r8, int c4) {
+// Rows run in descending order, so after row i only k-steps < 2i are still
+// needed: its two B fragments are then reloaded with the next block's
+// (nsrc != nullptr), which keeps one fragment set per lane in registers.
+template <int NRB, class Mid>
+__device__ __forceinline__ void wc_quad(double (&bf)[2 * NRB], const double2* __restrict__ FRl,
+                                        double (&qa)[2], double (&ra)[2], int r8, int c4,
+                                        const double* __restrict__ nsrc, size_t row2, int L,
+                                        bool nok, Mid&& mid) {
     qa[0] = qa[1] = ra[0] = ra[1] = 0.0;
     const int src0 = 8 * c4 + (r8 & 3);
     const bool hi = (r8 >> 2) != 0;
@@ -74,12 +84,21 @@ __device__ __forceinline__ void wc_quad(const double (&bf)[2 * NRB], const doubl
             dmma(tc, pa.x, bf[kk]);
             dmma(uc, pa.y, bf[kk]);
         }
+        // the previous block's column updates run under the longest chain
+        if (i == NRB - 1) mid();
         // S[4i + (r8 >> 1)][2 c4 + h], component r8 & 1, lives in B fragment
         // 2i + (r8 >> 2) of lane (2 c4 + h) * 4 + (r8 & 3)
         const double a0 = __shfl_sync(0xffffffffu, bf[2 * i], src0);
         const double a1 = __shfl_sync(0xffffffffu, bf[2 * i + 1], src0);
         const double b0 = __shfl_sync(0xffffffffu, bf[2 * i], src0 + 4);
         const double b1 = __shfl_sync(0xffffffffu, bf[2 * i + 1], src0 + 4);
+        if (nsrc) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int m = 2 * (2 * i + u) + (c4 >> 1);
+                bf[2 * i + u] = (nok && m < L) ? __ldg(nsrc + (size_t)m * row2) : 0.0;
+            }
+        }
         const double s0 = hi ? a1 : a0;
         const double s1 = hi ? b1 : b0;
         qa[0] = fma(s0, tc[0], qa[0]);
@@ -140,7 +159,7 @@ __device__ __forceinline__ void wc_rebuild(const double2* WS, const double2* SP,
 }
 
 template <int NRB>
-__global__ void __launch_bounds__(NT, 2) column_kernel_w(ColArgs a) {
+__global__ void __launch_bounds__(NT, PSCA_WCOL_MINB) column_kernel_w(ColArgs a) {
     using G = TG<NRB>;
     using W = TWC<NRB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -158,8 +177,8 @@ __global__ void __launch_bounds__(NT, 2) column_kernel_w(ColArgs a) {
     }
     double2* FR = reinterpret_cast<double2*>(smem_raw);
     double2* WS = FR + G::NB * FRAG_SLOTS;
-    double2* SP = WS + G::LP8 * G::WCAP;
-    double* wpart = reinterpret_cast<double*>(SP + G::LP8 * G::WCAP);   // [NWARP][2]
+    // WS / SP double buffer: [WS0 SP0 WS1 SP1], LP8 x WCAP slots each
+    double* wpart = reinterpret_cast<double*>(WS + 4 * G::LP8 * G::WCAP);   // [NWARP][2]
     int* s_cnt = reinterpret_cast<int*>(wpart + 2 * NWARP);               // [NWARP + 1] prefix
     const int cap = W::list_cap(a.chunk_cols);
     double* lv = wpart + 2 * NWARP + 16;                                  // [NWARP][cap]
@@ -189,35 +208,21 @@ __global__ void __launch_bounds__(NT, 2) column_kernel_w(ColArgs a) {
     double* my_v = lv + (size_t)warp * cap;
     int* my_c = lcol + (size_t)warp * cap;
 
-    double bA[2 * NRB], bB[2 * NRB];
-    auto load_block = [&](double (&bf)[2 * NRB], int jb) {
+    double bf[2 * NRB];
+    auto bsrc = [&](int jb) {
         const int n = n_begin + 8 * jb + r8;
-        wc_load_b<NRB>(bf, sbd + 2 * (size_t)n + (c4 & 1), row2, a.L, n < n_end, c4);
+        return sbd + 2 * (size_t)n + (c4 & 1);
     };
-    // one block: quad forms, update of its 8 columns (lane j -> column j), list
-    auto do_block = [&](const double (&bf)[2 * NRB], int jb) {
-        const int ncol = n_begin + 8 * jb + lane;
-        const bool cvalid = lane < 8 && ncol < n_end;
-        double x = 0.0, g = 1.0, pg = 0.0;
-        if (cvalid) {
-            x = x_cur[ncol];
-            if (known) g = a.gains[bN + ncol];
-            if (a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.pairwise))
-                pg = a.pgrad[bN + ncol];
-            else if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
-        }
-        double qa[2], ra[2];
-        wc_quad<NRB>(bf, FRl, qa, ra, r8, c4);
-        // lane j (< 8) takes column j = 2 c4' + h from lane c4' = j >> 1
-        const int srcl = (lane >> 1) & 3;
-        const double q0 = __shfl_sync(0xffffffffu, qa[0], srcl);
-        const double q1 = __shfl_sync(0xffffffffu, qa[1], srcl);
-        const double r0 = __shfl_sync(0xffffffffu, ra[0], srcl);
-        const double r1 = __shfl_sync(0xffffffffu, ra[1], srcl);
+    int jb = warp;
+    if (jb < nblk) wc_load_b<NRB>(bf, bsrc(jb), row2, a.L, n_begin + 8 * jb + r8 < n_end, c4);
+    cp_async_wait<0>();
+    __syncthreads();   // fragments staged
+    // per-device update (estimators.py:272-276) of one block's columns, lane
+    // j < 8 -> column j; appends the moving columns to the warp's list and
+    // asks L2 to keep their pilot lines for the rebuild gather
+    auto update = [&](double q, double r, double x, double g, double pg, int ncol, bool cvalid) {
         double v = 0.0;
         if (cvalid) {
-            const double q = (lane & 1) ? q1 : q0;
-            const double r = (lane & 1) ? r1 : r0;
             const double diff = __dsub_rn(q, r);
             double grad;
             if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
@@ -237,28 +242,66 @@ __global__ void __launch_bounds__(NT, 2) column_kernel_w(ColArgs a) {
             p_dx2 = fma(dx, dx, p_dx2);
             p_minq = (q < p_minq) ? q : p_minq;
         }
-        const unsigned mv = __ballot_sync(0xffffffffu, v != 0.0);
+        unsigned mv = __ballot_sync(0xffffffffu, v != 0.0);
         if (v != 0.0) {
             const int pos = cnt + __popc(mv & ((1u << lane) - 1u));
             my_v[pos] = v;
             my_c[pos] = ncol;
         }
         cnt += __popc(mv);
+        const int c0 = ncol - lane;
+        while (mv) {
+            const int j = __ffs(mv) - 1;
+            mv &= mv - 1;
+            for (int m = lane; m < a.L; m += 32)
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(sb + (size_t)m * a.N + c0 + j));
+        }
     };
 
-    int jb = warp;
-    if (jb < nblk) load_block(bA, jb);
-    cp_async_wait<0>();
-    __syncthreads();   // fragments staged
-    while (jb < nblk) {
-        if (jb + NWARP < nblk) load_block(bB, jb + NWARP);
-        do_block(bA, jb);
-        jb += NWARP;
-        if (jb >= nblk) break;
-        if (jb + NWARP < nblk) load_block(bA, jb + NWARP);
-        do_block(bB, jb);
-        jb += NWARP;
+    // software pipeline: the update of block j runs inside the quad forms of
+    // block j + 8 (after its longest row's DMMAs are issued)
+    bool pend = false;
+    double pq = 0.0, pr = 0.0, px = 0.0, pgn = 1.0, ppg = 0.0;
+    int pcol = 0;
+    bool pvalid = false;
+    for (; jb < nblk; jb += NWARP) {
+        const int jn = jb + NWARP;
+        {   // L2 prefetch of the block after the next one (40 lines of 128 B)
+            const int jp = jb + 2 * NWARP;
+            if (jp < nblk) {
+                const char* base = reinterpret_cast<const char*>(sb + n_begin + 8 * jp);
+                for (int m = lane; m < a.L; m += 32)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)m * a.N * 16));
+            }
+        }
+        // the block's 8 columns: lane j < 8 -> column j
+        const int ncol = n_begin + 8 * jb + lane;
+        const bool cvalid = lane < 8 && ncol < n_end;
+        double x = 0.0, g = 1.0, pg = 0.0;
+        if (cvalid) {
+            x = x_cur[ncol];
+            if (known) g = a.gains[bN + ncol];
+            if (a.kind == PSCA_MAP_UR || (a.kind == PSCA_MAP_K && a.pairwise))
+                pg = a.pgrad[bN + ncol];
+            else if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
+        }
+        double qa[2], ra[2];
+        wc_quad<NRB>(bf, FRl, qa, ra, r8, c4, jn < nblk ? bsrc(jn) : nullptr, row2, a.L,
+                     n_begin + 8 * jn + r8 < n_end, [&] {
+                         if (pend) update(pq, pr, px, pgn, ppg, pcol, pvalid);
+                     });
+        // lane j (< 8) takes column j = 2 c4' + h from lane c4' = j >> 1
+        const int srcl = (lane >> 1) & 3;
+        const double q0 = __shfl_sync(0xffffffffu, qa[0], srcl);
+        const double q1 = __shfl_sync(0xffffffffu, qa[1], srcl);
+        const double r0 = __shfl_sync(0xffffffffu, ra[0], srcl);
+        const double r1 = __shfl_sync(0xffffffffu, ra[1], srcl);
+        pq = (lane & 1) ? q1 : q0;
+        pr = (lane & 1) ? r1 : r0;
+        px = x; pgn = g; ppg = pg; pcol = ncol; pvalid = cvalid;
+        pend = true;
     }
+    if (pend) update(pq, pr, px, pgn, ppg, pcol, pvalid);
 
     // ---- per-warp partials of (sum dx^2, min q), list counts -----------------
 #pragma unroll
@@ -297,27 +340,55 @@ __global__ void __launch_bounds__(NT, 2) column_kernel_w(ColArgs a) {
 #pragma unroll
     for (int t = 0; t < G::MAXBW; ++t) acc[t][0] = acc[t][1] = 0.0;
     const int total = s_cnt[NWARP];
-    for (int base = 0; base < total; base += G::WCAP) {
+    // gather of round r (16 listed columns x LP8 rows) into registers, then
+    // into WS / SP buffer r & 1; the next round's loads are in flight while
+    // the current round's DMMAs run
+    double2 gs[W::GPT];
+    double gv[W::GPT];
+    auto gather_load = [&](int base) {
         const int rc = min(total - base, G::WCAP);
-        for (int e = tid; e < G::LP8 * G::WCAP; e += NT) {
+#pragma unroll
+        for (int u = 0; u < W::GPT; ++u) {
+            const int e = tid + u * NT;
             const int l = e / G::WCAP, s = e - l * G::WCAP;
-            double2 sv = make_double2(0.0, 0.0), wv = make_double2(0.0, 0.0);
-            if (s < rc && l < a.L) {
+            gs[u] = make_double2(0.0, 0.0);
+            gv[u] = 0.0;
+            if (e < G::LP8 * G::WCAP && s < rc && l < a.L) {
                 const int gi = base + s;
                 int w = 0;
                 while (gi >= s_cnt[w + 1]) ++w;
                 const int li = gi - s_cnt[w];
-                const double v = lv[(size_t)w * cap + li];
-                const int col = lcol[(size_t)w * cap + li];
-                sv = __ldg(sb + (size_t)l * a.N + col);
-                wv = make_double2(v * sv.x, v * sv.y);
+                gv[u] = lv[(size_t)w * cap + li];
+                gs[u] = __ldg(sb + (size_t)l * a.N + lcol[(size_t)w * cap + li]);
             }
-            const int o = l * G::WCAP + (s ^ (2 * (l & 3)));
-            WS[o] = wv;
-            SP[o] = sv;
         }
-        __syncthreads();
-        wc_rebuild<NRB>(WS, SP, rc, acc, slot, nbw, lane);
+    };
+    auto gather_store = [&](int buf) {
+        double2* WSb = WS + (size_t)buf * 2 * G::LP8 * G::WCAP;
+        double2* SPb = WSb + G::LP8 * G::WCAP;
+#pragma unroll
+        for (int u = 0; u < W::GPT; ++u) {
+            const int e = tid + u * NT;
+            if (e < G::LP8 * G::WCAP) {
+                const int l = e / G::WCAP, s = e - l * G::WCAP;
+                const int o = l * G::WCAP + (s ^ (2 * (l & 3)));
+                WSb[o] = make_double2(gv[u] * gs[u].x, gv[u] * gs[u].y);
+                SPb[o] = gs[u];
+            }
+        }
+    };
+    const int rounds = (total + G::WCAP - 1) / G::WCAP;
+    if (rounds > 0) {
+        gather_load(0);
+        gather_store(0);
+    }
+    __syncthreads();
+    for (int r = 0; r < rounds; ++r) {
+        if (r + 1 < rounds) gather_load((r + 1) * G::WCAP);
+        const double2* WSb = WS + (size_t)(r & 1) * 2 * G::LP8 * G::WCAP;
+        wc_rebuild<NRB>(WSb, WSb + G::LP8 * G::WCAP, min(total - r * G::WCAP, G::WCAP), acc, slot,
+                        nbw, lane);
+        if (r + 1 < rounds) gather_store((r + 1) & 1);
         __syncthreads();
     }
     {
