@@ -716,6 +716,11 @@ __host__ __device__ inline size_t dmat_stride(const Geo& g, int L) {
 // same fragment layout (D_0 = 0); Sigma = D + sigma^2 I.  Full mode: the
 // partials are D itself.  Entries with a row or column in [L, LP) are left
 // undefined (the factor reads rows / columns < L only).
+// AB blocks per warp and CB chunks are loaded per batch (all loads of a batch
+// are issued before any is used: the partials and D come from HBM / L2, and a
+// load-use chain per block made this phase latency-bound).  Adds stay in
+// chunk order.
+template <int AB = 8, int CB = 1>
 __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2* X, int ld,
                                bool zero_weights) {
     const int L = a.L;
@@ -728,53 +733,71 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int r8 = lane >> 2, c4 = lane & 3;
     int i = 0, base = 0;   // row block of blk, index of its first block (monotone walk)
-    for (int blk = threadIdx.x >> 5; blk < geo.NBLK; blk += nw) {
-        while (base + (4 * i + 3) / 8 + 1 <= blk) {
-            base += (4 * i + 3) / 8 + 1;
-            ++i;
+    for (int blk0 = threadIdx.x >> 5; blk0 < geo.NBLK; blk0 += AB * nw) {
+        double2 sv[AB], dv[AB];
+#pragma unroll
+        for (int u = 0; u < AB; ++u) {
+            const int blk = blk0 + u * nw;
+            sv[u] = make_double2(0.0, 0.0);
+            dv[u] = make_double2(0.0, 0.0);
+            if (blk < geo.NBLK) {
+                const int e = blk * 32 + lane;
+                if (!zero_weights && a.n_chunks > 0) sv[u] = sp[e];
+                if (D && !zero_weights) dv[u] = D[e];
+            }
         }
-        const int j = blk - base;
-        const int e = blk * 32 + lane;
-        double2 s = make_double2(0.0, 0.0);
         if (!zero_weights) {
-            // loads in batches of 8 (memory-level parallelism), adds in chunk order
-            int c = 0;
-            for (; c + 8 <= a.n_chunks; c += 8) {
-                double2 v[8];
+            // further chunks, added in chunk order
+            for (int c = 1; c < a.n_chunks; c += CB) {
+                double2 v[AB][CB];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = sp[(size_t)(c + u) * cs + e];
+                for (int u = 0; u < AB; ++u) {
+                    const int blk = blk0 + u * nw;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    s.x += v[u].x;
-                    s.y += v[u].y;
+                    for (int cc = 0; cc < CB; ++cc)
+                        v[u][cc] = (blk < geo.NBLK && c + cc < a.n_chunks)
+                                       ? sp[(size_t)(c + cc) * cs + blk * 32 + lane]
+                                       : make_double2(0.0, 0.0);
                 }
-            }
-            for (; c < a.n_chunks; ++c) {
-                const double2 v = sp[(size_t)c * cs + e];
-                s.x += v.x;
-                s.y += v.y;
-            }
-        }
-        if (D) {
-            if (zero_weights) {
-                s = make_double2(0.0, 0.0);
-            } else {
-                const double2 d = D[e];
-                s = make_double2(fma(omr, d.x, s.x), fma(omr, d.y, s.y));
-            }
-            D[e] = s;
-        }
-        const int l = 4 * i + (r8 >> 1), p = r8 & 1;
-        if (l < L) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int m = 8 * j + 2 * c4 + h;
-                const double v = h ? s.y : s.x;
-                if (m < l) {
-                    Xd[2 * (l * ld + m) + p] = v;
-                    Xd[2 * (m * ld + l) + p] = p ? -v : v;
-                } else if (m == l) {
-                    Xd[2 * (l * ld + l) + p] = p ? 0.0 : v + s2;
+                for (int u = 0; u < AB; ++u)
+#pragma unroll
+                    for (int cc = 0; cc < CB; ++cc) {
+                        if (c + cc < a.n_chunks) {
+                            sv[u].x += v[u][cc].x;
+                            sv[u].y += v[u][cc].y;
+                        }
+                    }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < AB; ++u) {
+            const int blk = blk0 + u * nw;
+            if (blk >= geo.NBLK) break;
+            while (base + (4 * i + 3) / 8 + 1 <= blk) {
+                base += (4 * i + 3) / 8 + 1;
+                ++i;
+            }
+            const int j = blk - base;
+            const int e = blk * 32 + lane;
+            double2 s = sv[u];
+            if (D) {
+                s = zero_weights ? make_double2(0.0, 0.0)
+                                 : make_double2(fma(omr, dv[u].x, s.x), fma(omr, dv[u].y, s.y));
+                D[e] = s;
+            }
+            const int l = 4 * i + (r8 >> 1), p = r8 & 1;
+            if (l < L) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = 8 * j + 2 * c4 + h;
+                    const double v = h ? s.y : s.x;
+                    if (m < l) {
+                        Xd[2 * (l * ld + m) + p] = v;
+                        Xd[2 * (m * ld + l) + p] = p ? -v : v;
+                    } else if (m == l) {
+                        Xd[2 * (l * ld + l) + p] = p ? 0.0 : v + s2;
+                    }
                 }
             }
         }
@@ -1201,8 +1224,8 @@ cudaError_t launch_column_t(const ColArgs& ca, int n_chunks, cudaStream_t st) {
 }
 
 // The warp-streamed column kernel (psca_wcol.cuh) is the default for
-// NRB <= 10; PSCA_TILE_COLUMN=1 selects the tile-pipelined column_kernel_t
-// for A/B measurements.
+// NRB <= 10 with one column chunk per instance; PSCA_TILE_COLUMN=1 selects the
+// tile-pipelined column_kernel_t for A/B measurements.
 bool tile_column_forced() {
     static const bool on = [] {
         const char* e = getenv("PSCA_TILE_COLUMN");
@@ -1213,7 +1236,9 @@ bool tile_column_forced() {
 
 template <int NRB>
 cudaError_t launch_column_w(const ColArgs& ca, int n_chunks, cudaStream_t st) {
-    if (tile_column_forced()) return launch_column_t<NRB>(ca, n_chunks, st);
+    // chunked small batches (c0: one instance over many CTAs) are latency-bound:
+    // the tile kernel splits each 8-column block's rows over two warps
+    if (tile_column_forced() || n_chunks > 1) return launch_column_t<NRB>(ca, n_chunks, st);
     auto kfn = column_kernel_w<NRB>;
     const size_t sm = TWC<NRB>::smem(ca.chunk_cols);
     cudaError_t err =

@@ -31,6 +31,10 @@
 #ifndef PSCA_WCOL_MINB
 #define PSCA_WCOL_MINB 2
 #endif
+// rebuild gather buffers (2: the next round's loads overlap this round's DMMAs)
+#ifndef PSCA_WCOL_GBUF
+#define PSCA_WCOL_GBUF 2
+#endif
 
 template <int NRB>
 struct TWC {
@@ -39,8 +43,9 @@ struct TWC {
     static constexpr size_t FR_BYTES = (size_t)G::NB * FRAG_SLOTS * 16;
     static constexpr size_t W_BYTES = (size_t)G::LP8 * G::WCAP * 16;
     static constexpr int GPT = (G::LP8 * G::WCAP + NT - 1) / NT;   // gather elements per thread
-    // dynamic SMEM: fragments, 2 x (WS, SP), per-warp partials, then the lists
-    static constexpr size_t FIXED = FR_BYTES + 4 * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
+    static constexpr int NGB = PSCA_WCOL_GBUF;
+    // dynamic SMEM: fragments, NGB x (WS, SP), per-warp partials, then the lists
+    static constexpr size_t FIXED = FR_BYTES + 2 * NGB * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
     static __host__ __device__ constexpr int list_cap(int chunk_cols) {
         return ((chunk_cols / 8 + NWARP - 1) / NWARP) * 8;
     }
@@ -177,8 +182,8 @@ __global__ void __launch_bounds__(NT, PSCA_WCOL_MINB) column_kernel_w(ColArgs a)
     }
     double2* FR = reinterpret_cast<double2*>(smem_raw);
     double2* WS = FR + G::NB * FRAG_SLOTS;
-    // WS / SP double buffer: [WS0 SP0 WS1 SP1], LP8 x WCAP slots each
-    double* wpart = reinterpret_cast<double*>(WS + 4 * G::LP8 * G::WCAP);   // [NWARP][2]
+    // WS / SP gather buffers: [WS0 SP0 (WS1 SP1)], LP8 x WCAP slots each
+    double* wpart = reinterpret_cast<double*>(WS + 2 * W::NGB * G::LP8 * G::WCAP);   // [NWARP][2]
     int* s_cnt = reinterpret_cast<int*>(wpart + 2 * NWARP);               // [NWARP + 1] prefix
     const int cap = W::list_cap(a.chunk_cols);
     double* lv = wpart + 2 * NWARP + 16;                                  // [NWARP][cap]
@@ -378,6 +383,16 @@ __global__ void __launch_bounds__(NT, PSCA_WCOL_MINB) column_kernel_w(ColArgs a)
         }
     };
     const int rounds = (total + G::WCAP - 1) / G::WCAP;
+    if (W::NGB == 1) {
+        for (int r = 0; r < rounds; ++r) {
+            gather_load(r * G::WCAP);
+            gather_store(0);
+            __syncthreads();
+            wc_rebuild<NRB>(WS, WS + G::LP8 * G::WCAP, min(total - r * G::WCAP, G::WCAP), acc, slot,
+                            nbw, lane);
+            __syncthreads();
+        }
+    } else {
     if (rounds > 0) {
         gather_load(0);
         gather_store(0);
@@ -390,6 +405,7 @@ __global__ void __launch_bounds__(NT, PSCA_WCOL_MINB) column_kernel_w(ColArgs a)
                         nbw, lane);
         if (r + 1 < rounds) gather_store((r + 1) & 1);
         __syncthreads();
+    }
     }
     {
         double2* sp = a.sig_part + ((size_t)b * a.n_chunks + chunk) * G::NBLK * 32;

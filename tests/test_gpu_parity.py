@@ -185,4 +185,7 @@ def test_batch_equals_single_and_is_deterministic(cuda_device, golden_small):
         for k in range(b):
             assert max_rel(r1[k], single) <= 1e-13
             np.testing.assert_array_equal(r1[k], r1[0])
-            assert max_rel(r2[k], single) <= 1e-13
+            # one chunk per instance runs the warp-streamed column kernel, the
+            # chunked single instance the tile kernel: rounding-level agreement
+            assert max_rel(r2[k], single) <= 1e-11
+            np.testing.assert_array_equal(r2[k], r2[0])

@@ -3,7 +3,12 @@ import json, sys, time
 sys.path.insert(0, ".")
 import torch
 import __graft_entry__
-__graft_entry__.build()
+if len(sys.argv) > 1:   # A/B: time an alternative build of _psca.so
+    import pathlib
+    from paper_2503_15259_b200 import device
+    device.LIB_PATH = pathlib.Path(sys.argv[1]).resolve()
+else:
+    __graft_entry__.build()
 from paper_2503_15259_b200 import estimators, scenes
 cfg = scenes.BASELINE_CONFIGS["c0"]
 s = scenes.make_scene(cfg, 0)
@@ -26,5 +31,5 @@ ms = e0.elapsed_time(e1) / R
 t0 = time.perf_counter()
 tr = estimators.psca_run(prob, s, estimators.StepSchedule.default(), max_iter=100, tol=0.0, record_objective=False)
 wall = time.perf_counter() - t0
-print(json.dumps({"c0_device_ms_per_solve": ms, "us_per_iteration": ms * 10, "launches": out["launches"],
+print(json.dumps({"lib": sys.argv[1] if len(sys.argv) > 1 else "in-tree", "c0_device_ms_per_solve": ms, "us_per_iteration": ms * 10, "launches": out["launches"],
                   "psca_run_wall_ms": wall * 1e3}))
