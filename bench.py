@@ -425,7 +425,7 @@ def ours_arm(args):
                 "executed_quad_frac": executed / peak,
                 "executed_note": "DMMA flops of the quadratic forms alone (a lower bound on "
                                  "what the kernel executes) over the same launch time; ncu "
-                                 "measures the DMMA sub-pipe ~73 % busy (profiles/README.md)",
+                                 "measures the DMMA sub-pipe ~78 % busy in column_kernel_w<10> (profiles/README.md)",
                 "overlap_note": "on the split-stream path the column launches of one half "
                                 "batch run concurrently with the other half's factor launches, "
                                 "so each CUDA-event launch duration includes that SM sharing",

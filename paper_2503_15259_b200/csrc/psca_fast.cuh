@@ -869,7 +869,8 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
     double2* X = sm + 4 * LP;       // [LP][ld]
     double2* G = X + (size_t)LP * ld;
     const double2* Es = nullptr;   // Sigma_hat read through L1/L2 (staging it in SMEM for the wide variants measured no gain)
-    assemble_sigma<(NTH >= 512 ? 2 : 8), (NTH >= 512 ? 8 : 1)>(a, geo, b, X, ld, a.k_new == 0);
+    if (NTH >= 512) assemble_sigma_seq(a, geo, b, X, ld, a.k_new == 0);
+    else assemble_sigma<8, 1>(a, geo, b, X, ld, a.k_new == 0);
     double frob, logdet, trace;
     double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
     if (!factor_pass<NRB, NTH>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet,
