@@ -33,6 +33,9 @@
 #ifndef PSCA_UPD_ONE
 #define PSCA_UPD_ONE 1
 #endif
+#ifndef PSCA_BLOCK_SWEEP
+#define PSCA_BLOCK_SWEEP 1
+#endif
 constexpr int QCB = PSCA_QCB;                // 8-column blocks per warp in the quad stage
 constexpr int QPARTS = NWARP / (NCB / QCB);  // row-block groups (LPT-balanced)
 
@@ -565,8 +568,148 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                 const int i = 2 * bi[u] + di, j = 2 * bj[u] + dj;
                 v[u][di][dj] = (bi[u] >= 0 && i < L && j < L && i >= j) ? X[i * ld + j]
                                                                        : make_double2(0.0, 0.0);
+                // odd L: the padding pivot L is an identity row (no effect on
+                // the L x L part, log 1 = 0), so pivots pair up as 2x2 blocks
+                if ((L & 1) && i == L && j == L) v[u][di][dj] = make_double2(1.0, 0.0);
             }
     }
+#if PSCA_BLOCK_SWEEP
+    // ---- 2x2 block pivots K = {k, k+1} (k even): one barrier per two pivots.
+    // Staged per step (ping-pong): the two columns of K for every row with the
+    // K entries zeroed (cs0, cs1), and K itself (kv: a = a_kk, b = a_k+1,k,
+    // c = a_k+1,k+1).  The sweep of K: a_ij -= C_i M C_j^H (i, j not in K,
+    // M = K^-1, C_i = (a_ik, a_i,k+1)), rows / columns of K -> M-scaled,
+    // a_KK -> -M; the pivots are those of the scalar sweep (a, then
+    // c - |b|^2 / a), so PD-ness and log|Sigma| are unchanged.
+    __shared__ double kv[2][4];
+    {
+        double2* cs0 = cbuf;
+        double2* cs1 = cbuf + LP;
+        for (int e = tid; e < LP; e += NTH) {
+            cs0[e] = (e < L && e >= 2) ? X[e * ld] : make_double2(0.0, 0.0);
+            cs1[e] = (e < L && e >= 2) ? X[e * ld + 1] : make_double2(0.0, 0.0);
+        }
+        if (tid == 0) {
+            kv[0][0] = X[0].x;
+            const double2 bb = (L > 1) ? X[ld] : make_double2(0.0, 0.0);
+            kv[0][1] = bb.x;
+            kv[0][2] = bb.y;
+            kv[0][3] = (L > 1) ? X[ld + 1].x : 1.0;
+        }
+    }
+    __syncthreads();
+    logdet = 0.0;
+    bool ok = true;
+    const bool want_logdet = a.record_objective;
+    const int LE = (L + 1) & ~1;
+    for (int k = 0; k < LE; k += 2) {
+        const int ph = (k >> 1) & 1;
+        const double2* c0 = cbuf + ph * 2 * LP;
+        const double2* c1 = c0 + LP;
+        double2* n0 = cbuf + (ph ^ 1) * 2 * LP;
+        double2* n1 = n0 + LP;
+        const double ka = kv[ph][0], kbr = kv[ph][1], kbi = kv[ph][2], kc = kv[ph][3];
+        if (!(ka > 0.0)) {
+            ok = false;
+            break;
+        }
+        const double ainv = __drcp_rn(ka);
+        const double d1 = kc - (kbr * kbr + kbi * kbi) * ainv;
+        if (!(d1 > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (want_logdet) logdet += log(ka) + log(d1);
+        const double d1inv = __drcp_rn(d1);
+        // M = K^-1 = [[1/a + |b|^2/(a^2 d1), -conj(b)/(a d1)], [-b/(a d1), 1/d1]]
+        const double m00 = fma((kbr * kbr + kbi * kbi) * ainv * ainv, d1inv, ainv);
+        const double m11 = d1inv;
+        const double2 m10 = make_double2(-kbr * ainv * d1inv, -kbi * ainv * d1inv);
+        const double2 m01 = make_double2(m10.x, -m10.y);
+        const int kb = k >> 1;
+#pragma unroll
+        for (int u = 0; u < F::SL; ++u) {
+            if (bi[u] < 0) continue;
+            const int i0 = 2 * bi[u], j0 = 2 * bj[u];
+            double2 ua[2], ub[2];   // U_j = M conj(C_j) for the block's columns
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj) {
+                const double2 p = c0[j0 + dj], q = c1[j0 + dj];   // C_j = (p, q)
+                // conj(p), conj(q)
+                ua[dj] = make_double2(fma(m01.x, q.x, fma(m01.y, q.y, m00 * p.x)),
+                                      fma(m01.y, q.x, fma(-m01.x, q.y, -m00 * p.y)));
+                ub[dj] = make_double2(fma(m11, q.x, fma(m10.x, p.x, m10.y * p.y)),
+                                      fma(-m11, q.y, fma(m10.y, p.x, -m10.x * p.y)));
+            }
+#pragma unroll
+            for (int di = 0; di < 2; ++di) {
+                const double2 p = c0[i0 + di], q = c1[i0 + di];   // C_i = (p, q)
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) {
+                    const double2 o = v[u][di][dj];
+                    // a_ij - (p ua + q ub)
+                    double nx = fma(-p.x, ua[dj].x, fma(p.y, ua[dj].y, o.x));
+                    double ny = fma(-p.x, ua[dj].y, fma(-p.y, ua[dj].x, o.y));
+                    nx = fma(-q.x, ub[dj].x, fma(q.y, ub[dj].y, nx));
+                    ny = fma(-q.x, ub[dj].y, fma(-q.y, ub[dj].x, ny));
+                    v[u][di][dj] = make_double2(nx, ny);
+                }
+            }
+            if (bi[u] == kb || bj[u] == kb || bi[u] == kb + 1 || bj[u] == kb + 1) {
+                if (bi[u] == kb && bj[u] == kb) {
+                    v[u][0][0] = make_double2(-m00, 0.0);
+                    v[u][1][0] = make_double2(-m10.x, -m10.y);
+                    v[u][1][1] = make_double2(-m11, 0.0);
+                } else if (bj[u] == kb) {
+                    // rows i not in K, columns K: (a_ik, a_ik+1) <- (a_ik, a_ik+1) M
+#pragma unroll
+                    for (int di = 0; di < 2; ++di) {
+                        const double2 x0 = v[u][di][0], x1 = v[u][di][1];
+                        v[u][di][0] = make_double2(fma(x1.x, m10.x, fma(-x1.y, m10.y, x0.x * m00)),
+                                                   fma(x1.x, m10.y, fma(x1.y, m10.x, x0.y * m00)));
+                        v[u][di][1] = make_double2(fma(x0.x, m01.x, fma(-x0.y, m01.y, x1.x * m11)),
+                                                   fma(x0.x, m01.y, fma(x0.y, m01.x, x1.y * m11)));
+                    }
+                } else if (bi[u] == kb) {
+                    // rows K, columns j not in K: (a_kj, a_k+1,j) <- M (a_kj, a_k+1,j)
+#pragma unroll
+                    for (int dj = 0; dj < 2; ++dj) {
+                        const double2 x0 = v[u][0][dj], x1 = v[u][1][dj];
+                        v[u][0][dj] = make_double2(fma(m01.x, x1.x, fma(-m01.y, x1.y, m00 * x0.x)),
+                                                   fma(m01.x, x1.y, fma(m01.y, x1.x, m00 * x0.y)));
+                        v[u][1][dj] = make_double2(fma(m10.x, x0.x, fma(-m10.y, x0.y, m11 * x1.x)),
+                                                   fma(m10.x, x0.y, fma(m10.y, x0.x, m11 * x1.y)));
+                    }
+                }
+                // stage K' = {k+2, k+3}: its columns for every row, K' zeroed
+                if (bi[u] == kb + 1 && bj[u] == kb + 1) {
+                    kv[ph ^ 1][0] = v[u][0][0].x;
+                    kv[ph ^ 1][1] = v[u][1][0].x;
+                    kv[ph ^ 1][2] = v[u][1][0].y;
+                    kv[ph ^ 1][3] = v[u][1][1].x;
+#pragma unroll
+                    for (int di = 0; di < 2; ++di) {
+                        n0[i0 + di] = make_double2(0.0, 0.0);
+                        n1[i0 + di] = make_double2(0.0, 0.0);
+                    }
+                } else if (bj[u] == kb + 1) {
+#pragma unroll
+                    for (int di = 0; di < 2; ++di) {
+                        n0[i0 + di] = v[u][di][0];
+                        n1[i0 + di] = v[u][di][1];
+                    }
+                } else if (bi[u] == kb + 1) {
+#pragma unroll
+                    for (int dj = 0; dj < 2; ++dj) {
+                        n0[j0 + dj] = make_double2(v[u][0][dj].x, -v[u][0][dj].y);
+                        n1[j0 + dj] = make_double2(v[u][1][dj].x, -v[u][1][dj].y);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+#else
     for (int e = tid; e < 2 * LP; e += NTH)
         cbuf[e] = (e < L) ? X[e * ld] : make_double2(0.0, 0.0);   // padding stays zero
     __syncthreads();
@@ -624,6 +767,7 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         }
         __syncthreads();
     }
+#endif
     if (!ok) {
         __syncthreads();
         return false;
