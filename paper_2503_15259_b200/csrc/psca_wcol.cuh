@@ -189,11 +189,12 @@ __global__ void __launch_bounds__(NT, PSCA_WCOL_MINB) column_kernel_w(ColArgs a)
     double* lv = wpart + 2 * NWARP + 16;                                  // [NWARP][cap]
     int* lcol = reinterpret_cast<int*>(lv + (size_t)NWARP * cap);          // [NWARP][cap]
 
-    {   // stage the instance's P'/A' fragments (one cp.async group)
-        const double2* src = a.frags + (size_t)b * G::NB * FRAG_SLOTS;
-        for (int e = tid; e < G::NB * FRAG_SLOTS; e += NT) cp_async16(FR + e, src + e, 16);
-        cp_async_commit();
-    }
+    // the instance's P'/A' fragments: one TMA bulk copy, completion on s_bar
+    __shared__ __align__(8) unsigned long long s_bar;
+    if (tid == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
+    if (tid == 0)
+        bulk_g2s(FR, a.frags + (size_t)b * G::NB * FRAG_SLOTS, (unsigned)W::FR_BYTES, &s_bar);
 
     const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
     const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
@@ -220,8 +221,7 @@ __global__ void __launch_bounds__(NT, PSCA_WCOL_MINB) column_kernel_w(ColArgs a)
     };
     int jb = warp;
     if (jb < nblk) wc_load_b<NRB>(bf, bsrc(jb), row2, a.L, n_begin + 8 * jb + r8 < n_end, c4);
-    cp_async_wait<0>();
-    __syncthreads();   // fragments staged
+    mbar_wait(&s_bar, 0);   // fragments staged
     // per-device update (estimators.py:272-276) of one block's columns, lane
     // j < 8 -> column j; appends the moving columns to the warp's list and
     // asks L2 to keep their pilot lines for the rebuild gather
