@@ -1386,9 +1386,9 @@ cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, c
             case 6: return launch_column_w<6>(ca, n_chunks, st);
             case 8: return launch_column_w<8>(ca, n_chunks, st);
             case 10: return launch_column_w<10>(ca, n_chunks, st);
-            case 12: return launch_column_t<12>(ca, n_chunks, st);
-            case 16: return launch_column_t<16>(ca, n_chunks, st);
-            case 20: return launch_column_t<20>(ca, n_chunks, st);
+            case 12: return launch_column_w<12>(ca, n_chunks, st);
+            case 16: return launch_column_w<16>(ca, n_chunks, st);
+            case 20: return launch_column_w<20>(ca, n_chunks, st);
             default: break;
         }
     }

@@ -1,5 +1,5 @@
-// psca_wcol.cuh -- warp-streamed column kernel (sm_100a), compiled shapes NRB <= 10
-// (L <= 40).  Included by psca.cu after psca_fast.cuh (uses TG, rebuild_slots,
+// psca_wcol.cuh -- warp-streamed column kernel (sm_100a), compiled shapes NRB <= 20
+// (L <= 80).  Included by psca.cu after psca_fast.cuh (uses TG, rebuild_slots,
 // ColArgs, dmma, the fragment layout and the packed rebuild layout).
 //
 // One CTA owns one (instance, column chunk) like column_kernel_t, but the
@@ -43,7 +43,11 @@ struct TWC {
     static constexpr size_t FR_BYTES = (size_t)G::NB * FRAG_SLOTS * 16;
     static constexpr size_t W_BYTES = (size_t)G::LP8 * G::WCAP * 16;
     static constexpr int GPT = (G::LP8 * G::WCAP + NT - 1) / NT;   // gather elements per thread
-    static constexpr int NGB = PSCA_WCOL_GBUF;
+    // L > 40: the 24-slot fragments of the whole triangle fill most of SMEM
+    // (L = 80: 161 KB), so one gather buffer and one CTA (up to 255 registers)
+    // per SM
+    static constexpr int NGB = NRB <= 10 ? PSCA_WCOL_GBUF : 1;
+    static constexpr int MINB = NRB <= 10 ? PSCA_WCOL_MINB : 1;
     // dynamic SMEM: fragments, NGB x (WS, SP), per-warp partials, then the lists
     static constexpr size_t FIXED = FR_BYTES + 2 * NGB * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
     static __host__ __device__ constexpr int list_cap(int chunk_cols) {
@@ -164,7 +168,7 @@ __device__ __forceinline__ void wc_rebuild(const double2* WS, const double2* SP,
 }
 
 template <int NRB>
-__global__ void __launch_bounds__(NT, PSCA_WCOL_MINB) column_kernel_w(ColArgs a) {
+__global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a) {
     using G = TG<NRB>;
     using W = TWC<NRB>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
