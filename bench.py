@@ -215,6 +215,19 @@ def fp64_peak_tflops(torch) -> float:
     return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
+def ncu_share():
+    """Column-kernel share of the step from the committed ncu launch list (serialised,
+    cold-cache launches: total column time / total column + factor time), if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        c, f = d["column_kernel"], d["factor_kernel"]
+        tc = c["mean_duration_ns_cold"] * c["launches"]
+        return tc / (tc + f["mean_duration_ns_cold"] * f["launches"])
+    except Exception:
+        return None
+
+
 def ncu_traffic(name: str = "column_kernel"):
     """dram bytes per launch of the column kernel from the committed ncu summary, if any."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -432,6 +445,10 @@ def ours_arm(args):
                 "column_ms_per_launch": col_ms,
                 "factor_ms_per_launch": prof["factor_ms"] / max(prof["factor_launches"], 1),
                 "column_share": prof["column_ms"] / max(prof["column_ms"] + prof["factor_ms"], 1e-9),
+                "column_share_ncu": ncu_share(),
+                "share_note": "column_share is from CUDA events on the split streams (each interval "
+                              "also spans the other half's concurrent kernel); column_share_ncu is "
+                              "from the serialised ncu launch list in profiles/ncu_summary.json",
                 "column_launches": prof["column_launches"],
                 "path": out.get("path"),
             },
