@@ -498,9 +498,6 @@ struct TF {
 constexpr int NT_FAC = 128;
 // L >= 64: the register-tiled products need more threads (128 spill at L = 80)
 // and the CTA is alone on its SM anyway (SMEM), so use all of NT.
-#ifndef PSCA_FAC_PREFETCH
-#define PSCA_FAC_PREFETCH 1
-#endif
 #ifndef PSCA_FAC_WIDE
 #define PSCA_FAC_WIDE 256
 #endif
@@ -992,17 +989,6 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
     const int LP = geo.LP;
     const int ld = LP + 1;
     if (a.status[b] != PSCA_RUNNING) return;
-#if PSCA_FAC_PREFETCH
-    {
-        // Sigma_hat is read in the G product, after the assembly and the pivot
-        // sweep: ask L2 for its lines now (the column kernel's pilot stream
-        // evicts it between iterations, so it comes from DRAM)
-        const char* e = reinterpret_cast<const char*>(a.emp_cov + (size_t)b * a.L * a.L);
-        const int lines = (a.L * a.L * 16 + 127) / 128;
-        for (int i = tid; i < lines; i += NTH)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(e + (size_t)i * 128));
-    }
-#endif
     if (a.k_new > 0) {
         if (fac_finalize(a, b, &s_flag)) return;
     }
@@ -1012,7 +998,13 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
     double2* colb = sm + 2 * LP;    // (unused)
     double2* X = sm + 4 * LP;       // [LP][ld]
     double2* G = X + (size_t)LP * ld;
-    const double2* Es = nullptr;   // Sigma_hat read through L1/L2 (staging it in SMEM for the wide variants measured no gain)
+    // Sigma_hat is staged (cp.async, landing during the assembly and the sweep)
+    // into the G buffer itself: G = Sigma_hat P is computed by row tiles, and
+    // the warp that writes G's row tile ri is the only reader of Sigma_hat's
+    // rows of that tile, so the product can overwrite its operand in place
+    // (no extra SMEM, so 4 CTAs per SM still fit)
+    const double2* Es = G;
+    stage_emp(a, b, G, ld);
     if (NTH >= 512) assemble_sigma_seq(a, geo, b, X, ld, a.k_new == 0);
     else assemble_sigma<8, 1>(a, geo, b, X, ld, a.k_new == 0);
     double frob, logdet, trace;
