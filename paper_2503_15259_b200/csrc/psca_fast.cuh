@@ -889,12 +889,12 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                             const double avv = f * acc[j][h];
                             const int blk = i4 * (i4 + 1) + (m >> 1);
                             const int ent = (l & 3) * 2 + (m & 1);
-                            double* o = od + ((size_t)blk * FRAG_SLOTS + 3 * ent) * 2;
+                            double2* o = reinterpret_cast<double2*>(od) + (size_t)blk * FRAG_SLOTS + 3 * ent;
                             if (p == 0) {
-                                o[0] = pv; o[1] = avv;
+                                o[0] = make_double2(pv, avv);
                             } else {
-                                o[2] = pv; o[3] = avv;
-                                o[4] = -pv; o[5] = -avv;
+                                o[1] = make_double2(pv, avv);
+                                o[2] = make_double2(-pv, -avv);
                             }
                         }
                     }
