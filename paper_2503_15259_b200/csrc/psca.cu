@@ -1335,9 +1335,12 @@ template <int NRB>
 cudaError_t launch_column_w(const ColArgs& ca, int n_chunks, cudaStream_t st) {
     // chunked small batches (c0: one instance over many CTAs) are latency-bound:
     // the tile kernel splits each 8-column block's rows over two warps
-    if (tile_column_forced() || n_chunks > 1) return launch_column_t<NRB>(ca, n_chunks, st);
-    auto kfn = column_kernel_w<NRB>;
+    // the per-warp moving-column lists grow with the chunk width: very wide
+    // single chunks (N beyond ~10K at L = 40, ~2.4K at L = 80) use the tile kernel
     const size_t sm = TWC<NRB>::smem(ca.chunk_cols);
+    if (tile_column_forced() || n_chunks > 1 || sm + 1024 > (size_t)227 * 1024)
+        return launch_column_t<NRB>(ca, n_chunks, st);
+    auto kfn = column_kernel_w<NRB>;
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;

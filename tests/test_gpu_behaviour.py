@@ -199,6 +199,25 @@ def test_edge_shapes_match_oracle(cuda_device, n, l):
         assert max_rel(tr.final, ref["final"]) <= 1e-9, (n, l, kind)
 
 
+@pytest.mark.parametrize("n,l", [(5, 3), (7, 1), (33, 2), (77, 11), (130, 17), (2600, 72)])
+def test_one_chunk_shapes_match_oracle(cuda_device, n, l):
+    """One column chunk per instance (the warp-streamed column kernel; a chunk
+    too wide for its SMEM lists, N = 2600 at L = 72, falls back to the tile
+    kernel): ragged and minimal shapes against the oracle."""
+    from paper_2503_15259_b200 import Problem, StepSchedule, psca_run_batch
+    T = 6 if n > 1000 else 20
+    for kind in ("ml-k", "ml-ud"):
+        ss = [unit_sample([n, l, i], n, l, 16)[1] for i in range(2)]
+        prob = Problem.ml_k() if kind == "ml-k" else Problem.ml_ud()
+        out = psca_run_batch(prob, np.stack([s.pilots for s in ss]), np.stack([s.emp_cov for s in ss]),
+                             np.ones(2), 16, gains=np.stack([s.gains for s in ss]),
+                             schedule=StepSchedule.default(), max_iter=T, n_chunks=1)
+        x = out["x"].cpu().numpy()
+        for i, s in enumerate(ss):
+            ref = orc.psca(kind, s.pilots, s.gains, s.emp_cov, 1.0, 16, orc.default_steps(T), T)
+            assert max_rel(x[i], ref["final"]) <= 1e-9, (n, l, kind, i)
+
+
 def test_empty_batch(cuda_device):
     from paper_2503_15259_b200 import Problem, psca_run_batch
     out = psca_run_batch(Problem.ml_ud(), np.zeros((0, 4, 10), complex), np.zeros((0, 4, 4), complex),
