@@ -8,6 +8,8 @@ for L, kind in ((40, "ml-ud"), (20, "map-ur"), (72, "map-k"), (33, "ml-k")):
     cfg = scenes.SceneConfig(7, kind, 100, L, 64, 10, 4, 2)
     ss = [scenes.make_scene(cfg, i) for i in range(2)]
     b = scenes.stack_batch(ss)
-    res = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"], b["noise"],
-                                    64, gains=b["gains"], max_iter=4, record_objective=True)
-    print(L, kind, float(res["x"].sum()))
+    for nck in (0, 1):   # chunked (tile column kernel) and one chunk (warp-streamed)
+        res = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"], b["noise"],
+                                        64, gains=b["gains"], max_iter=4, record_objective=True,
+                                        n_chunks=nck)
+        print(L, kind, nck, float(res["x"].sum()))
