@@ -482,55 +482,143 @@ gj_cluster(LargeArgs a) {
                                                                        : make_double2(0.0, 0.0);
             }
     }
-    for (int e = threadIdx.x; e < 2 * LP; e += GJ_NT)
-        cbuf[e] = (e < L) ? a.Xg[(size_t)e * LP] : make_double2(0.0, 0.0);
+    // 2x2 block pivots K = {k, k+1} (as factor_pass): one cluster barrier per
+    // two pivots.  Per step every CTA holds (ping-pong) the two columns of K
+    // for all rows with the K entries zeroed, and kv = (M = K^-1, the two
+    // pivots); the owners of the next block's row / column broadcast them
+    // into all CTAs through DSMEM.
+    __shared__ double kv[2][6];   // m00, m10.x, m10.y, m11, a, d1
+    auto invert_k = [&](double ka, double kbr, double kbi, double kc, double* out) {
+        out[4] = ka;
+        out[5] = -1.0;
+        if (!(ka > 0.0)) return;
+        const double ainv = __drcp_rn(ka);
+        const double d1 = kc - (kbr * kbr + kbi * kbi) * ainv;
+        out[5] = d1;
+        if (!(d1 > 0.0)) return;
+        const double d1inv = __drcp_rn(d1);
+        out[0] = fma((kbr * kbr + kbi * kbi) * ainv * ainv, d1inv, ainv);
+        out[1] = -kbr * ainv * d1inv;
+        out[2] = -kbi * ainv * d1inv;
+        out[3] = d1inv;
+    };
+#pragma unroll
+    for (int u = 0; u < SLMAX; ++u)
+#pragma unroll
+        for (int di = 0; di < 2; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 2; ++dj)
+                if ((L & 1) && 2 * bi[u] + di == L && 2 * bj[u] + dj == L)
+                    v[u][di][dj] = make_double2(1.0, 0.0);   // identity padding pivot
+    for (int e = threadIdx.x; e < LP; e += GJ_NT) {
+        cbuf[e] = (e < L && e >= 2) ? a.Xg[(size_t)e * LP] : make_double2(0.0, 0.0);
+        cbuf[LP + e] = (e < L && e >= 2) ? a.Xg[(size_t)e * LP + 1] : make_double2(0.0, 0.0);
+    }
+    if (threadIdx.x == 0) {
+        const double2 bb = (L > 1) ? a.Xg[LP] : make_double2(0.0, 0.0);
+        invert_k(a.Xg[0].x, bb.x, bb.y, (L > 1) ? a.Xg[LP + 1].x : 1.0, kv[0]);
+    }
     cl.sync();
     double logdet = 0.0;
     bool ok = true;
-    for (int k = 0; k < L; ++k) {
-        const double2* cb = cbuf + (k & 1) * LP;
-        const int nxt = ((k + 1) & 1) * LP;
-        const double d = cb[k].x;   // identical copy in every CTA: a uniform decision
-        if (!(d > 0.0)) {
+    const int LE = (L + 1) & ~1;
+    for (int k = 0; k < LE; k += 2) {
+        const int ph = (k >> 1) & 1;
+        const double2* c0 = cbuf + ph * 2 * LP;
+        const double2* c1 = c0 + LP;
+        const int nx0 = (ph ^ 1) * 2 * LP, nx1 = nx0 + LP;
+        const double ka = kv[ph][4], d1 = kv[ph][5];   // identical in every CTA
+        if (!(ka > 0.0) || !(d1 > 0.0)) {
             ok = false;
             break;
         }
-        if (a.record_objective) logdet += log(d);
-        const double dinv = __drcp_rn(d);
+        if (a.record_objective) logdet += log(ka) + log(d1);
+        const double m00 = kv[ph][0], m11 = kv[ph][3];
+        const double2 m10 = make_double2(kv[ph][1], kv[ph][2]);
+        const double2 m01 = make_double2(m10.x, -m10.y);
+        const int kb = k >> 1;
+        auto bcast = [&](int idx, double2 val) {
+#pragma unroll
+            for (int r = 0; r < GJ_CL; ++r) cl.map_shared_rank(cbuf, r)[idx] = val;
+        };
 #pragma unroll
         for (int u = 0; u < SLMAX; ++u) {
             if (bi[u] < 0) continue;
             const int i0 = 2 * bi[u], j0 = 2 * bj[u];
-            const double2 ci[2] = {cb[i0], cb[i0 + 1]};
-            const double2 cj[2] = {cb[j0], cb[j0 + 1]};
+            double2 ua[2], ub[2];   // U_j = M conj(C_j)
 #pragma unroll
-            for (int di = 0; di < 2; ++di)
+            for (int dj = 0; dj < 2; ++dj) {
+                const double2 p = c0[j0 + dj], q = c1[j0 + dj];
+                ua[dj] = make_double2(fma(m01.x, q.x, fma(m01.y, q.y, m00 * p.x)),
+                                      fma(m01.y, q.x, fma(-m01.x, q.y, -m00 * p.y)));
+                ub[dj] = make_double2(fma(m11, q.x, fma(m10.x, p.x, m10.y * p.y)),
+                                      fma(-m11, q.y, fma(m10.y, p.x, -m10.x * p.y)));
+            }
+#pragma unroll
+            for (int di = 0; di < 2; ++di) {
+                const double2 p = c0[i0 + di], q = c1[i0 + di];
 #pragma unroll
                 for (int dj = 0; dj < 2; ++dj) {
-                    const int i = i0 + di, j = j0 + dj;
                     const double2 o = v[u][di][dj];
-                    const double pr = ci[di].x * cj[dj].x + ci[di].y * cj[dj].y;
-                    const double pim = ci[di].y * cj[dj].x - ci[di].x * cj[dj].y;
-                    double nx = o.x - pr * dinv, ny = o.y - pim * dinv;
-                    const bool onrow = (i == k) || (j == k);
-                    nx = onrow ? o.x * dinv : nx;
-                    ny = onrow ? o.y * dinv : ny;
-                    nx = (i == k && j == k) ? -dinv : nx;
-                    ny = (i == k && j == k) ? 0.0 : ny;
-                    if (i < j) { nx = 0.0; ny = 0.0; }
+                    double nx = fma(-p.x, ua[dj].x, fma(p.y, ua[dj].y, o.x));
+                    double ny = fma(-p.x, ua[dj].y, fma(-p.y, ua[dj].x, o.y));
+                    nx = fma(-q.x, ub[dj].x, fma(q.y, ub[dj].y, nx));
+                    ny = fma(-q.x, ub[dj].y, fma(-q.y, ub[dj].x, ny));
                     v[u][di][dj] = make_double2(nx, ny);
-                    int dst = -1;
-                    double2 val;
-                    if (j == k + 1 && i >= j && i < L) { dst = i; val = make_double2(nx, ny); }
-                    if (i == k + 1 && j < i) { dst = j; val = make_double2(nx, -ny); }
-                    if (dst >= 0) {
+                }
+            }
+            if (bi[u] == kb || bj[u] == kb || bi[u] == kb + 1 || bj[u] == kb + 1) {
+                if (bi[u] == kb && bj[u] == kb) {
+                    v[u][0][0] = make_double2(-m00, 0.0);
+                    v[u][1][0] = make_double2(-m10.x, -m10.y);
+                    v[u][1][1] = make_double2(-m11, 0.0);
+                } else if (bj[u] == kb) {
 #pragma unroll
-                        for (int r = 0; r < GJ_CL; ++r) {
-                            double2* rb = cl.map_shared_rank(cbuf, r);
-                            rb[nxt + dst] = val;
-                        }
+                    for (int di = 0; di < 2; ++di) {
+                        const double2 x0 = v[u][di][0], x1 = v[u][di][1];
+                        v[u][di][0] = make_double2(fma(x1.x, m10.x, fma(-x1.y, m10.y, x0.x * m00)),
+                                                   fma(x1.x, m10.y, fma(x1.y, m10.x, x0.y * m00)));
+                        v[u][di][1] = make_double2(fma(x0.x, m01.x, fma(-x0.y, m01.y, x1.x * m11)),
+                                                   fma(x0.x, m01.y, fma(x0.y, m01.x, x1.y * m11)));
+                    }
+                } else if (bi[u] == kb) {
+#pragma unroll
+                    for (int dj = 0; dj < 2; ++dj) {
+                        const double2 x0 = v[u][0][dj], x1 = v[u][1][dj];
+                        v[u][0][dj] = make_double2(fma(m01.x, x1.x, fma(-m01.y, x1.y, m00 * x0.x)),
+                                                   fma(m01.x, x1.y, fma(m01.y, x1.x, m00 * x0.y)));
+                        v[u][1][dj] = make_double2(fma(m10.x, x0.x, fma(-m10.y, x0.y, m11 * x1.x)),
+                                                   fma(m10.x, x0.y, fma(m10.y, x0.x, m11 * x1.y)));
                     }
                 }
+                if (bi[u] == kb + 1 && bj[u] == kb + 1) {
+                    double kn[6];
+                    invert_k(v[u][0][0].x, v[u][1][0].x, v[u][1][0].y, v[u][1][1].x, kn);
+#pragma unroll
+                    for (int r = 0; r < GJ_CL; ++r) {
+                        double* rk = cl.map_shared_rank(&kv[0][0], r) + (ph ^ 1) * 6;
+#pragma unroll
+                        for (int t = 0; t < 6; ++t) rk[t] = kn[t];
+                    }
+#pragma unroll
+                    for (int di = 0; di < 2; ++di) {
+                        bcast(nx0 + i0 + di, make_double2(0.0, 0.0));
+                        bcast(nx1 + i0 + di, make_double2(0.0, 0.0));
+                    }
+                } else if (bj[u] == kb + 1) {
+#pragma unroll
+                    for (int di = 0; di < 2; ++di) {
+                        bcast(nx0 + i0 + di, v[u][di][0]);
+                        bcast(nx1 + i0 + di, v[u][di][1]);
+                    }
+                } else if (bi[u] == kb + 1) {
+#pragma unroll
+                    for (int dj = 0; dj < 2; ++dj) {
+                        bcast(nx0 + j0 + dj, make_double2(v[u][0][dj].x, -v[u][0][dj].y));
+                        bcast(nx1 + j0 + dj, make_double2(v[u][1][dj].x, -v[u][1][dj].y));
+                    }
+                }
+            }
         }
         cl.sync();
     }
