@@ -1775,7 +1775,7 @@ int large_factor_chain(const LargeArgs& g, const LargeLayout& l, const double* x
     PSCA_K((finish_sigma_large<<<(l.LP * l.LP + NT - 1) / NT, NT, 0, st>>>(g)));
     PSCA_K((frob_large<<<1, NT, 0, st>>>(g)));
     {
-        const size_t sm = (size_t)4 * l.LP * 16;   // [2 phases][2 pivot columns][LP]
+        const size_t sm = (size_t)8 * l.LP * 16;   // [2 phases][4 pivot columns][LP]
         PSCA_K((gj_cluster<<<GJ_CL, GJ_NT, sm, st>>>(g)));
     }
     if (g.record_objective) PSCA_K((trace_large<<<1, NT, 0, st>>>(g)));

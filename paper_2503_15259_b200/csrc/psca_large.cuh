@@ -34,7 +34,7 @@ constexpr int QL_KC = 16;    // complex rows per K chunk (8 k-steps)
 constexpr int QL_RT = 32;    // complex rows per row tile (8 row blocks)
 constexpr int RL_NC = 32;    // columns per rebuild chunk
 constexpr int GJ_CL = 8;     // CTAs per GJ cluster
-constexpr int GJ_NT = 1024;  // threads per GJ CTA
+constexpr int GJ_NT = 512;   // threads per GJ CTA
 
 struct LargeArgs {
     int kind, N, L, LP, NRB, T, n_antennas, record_objective, k;
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(NT) frob_large(LargeArgs a) {
 __global__ void __cluster_dims__(GJ_CL, 1, 1) __launch_bounds__(GJ_NT, 1)
 gj_cluster(LargeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* cbuf = reinterpret_cast<double2*>(smem_raw);   // [2][LP]
+    double2* cbuf = reinterpret_cast<double2*>(smem_raw);   // [2 phases][4 columns][LP]
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     if (a.flag[0]) return;   // uniform across the cluster
@@ -466,7 +466,7 @@ gj_cluster(LargeArgs a) {
     const int gtid = rank * GJ_NT + threadIdx.x;
     constexpr int GT = GJ_CL * GJ_NT;
     const int nbl = LP / 2, nlb = nbl * (nbl + 1) / 2;
-    constexpr int SLMAX = 2;   // LP <= 256: 8256 lower blocks <= 2 * 8192
+    constexpr int SLMAX = (256 / 2) * (256 / 2 + 1) / 2 / (GJ_CL * GJ_NT) + 1;   // LP <= 256
     int bi[SLMAX], bj[SLMAX];
     double2 v[SLMAX][2][2];
 #pragma unroll
@@ -482,142 +482,276 @@ gj_cluster(LargeArgs a) {
                                                                        : make_double2(0.0, 0.0);
             }
     }
-    // 2x2 block pivots K = {k, k+1} (as factor_pass): one cluster barrier per
-    // two pivots.  Per step every CTA holds (ping-pong) the two columns of K
-    // for all rows with the K entries zeroed, and kv = (M = K^-1, the two
-    // pivots); the owners of the next block's row / column broadcast them
-    // into all CTAs through DSMEM.
-    __shared__ double kv[2][6];   // m00, m10.x, m10.y, m11, a, d1
-    auto invert_k = [&](double ka, double kbr, double kbi, double kc, double* out) {
-        out[4] = ka;
-        out[5] = -1.0;
-        if (!(ka > 0.0)) return;
-        const double ainv = __drcp_rn(ka);
-        const double d1 = kc - (kbr * kbr + kbi * kbi) * ainv;
-        out[5] = d1;
-        if (!(d1 > 0.0)) return;
-        const double d1inv = __drcp_rn(d1);
-        out[0] = fma((kbr * kbr + kbi * kbi) * ainv * ainv, d1inv, ainv);
-        out[1] = -kbr * ainv * d1inv;
-        out[2] = -kbi * ainv * d1inv;
-        out[3] = d1inv;
-    };
+    // 4x4 block pivots K = {k, .., k+3}: one cluster barrier per four pivots.
+    // Per step every CTA holds (ping-pong) the four columns of K for all rows
+    // with the K rows zeroed (cs[q][i] = a_i,k+q) and K itself (kr, full
+    // 4 x 4); the owners of the next block's rows / columns broadcast them into
+    // all CTAs through DSMEM.  Every thread inverts K redundantly by 2 x 2
+    // blocks (pivots = those of the scalar sweep), then a_ij -= C_i M C_j^H
+    // (i, j not in K), the K rows / columns become M-scaled (from the staged
+    // pre-step values) and a_KK -> -M.
+    __shared__ double2 kr[2][16];
+    constexpr int PB = 4;
+    const int LE = (L + PB - 1) / PB * PB;   // identity padding pivots L..LE-1 (LE <= LP)
 #pragma unroll
     for (int u = 0; u < SLMAX; ++u)
 #pragma unroll
         for (int di = 0; di < 2; ++di)
 #pragma unroll
-            for (int dj = 0; dj < 2; ++dj)
-                if ((L & 1) && 2 * bi[u] + di == L && 2 * bj[u] + dj == L)
-                    v[u][di][dj] = make_double2(1.0, 0.0);   // identity padding pivot
+            for (int dj = 0; dj < 2; ++dj) {
+                const int i = 2 * bi[u] + di, j = 2 * bj[u] + dj;
+                if (i == j && i >= L && i < LE) v[u][di][dj] = make_double2(1.0, 0.0);
+            }
+    auto xval = [&](int i, int j) -> double2 {   // initial Sigma with the padding pivots
+        if (i < L && j < L) return a.Xg[(size_t)i * LP + j];
+        return (i == j && i < LE) ? make_double2(1.0, 0.0) : make_double2(0.0, 0.0);
+    };
     for (int e = threadIdx.x; e < LP; e += GJ_NT) {
-        cbuf[e] = (e < L && e >= 2) ? a.Xg[(size_t)e * LP] : make_double2(0.0, 0.0);
-        cbuf[LP + e] = (e < L && e >= 2) ? a.Xg[(size_t)e * LP + 1] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            cbuf[q * LP + e] = (e >= PB) ? xval(e, q) : make_double2(0.0, 0.0);
     }
-    if (threadIdx.x == 0) {
-        const double2 bb = (L > 1) ? a.Xg[LP] : make_double2(0.0, 0.0);
-        invert_k(a.Xg[0].x, bb.x, bb.y, (L > 1) ? a.Xg[LP + 1].x : 1.0, kv[0]);
-    }
+    if (threadIdx.x < 16) kr[0][threadIdx.x] = xval(threadIdx.x >> 2, threadIdx.x & 3);
     cl.sync();
     double logdet = 0.0;
     bool ok = true;
-    const int LE = (L + 1) & ~1;
-    for (int k = 0; k < LE; k += 2) {
-        const int ph = (k >> 1) & 1;
-        const double2* c0 = cbuf + ph * 2 * LP;
-        const double2* c1 = c0 + LP;
-        const int nx0 = (ph ^ 1) * 2 * LP, nx1 = nx0 + LP;
-        const double ka = kv[ph][4], d1 = kv[ph][5];   // identical in every CTA
-        if (!(ka > 0.0) || !(d1 > 0.0)) {
+    for (int k = 0; k < LE; k += PB) {
+        const int ph = (k / PB) & 1;
+        const double2* cs = cbuf + ph * PB * LP;
+        const int nbase = (ph ^ 1) * PB * LP;
+        // ---- M = K^-1 by 2 x 2 blocks K = [[A, B^H], [B, C]] ------------------
+        const double2* K = kr[ph];
+        __shared__ double2 msm[16];   // M = K^-1 (row-major)
+        __shared__ double spiv[4];
+        if (threadIdx.x == 0) {
+            double piv[4];
+            // A^-1 (a = K00, b = K10, c = K11)
+            const double a0 = K[0].x, br = K[4].x, bi_ = K[4].y, c0 = K[5].x;
+            const double ainv = __drcp_rn(a0);
+            const double d1 = c0 - (br * br + bi_ * bi_) * ainv;
+            const double d1inv = __drcp_rn(d1);
+            piv[0] = a0;
+            piv[1] = d1;
+            // Ai = [[p, conj(r)], [r, s]]
+            const double ap = fma((br * br + bi_ * bi_) * ainv * ainv, d1inv, ainv);
+            const double as = d1inv;
+            const double arx = -br * ainv * d1inv, ary = -bi_ * ainv * d1inv;
+            // T = B Ai (2 x 2), B rows 2,3 cols 0,1 of K
+            double tx[2][2], ty[2][2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const double2 b0 = K[(2 + r) * 4 + 0], b1 = K[(2 + r) * 4 + 1];
+                // col 0: b0 * p + b1 * r
+                tx[r][0] = fma(b0.x, ap, b1.x * arx - b1.y * ary);
+                ty[r][0] = fma(b0.y, ap, b1.x * ary + b1.y * arx);
+                // col 1: b0 * conj(r) + b1 * s
+                tx[r][1] = fma(b1.x, as, b0.x * arx + b0.y * ary);
+                ty[r][1] = fma(b1.y, as, b0.y * arx - b0.x * ary);
+            }
+            // S = C - T B^H  (Hermitian 2 x 2): S[r][c] = C[r][c] - sum_p T[r][p] conj(B[c][p])
+            double sx[2][2], sy[2][2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double2 cc = K[(2 + r) * 4 + 2 + c];
+                    double x = cc.x, y = cc.y;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const double2 bb = K[(2 + c) * 4 + q];   // B[c][q]
+                        // T[r][q] * conj(bb)
+                        x -= tx[r][q] * bb.x + ty[r][q] * bb.y;
+                        y -= ty[r][q] * bb.x - tx[r][q] * bb.y;
+                    }
+                    sx[r][c] = x;
+                    sy[r][c] = y;
+                }
+            const double s0 = sx[0][0], sbr = sx[1][0], sbi = sy[1][0], s1 = sx[1][1];
+            const double sinv0 = __drcp_rn(s0);
+            const double d3 = s1 - (sbr * sbr + sbi * sbi) * sinv0;
+            const double d3inv = __drcp_rn(d3);
+            piv[2] = s0;
+            piv[3] = d3;
+            // Si = [[sp, conj(sr)], [sr, ss]]
+            const double sp = fma((sbr * sbr + sbi * sbi) * sinv0 * sinv0, d3inv, sinv0);
+            const double ss = d3inv;
+            const double srx = -sbr * sinv0 * d3inv, sry = -sbi * sinv0 * d3inv;
+            const double six[2][2] = {{sp, srx}, {srx, ss}};
+            const double siy[2][2] = {{0.0, -sry}, {sry, 0.0}};
+            // M22 = Si; M21 = -Si T; M11 = Ai + T^H Si T
+            double nx[2][2], ny[2][2];   // Si T
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    double x = 0.0, y = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        x += six[r][q] * tx[q][c] - siy[r][q] * ty[q][c];
+                        y += six[r][q] * ty[q][c] + siy[r][q] * tx[q][c];
+                    }
+                    nx[r][c] = x;
+                    ny[r][c] = y;
+                }
+            const double aix[2][2] = {{ap, arx}, {arx, as}};
+            const double aiy[2][2] = {{0.0, -ary}, {ary, 0.0}};
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    msm[(2 + r) * 4 + 2 + c] = make_double2(six[r][c], siy[r][c]);
+                    msm[(2 + r) * 4 + c] = make_double2(-nx[r][c], -ny[r][c]);
+                    msm[c * 4 + 2 + r] = make_double2(-nx[r][c], ny[r][c]);   // M12 = M21^H
+                    // (T^H Si T)[r][c] = sum_q conj(T[q][r]) (Si T)[q][c]
+                    double x = aix[r][c], y = aiy[r][c];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        x += tx[q][r] * nx[q][c] + ty[q][r] * ny[q][c];
+                        y += tx[q][r] * ny[q][c] - ty[q][r] * nx[q][c];
+                    }
+                    msm[r * 4 + c] = make_double2(x, y);
+                }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) spiv[r] = piv[r];
+        }
+        __syncthreads();
+        const double piv[4] = {spiv[0], spiv[1], spiv[2], spiv[3]};
+        auto M = [&](int r, int c) { return msm[r * 4 + c]; };
+        // a failed pivot is identical in every thread (same staged K)
+        if (!(piv[0] > 0.0) || !(piv[1] > 0.0) || !(piv[2] > 0.0) || !(piv[3] > 0.0)) {
             ok = false;
             break;
         }
-        if (a.record_objective) logdet += log(ka) + log(d1);
-        const double m00 = kv[ph][0], m11 = kv[ph][3];
-        const double2 m10 = make_double2(kv[ph][1], kv[ph][2]);
-        const double2 m01 = make_double2(m10.x, -m10.y);
+        if (a.record_objective) logdet += log(piv[0]) + log(piv[1]) + log(piv[2]) + log(piv[3]);
         const int kb = k >> 1;
         auto bcast = [&](int idx, double2 val) {
 #pragma unroll
             for (int r = 0; r < GJ_CL; ++r) cl.map_shared_rank(cbuf, r)[idx] = val;
         };
+        auto in_k = [&](int bb) { return bb == kb || bb == kb + 1; };
+        auto in_kn = [&](int bb) { return bb == kb + 2 || bb == kb + 3; };
 #pragma unroll
         for (int u = 0; u < SLMAX; ++u) {
             if (bi[u] < 0) continue;
             const int i0 = 2 * bi[u], j0 = 2 * bj[u];
-            double2 ua[2], ub[2];   // U_j = M conj(C_j)
-#pragma unroll
-            for (int dj = 0; dj < 2; ++dj) {
-                const double2 p = c0[j0 + dj], q = c1[j0 + dj];
-                ua[dj] = make_double2(fma(m01.x, q.x, fma(m01.y, q.y, m00 * p.x)),
-                                      fma(m01.y, q.x, fma(-m01.x, q.y, -m00 * p.y)));
-                ub[dj] = make_double2(fma(m11, q.x, fma(m10.x, p.x, m10.y * p.y)),
-                                      fma(-m11, q.y, fma(m10.y, p.x, -m10.x * p.y)));
-            }
-#pragma unroll
-            for (int di = 0; di < 2; ++di) {
-                const double2 p = c0[i0 + di], q = c1[i0 + di];
+            if (!in_k(bi[u]) && !in_k(bj[u])) {
+                // generic: a_ij -= sum_p c_p[i] U_j[p], U_j = M conj(C_j); one
+                // column of the block at a time (register pressure)
 #pragma unroll
                 for (int dj = 0; dj < 2; ++dj) {
-                    const double2 o = v[u][di][dj];
-                    double nx = fma(-p.x, ua[dj].x, fma(p.y, ua[dj].y, o.x));
-                    double ny = fma(-p.x, ua[dj].y, fma(-p.y, ua[dj].x, o.y));
-                    nx = fma(-q.x, ub[dj].x, fma(q.y, ub[dj].y, nx));
-                    ny = fma(-q.x, ub[dj].y, fma(-q.y, ub[dj].x, ny));
-                    v[u][di][dj] = make_double2(nx, ny);
+                    double2 uu[PB];
+                    {
+                        double2 cj[PB];
+#pragma unroll
+                        for (int q = 0; q < PB; ++q) cj[q] = cs[q * LP + j0 + dj];
+#pragma unroll
+                        for (int p = 0; p < PB; ++p) {
+                            double x = 0.0, y = 0.0;
+#pragma unroll
+                            for (int q = 0; q < PB; ++q) {   // M[p][q] * conj(cj[q])
+                                const double2 mv = M(p, q);
+                                x = fma(mv.x, cj[q].x, fma(mv.y, cj[q].y, x));
+                                y = fma(mv.y, cj[q].x, fma(-mv.x, cj[q].y, y));
+                            }
+                            uu[p] = make_double2(x, y);
+                        }
+                    }
+#pragma unroll
+                    for (int di = 0; di < 2; ++di) {
+                        double nx = v[u][di][dj].x, ny = v[u][di][dj].y;
+#pragma unroll
+                        for (int p = 0; p < PB; ++p) {
+                            const double2 c = cs[p * LP + i0 + di];
+                            nx = fma(-c.x, uu[p].x, fma(c.y, uu[p].y, nx));
+                            ny = fma(-c.x, uu[p].y, fma(-c.y, uu[p].x, ny));
+                        }
+                        v[u][di][dj] = make_double2(nx, ny);
+                    }
+                }
+            } else if (in_k(bi[u]) && in_k(bj[u])) {
+#pragma unroll
+                for (int di = 0; di < 2; ++di)
+#pragma unroll
+                    for (int dj = 0; dj < 2; ++dj) {
+                        const int p = i0 + di - k, q = j0 + dj - k;
+                        v[u][di][dj] = make_double2(-M(p, q).x, -M(p, q).y);
+                    }
+            } else if (in_k(bj[u])) {
+                // rows i not in K, columns K: a_i,k+q <- sum_p a_i,k+p M[p][q]
+#pragma unroll
+                for (int di = 0; di < 2; ++di) {
+                    double2 ci[PB];
+#pragma unroll
+                    for (int p = 0; p < PB; ++p) ci[p] = cs[p * LP + i0 + di];
+#pragma unroll
+                    for (int dj = 0; dj < 2; ++dj) {
+                        const int q = j0 + dj - k;
+                        double x = 0.0, y = 0.0;
+#pragma unroll
+                        for (int p = 0; p < PB; ++p) {
+                            x = fma(ci[p].x, M(p, q).x, fma(-ci[p].y, M(p, q).y, x));
+                            y = fma(ci[p].x, M(p, q).y, fma(ci[p].y, M(p, q).x, y));
+                        }
+                        v[u][di][dj] = make_double2(x, y);
+                    }
+                }
+            } else {
+                // rows K, columns j not in K: a_k+p,j <- sum_q M[p][q] a_k+q,j
+                //   with a_k+q,j = conj(c_q[j])
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) {
+                    double2 cj[PB];
+#pragma unroll
+                    for (int q = 0; q < PB; ++q) cj[q] = cs[q * LP + j0 + dj];
+#pragma unroll
+                    for (int di = 0; di < 2; ++di) {
+                        const int p = i0 + di - k;
+                        double x = 0.0, y = 0.0;
+#pragma unroll
+                        for (int q = 0; q < PB; ++q) {
+                            x = fma(M(p, q).x, cj[q].x, fma(M(p, q).y, cj[q].y, x));
+                            y = fma(M(p, q).y, cj[q].x, fma(-M(p, q).x, cj[q].y, y));
+                        }
+                        v[u][di][dj] = make_double2(x, y);
+                    }
                 }
             }
-            if (bi[u] == kb || bj[u] == kb || bi[u] == kb + 1 || bj[u] == kb + 1) {
-                if (bi[u] == kb && bj[u] == kb) {
-                    v[u][0][0] = make_double2(-m00, 0.0);
-                    v[u][1][0] = make_double2(-m10.x, -m10.y);
-                    v[u][1][1] = make_double2(-m11, 0.0);
-                } else if (bj[u] == kb) {
+            // ---- stage the next pivot block K' = {k+4, .., k+7} ----------------
+            if (in_kn(bi[u]) && in_kn(bj[u])) {
 #pragma unroll
-                    for (int di = 0; di < 2; ++di) {
-                        const double2 x0 = v[u][di][0], x1 = v[u][di][1];
-                        v[u][di][0] = make_double2(fma(x1.x, m10.x, fma(-x1.y, m10.y, x0.x * m00)),
-                                                   fma(x1.x, m10.y, fma(x1.y, m10.x, x0.y * m00)));
-                        v[u][di][1] = make_double2(fma(x0.x, m01.x, fma(-x0.y, m01.y, x1.x * m11)),
-                                                   fma(x0.x, m01.y, fma(x0.y, m01.x, x1.y * m11)));
-                    }
-                } else if (bi[u] == kb) {
+                for (int di = 0; di < 2; ++di)
 #pragma unroll
                     for (int dj = 0; dj < 2; ++dj) {
-                        const double2 x0 = v[u][0][dj], x1 = v[u][1][dj];
-                        v[u][0][dj] = make_double2(fma(m01.x, x1.x, fma(-m01.y, x1.y, m00 * x0.x)),
-                                                   fma(m01.x, x1.y, fma(m01.y, x1.x, m00 * x0.y)));
-                        v[u][1][dj] = make_double2(fma(m10.x, x0.x, fma(-m10.y, x0.y, m11 * x1.x)),
-                                                   fma(m10.x, x0.y, fma(m10.y, x0.x, m11 * x1.y)));
+                        const int p = i0 + di - k - PB, q = j0 + dj - k - PB;
+                        if (p >= q) {
+                            const double2 val = v[u][di][dj];
+#pragma unroll
+                            for (int r = 0; r < GJ_CL; ++r) {
+                                double2* rk = cl.map_shared_rank(&kr[0][0], r) + (ph ^ 1) * 16;
+                                rk[p * 4 + q] = val;
+                                rk[q * 4 + p] = make_double2(val.x, -val.y);
+                            }
+                        }
                     }
+                if (bi[u] == bj[u]) {   // the diagonal owners zero K' rows in the staged columns
+#pragma unroll
+                    for (int di = 0; di < 2; ++di)
+#pragma unroll
+                        for (int q = 0; q < PB; ++q) bcast(nbase + q * LP + i0 + di, make_double2(0.0, 0.0));
                 }
-                if (bi[u] == kb + 1 && bj[u] == kb + 1) {
-                    double kn[6];
-                    invert_k(v[u][0][0].x, v[u][1][0].x, v[u][1][0].y, v[u][1][1].x, kn);
+            } else if (in_kn(bj[u])) {
 #pragma unroll
-                    for (int r = 0; r < GJ_CL; ++r) {
-                        double* rk = cl.map_shared_rank(&kv[0][0], r) + (ph ^ 1) * 6;
+                for (int di = 0; di < 2; ++di)
 #pragma unroll
-                        for (int t = 0; t < 6; ++t) rk[t] = kn[t];
-                    }
+                    for (int dj = 0; dj < 2; ++dj)
+                        bcast(nbase + (j0 + dj - k - PB) * LP + i0 + di, v[u][di][dj]);
+            } else if (in_kn(bi[u])) {
 #pragma unroll
-                    for (int di = 0; di < 2; ++di) {
-                        bcast(nx0 + i0 + di, make_double2(0.0, 0.0));
-                        bcast(nx1 + i0 + di, make_double2(0.0, 0.0));
-                    }
-                } else if (bj[u] == kb + 1) {
+                for (int di = 0; di < 2; ++di)
 #pragma unroll
-                    for (int di = 0; di < 2; ++di) {
-                        bcast(nx0 + i0 + di, v[u][di][0]);
-                        bcast(nx1 + i0 + di, v[u][di][1]);
-                    }
-                } else if (bi[u] == kb + 1) {
-#pragma unroll
-                    for (int dj = 0; dj < 2; ++dj) {
-                        bcast(nx0 + j0 + dj, make_double2(v[u][0][dj].x, -v[u][0][dj].y));
-                        bcast(nx1 + j0 + dj, make_double2(v[u][1][dj].x, -v[u][1][dj].y));
-                    }
-                }
+                    for (int dj = 0; dj < 2; ++dj)
+                        bcast(nbase + (i0 + di - k - PB) * LP + j0 + dj,
+                              make_double2(v[u][di][dj].x, -v[u][di][dj].y));
             }
         }
         cl.sync();
