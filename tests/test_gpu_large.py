@@ -61,7 +61,7 @@ def test_large_path_equals_batched_path(cuda_device, L, kind, monkeypatch):
         assert max_rel(xl[k], small[k]) <= 1e-11
 
 
-@pytest.mark.parametrize("L,kind", [(160, "ml-k"), (130, "map-ur")])
+@pytest.mark.parametrize("L,kind", [(160, "ml-k"), (130, "map-ur"), (131, "ml-ud")])
 def test_large_l_matches_oracle(cuda_device, L, kind):
     pkg, est, _ = _pkg()
     from paper_2503_15259_b200 import scenes
