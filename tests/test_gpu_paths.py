@@ -83,3 +83,41 @@ def test_persistent_equals_two_kernel_bitwise(cuda_device):
                                           err_msg=f"{key} {field}")
         # the objective's trace / Frobenius reductions run over different CTA sizes
         assert max_rel(np.array(pers[key]["obj"]), np.array(two[key]["obj"])) <= 1e-13
+
+
+def test_warp_kernel_options_match_tile_kernel(cuda_device):
+    """Options the batch path exercises rarely, with one chunk per instance (the
+    warp-streamed column kernel) against column chunks (the tile kernel): iterate
+    recording, a pairwise MAP-K prior, and a tol stop."""
+    from paper_2503_15259_b200 import device, estimators, priors, scenes
+    cfg = scenes.SceneConfig(5, "ml-ud", 240, 24, 48, 12, 15, 4)
+    ss = [scenes.make_scene(cfg, i) for i in range(4)]
+    b = scenes.stack_batch(ss)
+    steps = estimators.default_steps(15)
+    pr = priors.PairwiseMvbPrior.from_group_model(240, 4, 0.1)
+    c1 = np.broadcast_to(pr.c1, (240,)).astype(float)
+    un = device.solve("ml-k", b["pilots"], b["emp_cov"], b["noise"], 48, steps, gains=b["gains"],
+                      max_iter=15)["update_norm"].cpu().numpy()
+    cases = {
+        "iterates": dict(kind="ml-ud", record_iterates=True),
+        "pairwise": dict(kind="map-k", gains=b["gains"], prior_c1=c1, prior_c2=pr.csr_arrays(),
+                         record_objective=True),
+        # stops some instances around iteration 6
+        "tol": dict(kind="ml-k", gains=b["gains"], tol=float(np.median(un[:, 6]))),
+    }
+    for name, kw in cases.items():
+        kind = kw.pop("kind")
+        res = {}
+        for nck in (1, 0):
+            r = device.solve(kind, b["pilots"], b["emp_cov"], b["noise"], 48, steps, max_iter=15,
+                             n_chunks=nck, **kw)
+            res[nck] = {k: v.cpu().numpy() for k, v in r.items()
+                        if k in ("x", "iterates", "objective", "n_iter", "status") and v is not None}
+        assert max_rel(res[1]["x"], res[0]["x"]) <= 1e-10, name
+        np.testing.assert_array_equal(res[1]["n_iter"], res[0]["n_iter"], err_msg=name)
+        np.testing.assert_array_equal(res[1]["status"], res[0]["status"], err_msg=name)
+        if "iterates" in res[0]:
+            assert max_rel(res[1]["iterates"], res[0]["iterates"]) <= 1e-10, name
+        if "objective" in res[0]:
+            assert max_rel(res[1]["objective"], res[0]["objective"]) <= 1e-11, name
+    assert int(res[0]["n_iter"].min()) < 15   # the tol case stopped early
