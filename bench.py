@@ -405,7 +405,7 @@ def ours_arm(args):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": ems / args.steps,
                "api": "paper_2503_15259_b200.psca_run_batch_host (pinned host in, host out; "
-                      "growing chunks of 1, 6 and the remaining waves of instances, each "
+                      "growing chunks of 1, 2, 4 and the remaining waves of instances, each "
                       "chunk's H2D overlapped with the previous chunk's solve)",
                "x_matches_device_run": bool(torch.equal(r["x"], out["x"].cpu()))}
 

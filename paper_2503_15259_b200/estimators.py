@@ -299,7 +299,7 @@ def _host_chunk_bounds(B: int, chunks: int) -> list:
     if chunks <= 0:
         wave = 2 * device.sm_count()           # column CTAs resident at once
         if B >= 8 * wave:
-            return [0, wave, 7 * wave, B]
+            return [0, wave, 3 * wave, 7 * wave, B]
         chunks = 4 if B >= 4 * wave else (2 if B >= 2 * wave else 1)
     chunks = max(1, min(chunks, B))
     return [(B * c) // chunks for c in range(chunks + 1)]
@@ -316,9 +316,9 @@ def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=
     on a copy stream while chunk c is solved on the current stream, and each
     chunk's estimates are copied back as soon as it is solved.  ``chunks`` = 0
     picks growing chunks: one wave of column CTAs first (its upload is the only
-    copy not hidden), then six waves (uploaded while the first solves; the
-    upload runs ~6x faster than the solve consumes instances at L = 40), then
-    the rest; ``chunks`` > 0 cuts equal chunks.
+    copy not hidden), then two and four waves (each uploaded while the previous
+    chunk solves, with margin for a slower host link), then the rest
+    (tools/e2e_sweep.py compares schedules); ``chunks`` > 0 cuts equal chunks.
     Returns host tensors x (B,N), status (B,), n_iter (B,).
     """
     import torch
