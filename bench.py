@@ -228,6 +228,15 @@ def ncu_share():
         return None
 
 
+def ncu_pipe(name: str = "column_kernel"):
+    """DMMA sub-pipe busy fraction of the kernel's committed full ncu capture, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        return json.loads(p.read_text())[name]["dmma_pipe_active_pct_full_capture"] / 100.0
+    except Exception:
+        return None
+
+
 def ncu_traffic(name: str = "column_kernel"):
     """dram bytes per launch of the column kernel from the committed ncu summary, if any."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -438,7 +447,8 @@ def ours_arm(args):
                 "executed_quad_frac": executed / peak,
                 "executed_note": "DMMA flops of the quadratic forms alone (a lower bound on "
                                  "what the kernel executes) over the same launch time; ncu "
-                                 "measures the DMMA sub-pipe ~78 % busy in column_kernel_w<10> (profiles/README.md)",
+                                 "measures the DMMA sub-pipe busy fraction in column_kernel_w<10> (dmma_pipe_busy_ncu, "
+                                 "profiles/README.md)",
                 "overlap_note": "on the split-stream path the column launches of one half "
                                 "batch run concurrently with the other half's factor launches, "
                                 "so each CUDA-event launch duration includes that SM sharing",
@@ -446,6 +456,7 @@ def ours_arm(args):
                 "factor_ms_per_launch": prof["factor_ms"] / max(prof["factor_launches"], 1),
                 "column_share": prof["column_ms"] / max(prof["column_ms"] + prof["factor_ms"], 1e-9),
                 "column_share_ncu": ncu_share(),
+                "dmma_pipe_busy_ncu": ncu_pipe(),
                 "share_note": "column_share is from CUDA events on the split streams (each interval "
                               "also spans the other half's concurrent kernel); column_share_ncu is "
                               "from the serialised ncu launch list in profiles/ncu_summary.json",
