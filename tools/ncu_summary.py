@@ -35,5 +35,14 @@ for key, pat in (("column_kernel", "column_kernel"), ("factor_kernel", "factor_s
                 "dram_write_bytes_per_launch": int(wr), "mean_duration_ns_cold": int(dur)}
     if key == "column_kernel":
         out[key]["algorithmic_pilot_bytes_per_launch"] = per_launch * 1000 * 40 * 16
+# keep the full-capture figures (pipe utilisation of one --set full launch) already recorded
+try:
+    prev = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+    for key in ("column_kernel", "factor_kernel"):
+        for k, v in prev.get(key, {}).items():
+            if "full_capture" in k and key in out:
+                out[key][k] = v
+except Exception:
+    pass
 (ROOT / "profiles" / "ncu_summary.json").write_text(json.dumps(out, indent=2) + "\n")
 print(json.dumps(out, indent=2))
