@@ -36,6 +36,9 @@
 #ifndef PSCA_BLOCK_SWEEP
 #define PSCA_BLOCK_SWEEP 1
 #endif
+#ifndef PSCA_ADJ_INV
+#define PSCA_ADJ_INV 1   // 2x2 pivot block inverse as adj(K)/det(K)
+#endif
 constexpr int QCB = PSCA_QCB;                // 8-column blocks per warp in the quad stage
 constexpr int QPARTS = NWARP / (NCB / QCB);  // row-block groups (LPT-balanced)
 
@@ -612,6 +615,22 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
             ok = false;
             break;
         }
+#if PSCA_ADJ_INV
+        // M = K^-1 = adj(K) / det(K), det = a c - |b|^2 = a d1 (d1 = the
+        // second scalar-sweep pivot): one reciprocal per step instead of two
+        // dependent ones; K is PD iff a > 0 and det > 0
+        const double det = fma(ka, kc, -fma(kbr, kbr, kbi * kbi));
+        if (!(det > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (want_logdet) logdet += log(det);
+        const double dinv = __drcp_rn(det);
+        const double m00 = kc * dinv;
+        const double m11 = ka * dinv;
+        const double2 m10 = make_double2(-kbr * dinv, -kbi * dinv);
+        const double2 m01 = make_double2(m10.x, -m10.y);
+#else
         const double ainv = __drcp_rn(ka);
         const double d1 = kc - (kbr * kbr + kbi * kbi) * ainv;
         if (!(d1 > 0.0)) {
@@ -625,6 +644,7 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         const double m11 = d1inv;
         const double2 m10 = make_double2(-kbr * ainv * d1inv, -kbi * ainv * d1inv);
         const double2 m01 = make_double2(m10.x, -m10.y);
+#endif
         const int kb = k >> 1;
 #pragma unroll
         for (int u = 0; u < F::SL; ++u) {
