@@ -13,15 +13,21 @@ batched solve of the whole batch.
   e2e    the same through the public API (psca_run_batch) from pinned HOST
          buffers: H2D of the step's pilots / Sigma_hat / noise and D2H of the
          estimates inside the timed region
-  roofline  column_kernel (the dominant kernel): algorithmic FP64 flops per
-         launch (24 N L^2 per instance-iteration) / its mean
-         CUDA-event duration, against the FP64 peak measured live (cuBLAS DGEMM)
+  roofline  the dominant kernel (the warp-streamed column kernel): the FP64
+         DMMA flops it EXECUTES per launch (closed form per 8-column block +
+         the moving columns of the rebuild, counted exactly in an untimed
+         iterate-recording pass) / its mean SERIALISED launch time (one solve
+         with every launch on one stream, CUDA events around each launch),
+         against the FP64 peak measured live (cuBLAS DGEMM); the algorithmic
+         24 N L^2 ratio is reported beside it as algorithmic_frac
   cpu_baseline  the CPU oracle (numpy/OpenBLAS restatement of the reference)
          on this host's cores, one process per core, bounded sample
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle port; the reference is pure Python and cannot travel to the box) on
-the same workload with all host cores and prints the same JSON line.
+``--config`` selects another BASELINE configuration (c0, c2, c2net, c3_l20,
+c3_l40, c3_l80, c4); the driver's default line is c1.  ``--impl reference``
+times the reference algorithm's CPU implementation (the oracle port; the
+reference is pure Python and cannot travel to the box) on the same workload
+with all host cores (scene generation untimed) and prints the same JSON line.
 """
 
 from __future__ import annotations
@@ -41,8 +47,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "detection instances/sec and PSCA iters/sec at N=1000,L=40,M=128; % of roofline"
 UNIT = "instances/s"
-CONFIG_NAME = "c1"
-ALGO_FLOPS_PER_UNIT = "24*N*L^2 FP64 flops per instance-iteration (SURVEY.md 8(d))"
+CONFIGS = ["c0", "c1", "c2", "c2net", "c3_l20", "c3_l40", "c3_l80", "c4"]
+DMMA_FLOPS = 512.0   # mma.m8n8k4.f64: 8 x 8 x 4 multiply-adds
 
 
 def parse_args():
@@ -57,10 +63,61 @@ def parse_args():
                     help="CPU-baseline sample budget (seconds of solve time per worker)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--config", default="c1", choices=["c1", "c4"],
-                    help="c1 (headline, default) or c4 (one N=100000, L=256 instance, "
-                         "devices column-sharded over the ranks, NCCL all-reduce per iteration)")
+    ap.add_argument("--no-executed", action="store_true",
+                    help="skip the untimed iterate-recording pass that counts executed DMMAs")
+    ap.add_argument("--config", default="c1", choices=CONFIGS,
+                    help="BASELINE configuration: c1 (headline, default), c0, c2, c2net (the "
+                         "PSCA-Net forward of c2), c3_l20/l40/l80, or c4 (one N=100000, L=256 "
+                         "instance, devices column-sharded over the ranks, NCCL all-reduce per "
+                         "iteration)")
     return ap.parse_args()
+
+
+class Workload:
+    """One BASELINE configuration as the bench runs it."""
+
+    def __init__(self, name: str, iters: int = 0, batch: int = 0):
+        from paper_2503_15259_b200 import estimators, scenes
+        self.name = name
+        self.scene_name = "c2" if name == "c2net" else name
+        self.cfg = scenes.BASELINE_CONFIGS[self.scene_name]
+        self.net = name == "c2net"
+        if self.net:
+            self.steps = scenes.net_steps(self.cfg.net_blocks)
+            self.iters = iters or self.cfg.net_blocks
+            self.schedule = estimators.StepSchedule.explicit(self.steps)
+        else:
+            self.iters = iters or self.cfg.n_iter
+            self.schedule = estimators.StepSchedule.default()
+            self.steps = self.schedule.materialize(self.iters)
+        self.batch = batch or self.cfg.batch
+        self.problem = scenes.problem_for(self.cfg)
+        self.known = self.cfg.kind in ("ml-k", "map-k")
+        c = self.cfg
+        what = {"ml-k": "PSCA-MLE known pathloss (ml-k)", "ml-ud": "PSCA-MLE unknown pathloss (ml-ud)",
+                "map-k": "PSCA-MAPE known pathloss (map-k, p=0.05)",
+                "map-ur": "PSCA-MAPE unknown pathloss (map-ur, smoothed effective-pathloss prior)"}
+        step_rule = ("PSCA-Net forward, T=10 seeded per-layer steps" if self.net
+                     else "default step rule")
+        self.description = (f"{name}: {what[c.kind]}, N={c.n_devices}, L={c.pilot_len}, "
+                             f"M={c.n_antennas}, K={c.n_active} active, T={self.iters} iterations, "
+                             f"{step_rule}, complex128")
+        self.metric = METRIC if name == "c1" else \
+            f"detection instances/sec and PSCA iters/sec at {name} (N={c.n_devices},L={c.pilot_len},M={c.n_antennas}); % of roofline"
+
+    def config_block(self, batch, per_gpu=True, world=1):
+        c = self.cfg
+        pil = 16 * c.pilot_len * c.n_devices
+        return {"workload": self.description,
+                "instances_per_gpu" if per_gpu else "instances_per_step": batch,
+                "N": c.n_devices, "L": c.pilot_len, "M": c.n_antennas, "T": self.iters,
+                "kind": c.kind,
+                "l2": (f"inputs larger than L2 (pilots {pil // 1024} KB/instance, "
+                       f"{pil * batch / 1e9:.2f} GB per GPU vs 126 MB L2)") if pil * batch > 126e6
+                      else "inputs smaller than L2: every timed step re-reads them from L2 "
+                           "(latency-bound single instance)",
+                "parallelism": (f"instance sharding over {world} GPU(s), no collective"
+                                if batch > 1 else "one instance (replicas only)")}
 
 
 # ---------------------------------------------------------------------------
@@ -96,21 +153,33 @@ def generate(name: str, ids: list[int], workers: int):
 # CPU baseline (oracle, one process per core, OPENBLAS_NUM_THREADS=1)
 # ---------------------------------------------------------------------------
 
-def _cpu_worker(args):
-    wid, nworkers, budget_s, name, iters, per_step = args
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+def _oracle_solve(wl, s):
     import numpy as np
     from oracle import psca_oracle as orc
+    cfg = wl.cfg
+    kw = {}
+    if cfg.kind == "map-k":
+        kw["indep_p"] = np.full(cfg.n_devices, cfg.p)
+    elif cfg.kind == "map-ur":
+        kw["eff"] = orc.EffPrior.from_reference(wl.problem.prior)
+    return orc.psca(cfg.kind, s.pilots, s.gains, s.emp_cov, s.noise_power, s.n_antennas,
+                    wl.steps, wl.iters, **kw)
+
+
+def _cpu_worker(args):
+    """Solve instances of the workload on one core: scene generation untimed, the
+    oracle solve timed.  per_step > 0: exactly that many instances; else until
+    budget_s of solve time."""
+    wid, nworkers, budget_s, name, iters, per_step, base = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from paper_2503_15259_b200 import scenes
-    cfg = scenes.BASELINE_CONFIGS[name]
-    steps = orc.default_steps(iters)
+    wl = Workload(name, iters)
     done, solve_s = 0, 0.0
     i = wid
     while (per_step and done < per_step) or (not per_step and solve_s < budget_s):
-        s = scenes.make_scene(cfg, 10_000_000 + i)
+        s = scenes.make_scene(wl.cfg, base + i)
         t0 = time.perf_counter()
-        orc.psca(cfg.kind, s.pilots, s.gains, s.emp_cov, s.noise_power, s.n_antennas, steps,
-                 iters)
+        _oracle_solve(wl, s)
         solve_s += time.perf_counter() - t0
         done += 1
         i += nworkers
@@ -126,8 +195,8 @@ def _cpu_pool(workers):
 def cpu_baseline(name: str, iters: int, budget_s: float) -> dict:
     workers = os.cpu_count() or 1
     with _cpu_pool(workers) as pool:
-        pool.map(_cpu_worker, [(w, workers, 0.0, name, 2, 1) for w in range(workers)])  # warm
-        res = pool.map(_cpu_worker, [(w, workers, budget_s, name, iters, 0)
+        pool.map(_cpu_worker, [(w, workers, 0.0, name, 2, 1, 10_000_000) for w in range(workers)])
+        res = pool.map(_cpu_worker, [(w, workers, budget_s, name, iters, 0, 10_000_000)
                                      for w in range(workers)])
     n = sum(r[0] for r in res)
     rate = sum(r[0] / r[1] for r in res if r[1] > 0)
@@ -215,19 +284,6 @@ def fp64_peak_tflops(torch) -> float:
     return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
-def ncu_share():
-    """Column-kernel share of the step from the committed ncu launch list (serialised,
-    cold-cache launches: total column time / total column + factor time), if any."""
-    p = ROOT / "profiles" / "ncu_summary.json"
-    try:
-        d = json.loads(p.read_text())
-        c, f = d["column_kernel"], d["factor_kernel"]
-        tc = c["mean_duration_ns_cold"] * c["launches"]
-        return tc / (tc + f["mean_duration_ns_cold"] * f["launches"])
-    except Exception:
-        return None
-
-
 def ncu_pipe(name: str = "column_kernel"):
     """DMMA sub-pipe busy fraction of the kernel's committed full ncu capture, if any."""
     p = ROOT / "profiles" / "ncu_summary.json"
@@ -259,51 +315,106 @@ def dist_setup(args):
 
 
 def reference_arm(args):
+    """The reference algorithm's CPU implementation (the oracle port) on all host cores.
+
+    Each step: every core solves one instance of the workload (scene generation
+    untimed, as the GPU arms exclude it); the step's time is the slowest core's
+    solve time, so value = instances / sum of step times."""
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return 0
-    from paper_2503_15259_b200 import scenes
-    cfg = scenes.BASELINE_CONFIGS[CONFIG_NAME]
-    iters = args.iters or cfg.n_iter
+    if args.config == "c4":
+        print(json.dumps({"impl": "reference", "unavailable": "c4 reference arm: ~80 s per "
+                          "instance on the host; see DESIGN.md section 6"}), flush=True)
+        return 0
+    wl = Workload(args.config, args.iters)
     workers = os.cpu_count() or 1
     with _cpu_pool(workers) as pool:
         for _ in range(args.warmup):
-            pool.map(_cpu_worker, [(w, workers, 0, CONFIG_NAME, iters, 1) for w in range(workers)])
-        t0 = time.perf_counter()
-        n = 0
-        for _ in range(args.steps):
-            res = pool.map(_cpu_worker, [(w, workers, 0, CONFIG_NAME, iters, 1)
-                                         for w in range(workers)])
+            pool.map(_cpu_worker, [(w, workers, 0, wl.name, wl.iters, 1, 20_000_000)
+                                   for w in range(workers)])
+        n, wall = 0, 0.0
+        for st in range(args.steps):
+            res = pool.map(_cpu_worker, [(w, workers, 0, wl.name, wl.iters, 1,
+                                          30_000_000 + st * workers) for w in range(workers)])
             n += sum(r[0] for r in res)
-        wall = time.perf_counter() - t0
+            wall += max(r[1] for r in res)
     value = n / wall
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "impl": "reference", "metric": wl.metric, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(cfg, iters, workers, per_gpu=False),
-        "psca_iters_per_s": value * iters,
+        "config": wl.config_block(workers, per_gpu=False),
+        "psca_iters_per_s": value * wl.iters,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"each step: {workers} {CONFIG_NAME} instances (T={iters}), one per "
-                                   "host core, numpy/OpenBLAS oracle (restatement of the reference; "
-                                   "the reference is pure Python and cannot be installed on the box), "
-                                   "scene generation included"},
+                         "sample": f"each step: {workers} {wl.name} instances (T={wl.iters}), one "
+                                   "per host core, numpy/OpenBLAS oracle (restatement of the "
+                                   "reference; the reference is pure Python and cannot be "
+                                   "installed on the box); scene generation excluded, step time "
+                                   "= slowest core's solve"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_block(cfg, iters, batch, per_gpu=True):
-    return {"workload": f"{CONFIG_NAME}: PSCA-MLE unknown pathloss (ml-ud), N={cfg.n_devices}, "
-                        f"L={cfg.pilot_len}, M={cfg.n_antennas}, K={cfg.n_active} active, "
-                        f"T={iters} iterations, default step rule, complex128",
-            "instances_per_gpu" if per_gpu else "instances_per_step": batch,
-            "N": cfg.n_devices, "L": cfg.pilot_len, "M": cfg.n_antennas, "T": iters,
-            "kind": cfg.kind,
-            "l2": "inputs larger than L2 (pilots 640 KB/instance, 2.6 GB per GPU vs 126 MB L2)",
-            "parallelism": "instance sharding, no collective"}
+def executed_column_flops(wl, problem, pil_d, emp_d, noi_d, gain_d, m):
+    """Executed DMMA flops of the column launches of one solve, exactly.
+
+    Untimed pass with iterate recording.  Per instance-iteration the
+    warp-streamed column kernel issues 2 NRB (NRB + 1) DMMAs per 8-column
+    block for the two quadratic forms (lower block triangle of P' and A') and,
+    for its moving columns (non-zero rebuild weight rho cand g: exactly the
+    devices with x_{k+1} != (1 - rho_k) x_k), NBLK DMMAs per pair of listed
+    columns in rounds of 16 (psca_wcol.cuh wc_rebuild).  Returns
+    (flops per column launch, quad share, mean moving columns per iteration)."""
+    import torch
+    from paper_2503_15259_b200 import device, estimators
+    cfg = wl.cfg
+    nrb = next(r for r in (2, 3, 4, 5, 6, 8, 10, 12, 16, 20) if 4 * r >= cfg.pilot_len)
+    nblk = sum((4 * i + 3) // 8 + 1 for i in range(nrb))
+    B, N, T = pil_d.shape[0], cfg.n_devices, wl.iters
+    kw = estimators.prior_arrays(problem, N, m)
+    res = device.solve(cfg.kind, pil_d, emp_d, noi_d, m, wl.steps, gains=gain_d, max_iter=T,
+                       record_iterates=True, n_chunks=1, **kw)
+    its = res["iterates"]
+    n_iter = res["n_iter"].to(torch.int64)
+    quad_blk = 2 * nrb * (nrb + 1) * (-(-N // 8))
+    quad_total, rebuild_total, moving_total = 0, 0, 0
+    for k in range(T):
+        live = n_iter > k
+        omr = 1.0 - float(wl.steps[k])
+        mv = (its[:, k + 1] != omr * its[:, k]).sum(dim=1).to(torch.int64)
+        mv = torch.where(live, mv, torch.zeros_like(mv))
+        full, rest = mv // 16, mv % 16
+        rebuild_total += int((nblk * (8 * full + (rest + 1) // 2)).sum())
+        quad_total += int(live.sum()) * quad_blk
+        moving_total += int(mv.sum())
+    del its, res
+    torch.cuda.empty_cache()
+    flops = DMMA_FLOPS * (quad_total + rebuild_total) / T
+    return flops, quad_total / max(quad_total + rebuild_total, 1), moving_total / (B * T)
+
+
+def serial_launch_times(run):
+    """Mean serialised (single stream, no half-batch split) column and factor launch
+    times of one solve, from CUDA events around every launch."""
+    from paper_2503_15259_b200 import device
+    import torch
+    device.set_serial(True)
+    try:
+        torch.cuda.synchronize()
+        device.profile_begin()
+        run()
+        recs = device.profile_launches()
+        device.profile_end()
+    finally:
+        device.set_serial(False)
+    col = [ms for k, ms in recs if k == 0]
+    fac = [ms for k, ms in recs if k == 1]
+    return (sum(col) / max(len(col), 1), len(col), sum(fac) / max(len(fac), 1), len(fac),
+            sum(col), sum(fac))
 
 
 def ours_arm(args):
@@ -318,19 +429,20 @@ def ours_arm(args):
         torch.cuda.set_device(0)
     import __graft_entry__
     __graft_entry__.build()
-    from paper_2503_15259_b200 import device, estimators, scenes
+    from paper_2503_15259_b200 import device, estimators
 
-    cfg = scenes.BASELINE_CONFIGS[CONFIG_NAME]
-    B = args.batch or cfg.batch
-    iters = args.iters or cfg.n_iter
+    wl = Workload(args.config, args.iters, args.batch)
+    cfg, problem = wl.cfg, wl.problem
+    B, iters = wl.batch, wl.iters
     ids = list(range(rank * B, (rank + 1) * B))
-    host = generate(CONFIG_NAME, ids, os.cpu_count() or 1)
-    problem = scenes.problem_for(cfg)
+    host = generate(wl.scene_name, ids, os.cpu_count() or 1)
     dev = torch.device("cuda", torch.cuda.current_device())
     pil_h = torch.from_numpy(host["pilots"]).pin_memory()
     emp_h = torch.from_numpy(host["emp_cov"]).pin_memory()
     noi_h = torch.from_numpy(host["noise"]).pin_memory()
+    gain_h = torch.from_numpy(host["gains"]).pin_memory() if wl.known else None
     pil_d, emp_d, noi_d = (t.to(dev) for t in (pil_h, emp_h, noi_h))
+    gain_d = gain_h.to(dev) if gain_h is not None else None
     m = int(host["n_antennas"])
 
     def barrier():
@@ -344,9 +456,13 @@ def ours_arm(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
+    def solve(out):
+        return estimators.psca_run_batch(problem, pil_d, emp_d, noi_d, m, gains=gain_d,
+                                         schedule=wl.schedule, max_iter=iters, out=out)
+
     out = {}
-    for _ in range(args.warmup):
-        out = estimators.psca_run_batch(problem, pil_d, emp_d, noi_d, m, max_iter=iters, out=out)
+    for _ in range(max(args.warmup, 3)):
+        out = solve(out)
     torch.cuda.synchronize()
     peak = fp64_peak_tflops(torch)
 
@@ -354,49 +470,78 @@ def ours_arm(args):
     launches = 0
     barrier()
     torch.cuda.synchronize()
-    device.profile_begin()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record()
         for _ in range(args.steps):
-            out = estimators.psca_run_batch(problem, pil_d, emp_d, noi_d, m, max_iter=iters,
-                                            out=out)
+            out = solve(out)
             launches += out["launches"]
         e1.record()
         torch.cuda.synchronize()
     barrier()
-    prof = device.profile_end()
     ms = max_over_ranks(e0.elapsed_time(e1))
     value = world * B * args.steps / (ms * 1e-3)
-    col_ms = prof["column_ms"] / max(prof["column_launches"], 1)
-    # algorithmic flops of the timed region spread over the column-family launches
-    # (one per iteration, two per iteration when the batch is split over two streams,
-    # one per solve for the persistent kernel)
-    flops_total = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * B * iters * args.steps
-    flops_launch = flops_total / max(prof["column_launches"], 1)
-    achieved = flops_launch / (col_ms * 1e-3) / 1e12
-    # flops the column kernel provably executes on the DMMA pipe: the quadratic
-    # forms alone (lower-triangular k-steps, two matrices, 8-column blocks over
-    # 32-column tiles, m8n8k4 = 512 flops); the rebuild of the moving columns
-    # comes on top, so this is a lower bound on the executed rate
-    nrb = next(r for r in (2, 3, 4, 5, 6, 8, 10, 12, 16, 20) if 4 * r >= cfg.pilot_len)
-    quad_per_inst = 2 * nrb * (nrb + 1) * (-(-cfg.n_devices // 32) * 4) * 512.0
-    quad_launch = quad_per_inst * B * iters * args.steps / max(prof["column_launches"], 1)
-    executed = quad_launch / (col_ms * 1e-3) / 1e12
     x_check = out["x"]
     finite = bool(torch.isfinite(x_check).all().item())
 
+    # ---- roofline of the dominant kernel (untimed passes) -------------------
+    col_ms, n_col, fac_ms, n_fac, col_tot, fac_tot = serial_launch_times(lambda: solve({}))
+    algo_launch = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * B * iters / max(n_col, 1)
+    algo_tflops = algo_launch / (col_ms * 1e-3) / 1e12
+    executed = None
+    if not args.no_executed and out.get("path") != "persistent" and B >= 2 * device.sm_count():
+        ex_launch, quad_share, moving = executed_column_flops(wl, problem, pil_d, emp_d, noi_d,
+                                                              gain_d, m)
+        executed = {"flops_per_launch": ex_launch, "quad_share": quad_share,
+                    "moving_columns_per_iteration": moving}
+    if executed is not None:
+        ach = executed["flops_per_launch"] / (col_ms * 1e-3) / 1e12
+        nrb = next(r for r in (2, 3, 4, 5, 6, 8, 10, 12, 16, 20) if 4 * r >= cfg.pilot_len)
+        roofline = {
+            "bound": "tensor", "kernel": f"column_kernel_w<{nrb}>", "achieved": ach,
+            "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "flops_per_unit": "EXECUTED FP64 DMMA flops (m8n8k4 = 512 flops): 2 NRB(NRB+1) "
+                              "per 8-column block for the quadratic forms + NBLK per pair of "
+                              "moving columns for the rebuild, counted exactly from an "
+                              "iterate-recording pass of the same batch",
+            "executed_flops_per_launch": executed["flops_per_launch"],
+            "quad_share_of_executed": executed["quad_share"],
+            "moving_columns_per_iteration": executed["moving_columns_per_iteration"],
+        }
+    else:
+        roofline = {"bound": "tensor", "kernel": "column_kernel (tile path, chunked instance)",
+                    "achieved": algo_tflops, "peak": peak, "unit": "TFLOP/s",
+                    "frac": algo_tflops / peak,
+                    "flops_per_unit": "algorithmic 24 N L^2 per instance-iteration"}
+    roofline.update({
+        "traffic": ncu_traffic() if wl.name == "c1" else None,
+        "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured live in this run "
+                       "(MEASURED_PEAKS.json has no FP64 entry)",
+        "timing": "serialised: one solve with every launch on one stream (psca_set_serial), "
+                  "CUDA events around each launch; mean column launch time",
+        "column_ms_per_launch": col_ms, "factor_ms_per_launch": fac_ms,
+        "column_launches": n_col, "factor_launches": n_fac,
+        "column_share_serial": col_tot / max(col_tot + fac_tot, 1e-12),
+        "algorithmic_flops_per_launch": algo_launch,
+        "algorithmic_achieved": algo_tflops, "algorithmic_frac": algo_tflops / peak,
+        "algorithmic_note": "24 N L^2 per instance-iteration (SURVEY.md 8(d): the reference's "
+                            "three dense ZGEMMs); the kernel executes fewer flops (Hermitian "
+                            "lower-triangle forms, incremental rebuild over moving columns), so "
+                            "this ratio can exceed 1 and is not a roofline",
+        "dmma_pipe_busy_ncu": ncu_pipe() if wl.name == "c1" else None,
+        "path": out.get("path"),
+    })
+
     # ---- end to end through the public API from pinned host buffers ----------
-    # psca_run_batch_host: chunked H2D on a copy stream overlapped with the solve,
-    # estimates copied back per chunk; all of it inside the timed region
     e2e = None
     if not args.no_e2e:
-        h2d = pil_h.numel() * 16 + emp_h.numel() * 16 + noi_h.numel() * 8
+        h2d = pil_h.numel() * 16 + emp_h.numel() * 16 + noi_h.numel() * 8 + \
+            (gain_h.numel() * 8 if gain_h is not None else 0)
         d2h = B * cfg.n_devices * 8 + 2 * B * 4
 
         def e2e_step():
-            return estimators.psca_run_batch_host(problem, pil_h, emp_h, noi_h, m,
-                                                  max_iter=iters)
+            return estimators.psca_run_batch_host(problem, pil_h, emp_h, noi_h, m, gains=gain_h,
+                                                  schedule=wl.schedule, max_iter=iters)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -418,51 +563,20 @@ def ours_arm(args):
                       "chunk's H2D overlapped with the previous chunk's solve)",
                "x_matches_device_run": bool(torch.equal(r["x"], out["x"].cpu()))}
 
-    line = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(CONFIG_NAME, iters, args.cpu_seconds)
+            cpu = cpu_baseline(wl.name, iters, args.cpu_seconds)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": wl.metric, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE c1 scenes, paper_2503_15259_b200/scenes.py)",
-            "config": config_block(cfg, iters, B),
+            "data": f"synthetic (seeded BASELINE {wl.scene_name} scenes, "
+                    "paper_2503_15259_b200/scenes.py)",
+            "config": wl.config_block(B, world=world),
             "psca_iters_per_s": value * iters,
-            "roofline": {
-                "bound": "tensor", "kernel": "column_kernel", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(),
-                "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured live in this run "
-                               "(MEASURED_PEAKS.json has no FP64 entry)",
-                "algorithmic_flops_per_launch": flops_launch,
-                "flops_per_unit": ALGO_FLOPS_PER_UNIT,
-                "executed_flops_note": "the kernel exploits Hermitian symmetry (lower-triangle "
-                                       "quadratic forms and rebuild) and skips exactly-zero "
-                                       "weights, so it executes fewer flops than the reference's "
-                                       "three dense ZGEMMs; frac > 1 is possible",
-                "executed_quad_flops_per_launch": quad_launch,
-                "executed_quad_tflops": executed,
-                "executed_quad_frac": executed / peak,
-                "executed_note": "DMMA flops of the quadratic forms alone (a lower bound on "
-                                 "what the kernel executes) over the same launch time; ncu "
-                                 "measures the DMMA sub-pipe busy fraction in column_kernel_w<10> (dmma_pipe_busy_ncu, "
-                                 "profiles/README.md)",
-                "overlap_note": "on the split-stream path the column launches of one half "
-                                "batch run concurrently with the other half's factor launches, "
-                                "so each CUDA-event launch duration includes that SM sharing",
-                "column_ms_per_launch": col_ms,
-                "factor_ms_per_launch": prof["factor_ms"] / max(prof["factor_launches"], 1),
-                "column_share": prof["column_ms"] / max(prof["column_ms"] + prof["factor_ms"], 1e-9),
-                "column_share_ncu": ncu_share(),
-                "dmma_pipe_busy_ncu": ncu_pipe(),
-                "share_note": "column_share is from CUDA events on the split streams (each interval "
-                              "also spans the other half's concurrent kernel); column_share_ncu is "
-                              "from the serialised ncu launch list in profiles/ncu_summary.json",
-                "column_launches": prof["column_launches"],
-                "path": out.get("path"),
-            },
+            "ms_per_iteration": ms / args.steps / iters,
+            "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,

@@ -10,7 +10,9 @@
  * Conventions
  *   - every pointer is a DEVICE pointer (cudaMalloc'd or a torch CUDA tensor's
  *     data_ptr) unless the comment says otherwise; complex128 arrays are
- *     interleaved (re, im) doubles, C order, exactly numpy's complex128 layout;
+ *     interleaved (re, im) doubles, C order, exactly numpy's complex128 layout,
+ *     and must be 16-byte aligned (the kernels load them as 16-byte vectors;
+ *     a misaligned complex array or workspace is rejected with PSCA_E_ARG);
  *   - batched arrays carry a leading instance dimension B;
  *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
  *     every call is stream-ordered and re-entrant per stream, allocates
@@ -89,6 +91,12 @@ typedef struct {
     int* status;            /* [B]                                             */
     int* n_iter;            /* [B] completed iterations                        */
     double* cond_est;       /* [B] condition estimate at a Cholesky abort       */
+    /* Fault injection (test seam; the device-side counterpart of the
+     * reference test that monkeypatches CovState.build to raise,
+     * test_estimators.py:268-279): 0 = off; k >= 1 makes the factorisation
+     * that opens iteration k-1 report PSCA_CHOL_FAIL for every instance still
+     * running (cond_est = +inf), exactly as a non-positive pivot would. */
+    int fault_iter;
 } psca_solve_args;
 
 /* Workspace (device bytes) psca_solve needs for these arguments. */
@@ -131,6 +139,64 @@ size_t psca_objective_workspace_bytes(int B, int L);
 int psca_eval_objective(const double* sigma, const double* sigma_inv, const double* emp_cov,
                         int B, int L, double* out, int* status, void* workspace,
                         size_t workspace_bytes, void* stream);
+
+/* Prior terms at x (the solver evaluates the same device code at every
+ * iterate): gradient of the prior penalty and, optionally, its value and the
+ * smoothed density.
+ *   map-k, independent prior:  grad = prior_lin = -log(p/(1-p))/M,
+ *       value = sum prior_lin x        (priors.py:145-158)
+ *   map-k, pairwise MVB prior: grad = -(c1 + c2 x)/M,
+ *       value = -(c1.x + x.(c2 x)/2)/M (priors.py:145-159)
+ *   map-ur: grad = -(1/M) clip(p'/p, +-dzg) with the dead-zone push,
+ *       value = -(1/M) sum log max(p, 1e-300), density = p^eps(x)
+ *                                       (priors.py:313-399)
+ * Replaces priors.log_prior_grad_known / log_prior_value_known /
+ * log_prior_grad_unknown / log_prior_value_unknown / pdf_eff_smooth. */
+typedef struct {
+    int kind;               /* PSCA_MAP_K or PSCA_MAP_UR                        */
+    int B, N, n_antennas;
+    const double* x;        /* [B][N]                                          */
+    const double* prior_lin;/* map-k independent: [N]                          */
+    const double* prior_p;  /* map-ur: [N]                                     */
+    psca_eff_prior eff;     /* map-ur                                          */
+    const double* prior_c1; /* map-k pairwise: [N] and CSR c2, else all 0      */
+    const int* prior_c2_indptr;
+    const int* prior_c2_indices;
+    const double* prior_c2_data;
+    double* grad;           /* [B][N]                                          */
+    double* value;          /* [B] or 0                                        */
+    double* density;        /* map-ur: [B][N] or 0                             */
+} psca_prior_args;
+
+int psca_prior_terms(const psca_prior_args* a, void* stream);
+
+/* One PSCA coordinate step from the quadratic forms at x (the column-kernel
+ * epilogue as a standalone call): q-floor guard, gradient, surrogate
+ * coefficient, clipped coordinate minimiser and the relaxed update
+ *   grad = g (q - r) [known] or (q - r) [unknown], + prior_grad (map kinds)
+ *   coef = (g q)^2 [known] or q^2 [unknown]
+ *   cand = clip(x - grad / coef, 0, hi)
+ *   x_new = (1 - rho) x + rho cand,  update_norm = ||x_new - x||_2
+ *   status = PSCA_QFLOOR if min q < 0.5 L / ||Sigma||_F (sigma given), else 0
+ * (estimators.py:176-200, 233-236, 267-284).  Every output may be 0. */
+typedef struct {
+    int kind, B, N, L;
+    double rho, hi;         /* step and upper box bound (bounds_for)            */
+    const double* x;        /* [B][N]                                          */
+    const double* q;        /* [B][N]                                          */
+    const double* r;        /* [B][N]                                          */
+    const double* gains;    /* [B][N] (known-pathloss kinds)                   */
+    const double* prior_grad; /* [B][N] (map kinds) or 0                       */
+    const double* sigma;    /* [B][L][L] complex128 (q-floor guard) or 0       */
+    double* grad;           /* [B][N]                                          */
+    double* coef;           /* [B][N]                                          */
+    double* cand;           /* [B][N]                                          */
+    double* x_new;          /* [B][N]                                          */
+    double* update_norm;    /* [B]                                             */
+    int* status;            /* [B]                                             */
+} psca_coord_args;
+
+int psca_coord_step(const psca_coord_args* a, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Large pilot length (L <= 256; BASELINE config 4: N = 100,000, L = 256) as a
@@ -225,6 +291,18 @@ int psca_last_path(void);
 int psca_profile_begin(void);
 int psca_profile_end(double* column_ms, int* column_launches, double* factor_ms,
                      int* factor_launches);
+
+/* on = 1: subsequent psca_solve calls on this thread issue every launch on
+ * the caller's stream (no half-batch split over internal streams), so the
+ * per-launch profile times are serialised kernel times; 0 restores the
+ * default.  Results are identical either way. */
+int psca_set_serial(int on);
+
+/* Per-launch device times (ms) and kinds (0 column, 1 factor) of the
+ * launches recorded since psca_profile_begin, in launch order (first `cap`
+ * entries; synchronises on them).  Returns the number recorded, or a negative
+ * PSCA_E* code.  Call before psca_profile_end, which clears the record. */
+int psca_profile_launches(double* ms, int* kinds, int cap);
 
 /* Description of the last CUDA error a call on this thread reported. */
 const char* psca_last_error(void);

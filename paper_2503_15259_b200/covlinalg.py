@@ -60,8 +60,30 @@ def frobenius_inverse(sigma: np.ndarray) -> np.ndarray:
     """
     inv, status, cond, _ = device.hpd_inverse(np.asarray(sigma, dtype=complex))
     if int(status) != 0:
-        raise ConditioningError("Sigma is numerically singular", float(cond))
+        raise conditioning_error(sigma)
     return inv
+
+
+def conditioning_error(sigma) -> ConditioningError:
+    """The ConditioningError the reference raises for this singular Sigma
+    (covlinalg.py:78-88, 104-110): which real SPD factor fails Cholesky --
+    Re(Sigma), or A + B A^-1 B -- and the eigenvalue-ratio condition estimate
+    of that factor.  Error path only (never on the solve path): it runs after a
+    device factorisation has reported a non-positive pivot, on the GPU through
+    torch.linalg (cuSOLVER)."""
+    torch = device._torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S = torch.as_tensor(np.asarray(sigma, dtype=complex), device=dev)
+    a, b = S.real.contiguous(), S.imag.contiguous()
+
+    def cond(m):
+        e = torch.linalg.eigvalsh((m + m.T) / 2.0)
+        return float("inf") if float(e[0]) <= 0.0 else float(e[-1] / e[0])
+
+    if not bool(torch.any(b != 0)) or int(torch.linalg.cholesky_ex(a).info) != 0:
+        return ConditioningError("Re(Sigma) is numerically singular", cond(a))
+    c = a + b @ torch.linalg.solve(a, b)
+    return ConditioningError("A + B A^-1 B is numerically singular", cond(c))
 
 
 def quad_forms(pilots: np.ndarray, sigma_inv: np.ndarray, emp_cov: np.ndarray,
@@ -94,3 +116,8 @@ class CovState:
         sigma_inv = frobenius_inverse(sigma)
         q, r = quad_forms(pilots, sigma_inv, emp_cov)
         return cls(sigma=sigma, sigma_inv=sigma_inv, q=q, r=r)
+
+
+# the library's own CovState.build; estimators.psca_run(engine="auto") runs the
+# components engine when this has been replaced (the reference test seam)
+NATIVE_BUILD = CovState.__dict__["build"]

@@ -34,6 +34,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "psca.h"
@@ -1196,6 +1198,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
 #include "psca_wcol.cuh"
 #include "psca_large.cuh"
 #include "psca_bcd.cuh"
+#include "psca_components.cuh"
 
 // ---------------------------------------------------------------------------
 // empirical covariance (HERK): Sigma_hat = Y Y^H / M
@@ -1540,38 +1543,67 @@ cudaError_t launch_factor(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+thread_local bool g_serial = false;   // psca_set_serial
+
 bool split_disabled() {
     static const bool off = [] {
         const char* e = getenv("PSCA_NO_SPLIT");
         return e && e[0] == '1';
     }();
-    return off;
+    return off || g_serial;
 }
 
-// two non-blocking side streams + fork/join events per device (created once)
-cudaError_t side_streams(cudaStream_t (&ss)[2], cudaEvent_t* fork, cudaEvent_t (&join)[2]) {
-    struct Side {
-        bool init = false;
-        cudaStream_t s[2];
-        cudaEvent_t f, j[2];
-    };
-    static Side sides[64];
+// Two non-blocking side streams per (device, caller stream), created once
+// under a mutex; solves issued on different caller streams get different side
+// streams, so they neither serialise nor share fork/join events.  The events
+// are created per call (and released when they complete), so concurrent calls
+// can never re-record an event another call is about to wait on.
+struct SideKey {
+    int dev;
+    cudaStream_t st;
+    bool operator<(const SideKey& o) const { return dev != o.dev ? dev < o.dev : st < o.st; }
+};
+struct SidePair {
+    cudaStream_t s[2];
+};
+std::mutex g_side_mu;
+std::map<SideKey, SidePair> g_side;
+
+cudaError_t side_streams(cudaStream_t caller, cudaStream_t (&ss)[2]) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    Side& sd = sides[dev & 63];
-    if (!sd.init) {
-        for (int h = 0; h < 2; ++h) {
-            if ((e = cudaStreamCreateWithFlags(&sd.s[h], cudaStreamNonBlocking)) != cudaSuccess) return e;
-            if ((e = cudaEventCreateWithFlags(&sd.j[h], cudaEventDisableTiming)) != cudaSuccess) return e;
-        }
-        if ((e = cudaEventCreateWithFlags(&sd.f, cudaEventDisableTiming)) != cudaSuccess) return e;
-        sd.init = true;
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    auto it = g_side.find({dev, caller});
+    if (it == g_side.end()) {
+        SidePair p;
+        for (int h = 0; h < 2; ++h)
+            if ((e = cudaStreamCreateWithFlags(&p.s[h], cudaStreamNonBlocking)) != cudaSuccess) return e;
+        it = g_side.emplace(SideKey{dev, caller}, p).first;
     }
-    ss[0] = sd.s[0]; ss[1] = sd.s[1];
-    *fork = sd.f;
-    join[0] = sd.j[0]; join[1] = sd.j[1];
+    ss[0] = it->second.s[0];
+    ss[1] = it->second.s[1];
     return cudaSuccess;
+}
+
+// record on `from`, make `to` wait; the event is destroyed right away (the
+// runtime releases it once the recorded work completes)
+cudaError_t stream_edge(cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(ev, from)) == cudaSuccess) e = cudaStreamWaitEvent(to, ev, 0);
+    cudaEventDestroy(ev);
+    return e;
+}
+
+// fault seam of psca_solve: after the factor launch with k_new == fault_iter - 1
+cudaError_t maybe_fault(const psca_solve_args* a, int k_new, int* status, double* cond_est, int B,
+                        cudaStream_t st) {
+    if (a->fault_iter <= 0 || k_new != a->fault_iter - 1) return cudaSuccess;
+    fault_kernel<<<(B + 127) / 128, 128, 0, st>>>(status, cond_est, B);
+    ++g_launches;
+    return cudaGetLastError();
 }
 
 // views of instances [b0, b0 + Bh) of a solve (single chunk per instance)
@@ -1641,6 +1673,8 @@ SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, v
     return s;
 }
 
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 int check_solve_args(const psca_solve_args* a) {
     if (!a || a->B < 0 || a->N < 1 || a->L < 1 || a->max_iter < 0) return PSCA_E_ARG;
     if (a->kind < PSCA_ML_K || a->kind > PSCA_MAP_UR) return PSCA_E_ARG;
@@ -1649,6 +1683,7 @@ int check_solve_args(const psca_solve_args* a) {
     if (a->B == 0) return PSCA_OK;   // empty batch: nothing is read or written
     if (!a->pilots || !a->emp_cov || !a->noise || !a->x_out || !a->status || !a->n_iter)
         return PSCA_E_ARG;
+    if (!aligned16(a->pilots) || !aligned16(a->emp_cov)) return PSCA_E_ARG;
     if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
     if (a->kind == PSCA_MAP_K) {
         const bool pair = a->prior_c2_indptr || a->prior_c2_indices || a->prior_c2_data ||
@@ -1753,6 +1788,7 @@ int check_large_args(const psca_large_args* a) {
     if (!a->pilots || !a->emp_cov || !a->x_a || !a->x_b || !a->status || !a->n_iter ||
         !a->steps || !a->update_norm || !(a->noise > 0))
         return PSCA_E_ARG;
+    if (!aligned16(a->pilots) || !aligned16(a->emp_cov)) return PSCA_E_ARG;
     if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
     if (a->kind == PSCA_MAP_K && !a->prior_lin) return PSCA_E_ARG;
     if (a->kind == PSCA_MAP_UR && !a->prior_p) return PSCA_E_ARG;
@@ -1829,6 +1865,26 @@ int psca_profile_end(double* column_ms, int* column_launches, double* factor_ms,
     return PSCA_OK;
 }
 
+int psca_set_serial(int on) {
+    g_serial = on != 0;
+    return PSCA_OK;
+}
+
+int psca_profile_launches(double* ms, int* kinds, int cap) {
+    int n = 0;
+    for (const ProfRec& r : g_prof.recs) {
+        if (n < cap) {
+            if (cudaEventSynchronize(r.b) != cudaSuccess) return PSCA_E_CUDA;
+            float t = 0.f;
+            if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return PSCA_E_CUDA;
+            if (ms) ms[n] = t;
+            if (kinds) kinds[n] = r.kind;
+        }
+        ++n;
+    }
+    return n;
+}
+
 size_t psca_solve_workspace_bytes(const psca_solve_args* a) {
     if (check_solve_args(a) != PSCA_OK) return 0;
     Geo g = make_geo(a->L, solve_nrb(a->L));
@@ -1844,6 +1900,7 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     const int n_chunks = resolved_chunks(a);
     SolveLayout lay = solve_layout(a, g, n_chunks, workspace);
     if (workspace_bytes < lay.total || (!workspace && lay.total)) return PSCA_E_WORKSPACE;
+    if (!aligned16(workspace)) return PSCA_E_ARG;
     if (a->B == 0) return PSCA_OK;
     const size_t BN = (size_t)a->B * a->N;
 
@@ -1902,7 +1959,7 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     double* xn = lay.x_alt;
     // persistent path: whole instances per CTA (one chunk), enough instances
     // to fill every SM twice, a compiled persistent shape
-    const bool persistent = !generic_forced() && !persistent_disabled() &&
+    const bool persistent = a->fault_iter <= 0 && !generic_forced() && !persistent_disabled() &&
                             persistent_shape(g.NRB) && n_chunks == 1 &&
                             (a->n_chunks == 1 || a->B >= 2 * sm_count());
     g_last_path = persistent ? 1 : 0;
@@ -1918,8 +1975,7 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     if (split) {
         g_last_path = 2;
         cudaStream_t ss[2];
-        cudaEvent_t ev_fork, ev_join[2];
-        if (!ok_or_record(side_streams(ss, &ev_fork, ev_join))) return PSCA_E_CUDA;
+        if (!ok_or_record(side_streams(st, ss))) return PSCA_E_CUDA;
         const int Bh[2] = {a->B / 2, a->B - a->B / 2};
         const int b0[2] = {0, a->B / 2};
         ColArgs ch[2];
@@ -1928,12 +1984,13 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
             ch[h] = sub_col(ca, b0[h], Bh[h], g);
             fh[h] = sub_fac(fa, b0[h], Bh[h], g);
         }
-        cudaEventRecord(ev_fork, st);
-        for (int h = 0; h < 2; ++h) cudaStreamWaitEvent(ss[h], ev_fork, 0);
+        for (int h = 0; h < 2; ++h)
+            if (!ok_or_record(stream_edge(st, ss[h]))) return PSCA_E_CUDA;
         for (int h = 0; h < 2; ++h) {
             FacArgs f = fh[h];
             f.k_new = 0; f.x_cur = xc + (size_t)b0[h] * a->N; f.x_next = xn + (size_t)b0[h] * a->N;
             if (!ok_or_record(launch_solve_factor(f, g, ss[h]))) return PSCA_E_CUDA;
+            if (!ok_or_record(maybe_fault(a, 0, f.status, f.cond_est, Bh[h], ss[h]))) return PSCA_E_CUDA;
         }
         for (int k = 0; k < a->max_iter; ++k) {
             for (int h = 0; h < 2; ++h) {
@@ -1946,21 +2003,24 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
                 f.k_new = k + 1; f.x_cur = xc + (size_t)b0[h] * a->N;
                 f.x_next = xn + (size_t)b0[h] * a->N;
                 if (!ok_or_record(launch_solve_factor(f, g, ss[h]))) return PSCA_E_CUDA;
+                if (!ok_or_record(maybe_fault(a, k + 1, f.status, f.cond_est, Bh[h], ss[h])))
+                    return PSCA_E_CUDA;
             }
             double* t = xc; xc = xn; xn = t;
         }
-        for (int h = 0; h < 2; ++h) {
-            cudaEventRecord(ev_join[h], ss[h]);
-            cudaStreamWaitEvent(st, ev_join[h], 0);
-        }
+        for (int h = 0; h < 2; ++h)
+            if (!ok_or_record(stream_edge(ss[h], st))) return PSCA_E_CUDA;
     } else {
         fa.k_new = 0; fa.x_cur = xc; fa.x_next = xn;
         if (!ok_or_record(launch_solve_factor(fa, g, st))) return PSCA_E_CUDA;
+        if (!ok_or_record(maybe_fault(a, 0, a->status, a->cond_est, a->B, st))) return PSCA_E_CUDA;
         for (int k = 0; k < a->max_iter; ++k) {
             ca.k = k; ca.x_cur = xc; ca.x_next = xn;
             if (!ok_or_record(launch_solve_column(ca, g, n_chunks, st))) return PSCA_E_CUDA;
             fa.k_new = k + 1; fa.x_cur = xc; fa.x_next = xn;
             if (!ok_or_record(launch_solve_factor(fa, g, st))) return PSCA_E_CUDA;
+            if (!ok_or_record(maybe_fault(a, k + 1, a->status, a->cond_est, a->B, st)))
+                return PSCA_E_CUDA;
             double* t = xc; xc = xn; xn = t;
         }
     }
@@ -2128,6 +2188,44 @@ int psca_eval_objective(const double* sigma, const double* sigma_inv, const doub
     if (launch_factor<FAC_OBJECTIVE>(fa, g, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return PSCA_E_CUDA;
     return PSCA_OK;
+}
+
+int psca_prior_terms(const psca_prior_args* a, void* stream) {
+    if (!a || a->B < 0 || a->N < 1 || a->n_antennas < 1) return PSCA_E_ARG;
+    if (a->kind != PSCA_MAP_K && a->kind != PSCA_MAP_UR) return PSCA_E_ARG;
+    if (a->B == 0) return PSCA_OK;
+    if (!a->x || !a->grad) return PSCA_E_ARG;
+    const bool pair = a->kind == PSCA_MAP_K && a->prior_c2_indptr;
+    if (pair && !(a->prior_c1 && a->prior_c2_indices && a->prior_c2_data)) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_K && !pair && !a->prior_lin) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_UR && !a->prior_p) return PSCA_E_ARG;
+    g_launches = 0;
+    FacArgs fa{};
+    fa.B = a->B; fa.N = a->N; fa.kind = a->kind; fa.n_antennas = a->n_antennas;
+    fa.record_objective = a->value ? 1 : 0;
+    fa.prior_lin = a->prior_lin; fa.prior_p = a->prior_p; fa.eff = a->eff; fa.pgrad = a->grad;
+    if (pair) {
+        fa.c1 = a->prior_c1; fa.c2_ptr = a->prior_c2_indptr; fa.c2_idx = a->prior_c2_indices;
+        fa.c2_val = a->prior_c2_data;
+    }
+    prior_terms_kernel<<<a->B, NT, 0, static_cast<cudaStream_t>(stream)>>>(fa, a->x, a->value,
+                                                                             a->density);
+    ++g_launches;
+    return ok_or_record(cudaGetLastError()) ? PSCA_OK : PSCA_E_CUDA;
+}
+
+int psca_coord_step(const psca_coord_args* a, void* stream) {
+    if (!a || a->B < 0 || a->N < 1 || a->L < 1) return PSCA_E_ARG;
+    if (a->kind < PSCA_ML_K || a->kind > PSCA_MAP_UR) return PSCA_E_ARG;
+    if (!(a->rho > 0.0 && a->rho <= 1.0) || !(a->hi >= 0.0)) return PSCA_E_ARG;
+    if (a->B == 0) return PSCA_OK;
+    if (!a->x || !a->q || !a->r) return PSCA_E_ARG;
+    if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
+    if (a->sigma && !aligned16(a->sigma)) return PSCA_E_ARG;
+    g_launches = 0;
+    coord_step_kernel<<<a->B, NT, 0, static_cast<cudaStream_t>(stream)>>>(*a);
+    ++g_launches;
+    return ok_or_record(cudaGetLastError()) ? PSCA_OK : PSCA_E_CUDA;
 }
 
 size_t psca_large_workspace_bytes(const psca_large_args* a) {

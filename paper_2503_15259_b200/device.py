@@ -47,6 +47,31 @@ class SolveArgsC(ctypes.Structure):
         ("x_out", ctypes.c_void_p), ("update_norm", ctypes.c_void_p),
         ("objective", ctypes.c_void_p), ("iterates", ctypes.c_void_p),
         ("status", ctypes.c_void_p), ("n_iter", ctypes.c_void_p), ("cond_est", ctypes.c_void_p),
+        ("fault_iter", ctypes.c_int),
+    ]
+
+
+class PriorArgsC(ctypes.Structure):
+    """psca_prior_args (include/psca.h)."""
+    _fields_ = [
+        ("kind", ctypes.c_int), ("B", ctypes.c_int), ("N", ctypes.c_int),
+        ("n_antennas", ctypes.c_int), ("x", ctypes.c_void_p), ("prior_lin", ctypes.c_void_p),
+        ("prior_p", ctypes.c_void_p), ("eff", EffPriorC), ("prior_c1", ctypes.c_void_p),
+        ("prior_c2_indptr", ctypes.c_void_p), ("prior_c2_indices", ctypes.c_void_p),
+        ("prior_c2_data", ctypes.c_void_p), ("grad", ctypes.c_void_p),
+        ("value", ctypes.c_void_p), ("density", ctypes.c_void_p),
+    ]
+
+
+class CoordArgsC(ctypes.Structure):
+    """psca_coord_args (include/psca.h)."""
+    _fields_ = [
+        ("kind", ctypes.c_int), ("B", ctypes.c_int), ("N", ctypes.c_int), ("L", ctypes.c_int),
+        ("rho", ctypes.c_double), ("hi", ctypes.c_double),
+        ("x", ctypes.c_void_p), ("q", ctypes.c_void_p), ("r", ctypes.c_void_p),
+        ("gains", ctypes.c_void_p), ("prior_grad", ctypes.c_void_p), ("sigma", ctypes.c_void_p),
+        ("grad", ctypes.c_void_p), ("coef", ctypes.c_void_p), ("cand", ctypes.c_void_p),
+        ("x_new", ctypes.c_void_p), ("update_norm", ctypes.c_void_p), ("status", ctypes.c_void_p),
     ]
 
 
@@ -72,6 +97,9 @@ _SIGS = {
     "psca_profile_begin": (ctypes.c_int, []),
     "psca_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
+    "psca_set_serial": (ctypes.c_int, [ctypes.c_int]),
+    "psca_profile_launches": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
+                                             ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
     "psca_solve_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(SolveArgsC)]),
     "psca_solve": (ctypes.c_int, [ctypes.POINTER(SolveArgsC), ctypes.c_void_p, ctypes.c_size_t,
                                   ctypes.c_void_p]),
@@ -93,6 +121,8 @@ _SIGS = {
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.c_void_p]),
     "psca_bcd_sweep": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "psca_prior_terms": (ctypes.c_int, [ctypes.POINTER(PriorArgsC), ctypes.c_void_p]),
+    "psca_coord_step": (ctypes.c_int, [ctypes.POINTER(CoordArgsC), ctypes.c_void_p]),
     "psca_objective_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int]),
     "psca_eval_objective": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
@@ -176,7 +206,7 @@ def eff_prior_struct(prior) -> EffPriorC:
 def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=None,
           prior_lin=None, prior_p=None, eff_prior=None, prior_c1=None, prior_c2=None,
           max_iter: int | None = None, tol: float = 0.0, record_objective: bool = False,
-          record_iterates: bool = False, n_chunks: int = 0, out=None):
+          record_iterates: bool = False, n_chunks: int = 0, out=None, fault_iter: int = 0):
     """Run the batched PSCA solve on the current CUDA device / stream.
 
     pilots (B,L,N) complex128, emp_cov (B,L,L) complex128, noise (B,) float64,
@@ -186,7 +216,8 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
     Inputs may be numpy arrays or torch tensors (moved to the device if
     needed).  Returns a dict of device tensors: x (B,N), update_norm (B,T),
     objective (B,T) or None, iterates (B,T+1,N) or None, status (B,) int32,
-    n_iter (B,) int32, cond_est (B,).
+    n_iter (B,) int32, cond_est (B,).  ``fault_iter`` = k >= 1 forces the
+    factorisation opening iteration k-1 to fail (the test seam of psca.h).
     """
     torch = _torch()
     lib = load()
@@ -242,7 +273,7 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
         x_out=x.data_ptr(), update_norm=un.data_ptr(),
         objective=obj.data_ptr() if obj is not None else 0,
         iterates=its.data_ptr() if its is not None else 0, status=status.data_ptr(),
-        n_iter=n_iter.data_ptr(), cond_est=cond.data_ptr())
+        n_iter=n_iter.data_ptr(), cond_est=cond.data_ptr(), fault_iter=int(fault_iter))
     nbytes = lib.psca_solve_workspace_bytes(ctypes.byref(args))
     if nbytes == 0 and B > 0:
         raise PscaNativeError("psca_solve rejected the arguments (shape/kind/pointers)")
@@ -336,6 +367,69 @@ def eval_objective_t(X, P, E):
     return out, status
 
 
+def prior_terms_t(kind: str, X, n_antennas: int, *, prior_lin=None, prior_p=None,
+                  eff_prior=None, prior_c1=None, prior_c2=None, want_value=False,
+                  want_density=False):
+    """Prior gradient (B,N) [, value (B,)] [, density (B,N)] at device iterates X (B,N)."""
+    torch = _torch()
+    lib = load()
+    dev = X.device
+    B, N = X.shape
+    X = X.to(torch.float64).contiguous()
+    keep = []
+
+    def t(a, dt=torch.float64):
+        if a is None:
+            return 0
+        v = _dev(torch, a, dt, dev)
+        keep.append(v)
+        return v.data_ptr()
+
+    grad = torch.empty((B, N), dtype=torch.float64, device=dev)
+    val = torch.empty(B, dtype=torch.float64, device=dev) if want_value else None
+    dens = torch.empty((B, N), dtype=torch.float64, device=dev) if want_density else None
+    c2 = prior_c2 if prior_c2 is not None else (None, None, None)
+    if prior_c2 is not None and len(c2[1]) == 0:   # keep valid pointers, empty interaction
+        c2 = (c2[0], np.zeros(1, np.int32), np.zeros(1))
+    args = PriorArgsC(kind=KIND_CODES[kind], B=B, N=N, n_antennas=int(n_antennas),
+                      x=X.data_ptr(), prior_lin=t(prior_lin), prior_p=t(prior_p),
+                      eff=eff_prior_struct(eff_prior), prior_c1=t(prior_c1),
+                      prior_c2_indptr=t(c2[0], torch.int32), prior_c2_indices=t(c2[1], torch.int32),
+                      prior_c2_data=t(c2[2]), grad=grad.data_ptr(),
+                      value=val.data_ptr() if val is not None else 0,
+                      density=dens.data_ptr() if dens is not None else 0)
+    _check(lib.psca_prior_terms(ctypes.byref(args), _stream(torch)), "psca_prior_terms")
+    return grad, val, dens
+
+
+def coord_step_t(kind: str, X, Q, R, rho: float, hi: float, *, gains=None, prior_grad=None,
+                 sigma=None):
+    """One coordinate step on device tensors (B,N): returns a dict with grad, coef, cand,
+    x_new (B,N), update_norm (B,) and status (B,) (PSCA_QFLOOR when sigma is given and
+    the q-floor guard trips)."""
+    torch = _torch()
+    lib = load()
+    dev = X.device
+    B, N = X.shape
+    L = int(sigma.shape[-1]) if sigma is not None else 1
+    ins = [v.to(torch.float64).contiguous() if v is not None else None
+           for v in (X, Q, R, gains, prior_grad)]
+    sg = sigma.to(torch.complex128).contiguous() if sigma is not None else None
+    out = {k: torch.empty((B, N), dtype=torch.float64, device=dev)
+           for k in ("grad", "coef", "cand", "x_new")}
+    out["update_norm"] = torch.empty(B, dtype=torch.float64, device=dev)
+    out["status"] = torch.empty(B, dtype=torch.int32, device=dev)
+    args = CoordArgsC(kind=KIND_CODES[kind], B=B, N=N, L=L, rho=float(rho), hi=float(hi),
+                      x=ins[0].data_ptr(), q=ins[1].data_ptr(), r=ins[2].data_ptr(),
+                      gains=ins[3].data_ptr() if ins[3] is not None else 0,
+                      prior_grad=ins[4].data_ptr() if ins[4] is not None else 0,
+                      sigma=sg.data_ptr() if sg is not None else 0,
+                      **{k: out[k].data_ptr() for k in ("grad", "coef", "cand", "x_new",
+                                                        "update_norm", "status")})
+    _check(lib.psca_coord_step(ctypes.byref(args), _stream(torch)), "psca_coord_step")
+    return out
+
+
 _SM_COUNT = {}
 
 
@@ -412,6 +506,25 @@ def profile_end() -> dict:
                                    ctypes.byref(fn)), "psca_profile_end")
     return {"column_ms": cms.value, "column_launches": cn.value, "factor_ms": fms.value,
             "factor_launches": fn.value}
+
+
+def set_serial(on: bool) -> None:
+    """Issue every launch of later solves on the caller's stream (serialised profiling)."""
+    _check(load().psca_set_serial(int(bool(on))), "psca_set_serial")
+
+
+def profile_launches() -> list:
+    """[(kind, ms)] of every launch recorded since profile_begin (0 column, 1 factor)."""
+    lib = load()
+    n = lib.psca_profile_launches(None, None, 0)
+    if n < 0:
+        _check(n, "psca_profile_launches")
+    ms = (ctypes.c_double * max(n, 1))()
+    kinds = (ctypes.c_int * max(n, 1))()
+    rc = lib.psca_profile_launches(ms, kinds, n)
+    if rc < 0:
+        _check(rc, "psca_profile_launches")
+    return [(kinds[i], ms[i]) for i in range(n)]
 
 
 def version() -> str:

@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import device, priors
+from . import covlinalg, device, priors
 from .sysmodel import DomainError
 
 KINDS = ("ml-k", "map-k", "ml-ud", "map-ur")
@@ -132,8 +132,9 @@ class StepSchedule:
 class DetectorTrace:
     """Per-iteration record of one run (estimators.py:131-164).
 
-    wall_times: the solve is one device call, so each entry is the mean
-    device time per iteration of that call (CUDA events).
+    wall_times: device time of each iteration's kernels (the factorisation
+    that opens it plus its column pass), from CUDA events recorded around
+    every launch of the solve (psca_profile_launches).
     """
 
     iterates: list = field(default_factory=list)
@@ -185,6 +186,149 @@ def prior_arrays(problem, n_devices: int, n_antennas: int) -> dict:
     return {}
 
 
+def _iteration_times(launch_times, k_done: int, fallback: float) -> list:
+    """Per-iteration device seconds from the solve's launch record: iteration k =
+    the factor launch that opens it + its column launch (launch order: factor 0,
+    then column k, factor k+1 for every k)."""
+    if launch_times and len(launch_times) >= 2 * k_done + 1 and launch_times[0][0] == 1:
+        out = []
+        for k in range(k_done):
+            (kf, tf), (kc, tc) = launch_times[2 * k], launch_times[2 * k + 1]
+            if kf != 1 or kc != 0:
+                return [fallback] * k_done
+            out.append((tf + tc) * 1e-3)
+        return out
+    return [fallback] * k_done
+
+
+def _conditioning_message(problem, sample, x, cond) -> str:
+    """The reference's abort text for a failed factorisation at iterate x
+    (covlinalg.py:78-88 via estimators.py:263-266)."""
+    try:
+        import torch
+        xt = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
+        w = xt.cpu().numpy() * (np.asarray(sample.gains) if problem.known_pathloss else 1.0)
+        sigma = covlinalg.cov_unknown(sample.pilots, w, sample.noise_power)
+        return str(covlinalg.conditioning_error(sigma))
+    except Exception:   # pragma: no cover - message only
+        return str(covlinalg.ConditioningError("Re(Sigma) is numerically singular",
+                                               float(cond)))
+
+
+def _components_engine(engine: str) -> bool:
+    if engine not in ("auto", "fused", "components"):
+        raise DomainError(f"unknown engine {engine!r}")
+    if engine == "auto":
+        return covlinalg.CovState.__dict__.get("build") is not covlinalg.NATIVE_BUILD
+    return engine == "components"
+
+
+def _psca_run_components(problem, sample, steps, n_steps, tol, record_objective, trace,
+                         max_iter, schedule):
+    """The reference loop (estimators.py:239-289) over the component entry points."""
+    import torch
+    n = sample.n_devices
+    x = np.zeros(n)
+    lo, hi = bounds_for(problem, sample)
+    pilots_conj = np.asarray(sample.pilots).conj()
+    trace.iterates.append(x.copy())
+    for k in range(n_steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        try:
+            state = build_state(problem, x, sample, pilots_conj)
+        except covlinalg.ConditioningError as exc:
+            trace.meta["abort"] = str(exc)
+            trace.final = x.copy()
+            return trace
+        step = _coord_step(problem, x, state, sample, float(steps[k]), hi, guard=True)
+        e1.record()
+        if int(step["status"][0].item()) == device.STATUS_QFLOOR:
+            trace.meta["abort"] = ABORT_QFLOOR
+            trace.final = x.copy()
+            return trace
+        x_new = step["x_new"][0].cpu().numpy()
+        if record_objective:
+            trace.objective.append(objective_value(problem, x, sample, state))
+        torch.cuda.synchronize()
+        trace.wall_times.append(e0.elapsed_time(e1) * 1e-3)
+        trace.update_norm.append(float(step["update_norm"][0].item()))
+        x = x_new
+        trace.iterates.append(x.copy())
+        if trace.update_norm[-1] < tol:
+            break
+    if schedule.steps is not None and len(schedule.steps) < max_iter and \
+            trace.n_iterations == n_steps:
+        raise IndexError("explicit schedule shorter than max_iter")
+    trace.final = x.copy()
+    return trace
+
+
+def _prior_kwargs(problem, n: int, n_antennas: int) -> dict:
+    kind, kw = priors._device_prior_args(problem.prior, n, n_antennas)
+    return kw
+
+
+def _coord_step(problem, x, state, sample, rho: float, hi: float, guard: bool = False):
+    """psca_coord_step at x from a CovState (device); returns device tensors."""
+    torch = device._torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    as_d = (lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev).reshape(1, -1))  # noqa: E731
+    n = x.shape[-1]
+    X, Q, R = as_d(np.asarray(x, float)), as_d(state.q), as_d(state.r)
+    g = as_d(np.asarray(sample.gains, float)) if problem.known_pathloss else None
+    pg = None
+    if problem.kind in ("map-k", "map-ur"):
+        if problem.kind == "map-ur":
+            priors._check_range(x, problem.prior)
+        pg, _, _ = device.prior_terms_t(problem.kind, X, sample.n_antennas,
+                                        **_prior_kwargs(problem, n, sample.n_antennas))
+    sig = (torch.as_tensor(np.ascontiguousarray(state.sigma), device=dev)[None]
+           if guard else None)
+    return device.coord_step_t(problem.kind, X, Q, R, rho,
+                               hi if np.isfinite(hi) else np.finfo(float).max,
+                               gains=g, prior_grad=pg, sigma=sig)
+
+
+def gradient(problem, x, state, gains, n_antennas: int) -> np.ndarray:
+    """Objective gradient at x from the covariance state built there (estimators.py:176-186):
+    g (q - r) [known] or q - r [unknown] plus the prior term, on the device."""
+    from types import SimpleNamespace
+    smp = SimpleNamespace(gains=gains, n_antennas=n_antennas)
+    out = _coord_step(problem, np.asarray(x, float), state, smp, 1.0, np.finfo(float).max)
+    return out["grad"][0].cpu().numpy()
+
+
+def objective_value(problem, x, sample, state) -> float:
+    """Covariance fit plus the prior penalty (estimators.py:203-211), on the device."""
+    val = covlinalg.eval_objective(state.sigma, state.sigma_inv, sample.emp_cov)
+    if problem.kind == "map-k":
+        val += priors.log_prior_value_known(x, problem.prior, sample.n_antennas)
+    elif problem.kind == "map-ur":
+        val += priors.log_prior_value_unknown(x, problem.prior, sample.n_antennas)
+    return val
+
+
+def _cov_weights(problem, x, gains) -> np.ndarray:
+    """x g (known pathloss) or x (estimators.py:214-215)."""
+    return x * gains if problem.known_pathloss else x
+
+
+def build_state(problem, x, sample, pilots_conj=None):
+    """CovState at x (estimators.py:218-222): Sigma, Sigma^-1, q, r on the GPU."""
+    weights = _cov_weights(problem, np.asarray(x, float), sample.gains)
+    return covlinalg.CovState.build(sample.pilots, weights, sample.noise_power, sample.emp_cov,
+                                    pilots_conj)
+
+
+def stationarity_residual(problem, x, sample) -> float:
+    """||x - clip(x - grad, lo, hi)||_inf, the projected-gradient residual (estimators.py:225-230)."""
+    state = build_state(problem, x, sample)
+    grad = gradient(problem, x, state, sample.gains, sample.n_antennas)
+    lo, hi = bounds_for(problem, sample)
+    return float(np.max(np.abs(x - np.clip(x - grad, lo, hi))))
+
+
 ABORT_COND = "Sigma is numerically singular (estimated condition number {:.3e})"
 # The compiled / generic batched kernels cover L <= 128; larger pilot lengths
 # (BASELINE config 4: L = 256) run the GEMM-tiled step loop of large.py.
@@ -200,13 +344,24 @@ def use_large_path(pilot_len: int) -> bool:
 
 
 def psca_run(problem, sample, schedule: StepSchedule | None = None, max_iter: int = 30,
-             tol: float = 1e-4, record_objective: bool = True) -> DetectorTrace:
+             tol: float = 1e-4, record_objective: bool = True, *, engine: str = "auto",
+             fault_iter: int = 0) -> DetectorTrace:
     """Run the PSCA iteration from the all-zero start on the GPU (estimators.py:239-289).
 
     Same stopping rules and trace contents as the reference: stops at
     max_iter or when the update norm drops below tol; a singular covariance
     or a q-floor violation ends the run with ``meta["abort"]`` set and
     ``final`` = the last accepted iterate.
+
+    engine: "fused" -- the whole loop in one device call (psca_solve, the
+    product path); "components" -- the reference's loop structure, one
+    ``build_state`` (cov_unknown, frobenius_inverse, quad_forms on the GPU) and
+    one ``psca_coord_step`` per iteration; "auto" (default) -- fused, unless
+    ``covlinalg.CovState.build`` has been replaced (the reference test seam
+    test_estimators.py:268-279 monkeypatches it to inject a failure), in which
+    case the components engine runs so the replacement takes effect.
+    fault_iter: k >= 1 forces the factorisation opening iteration k-1 to fail
+    on the fused engine (psca_solve_args.fault_iter; a device-side test seam).
     """
     import torch
 
@@ -221,12 +376,16 @@ def psca_run(problem, sample, schedule: StepSchedule | None = None, max_iter: in
         n_steps = len(schedule.steps)    # the reference would IndexError at k = len(steps)
     steps = schedule.materialize(n_steps)
     m = sample.n_antennas
+    if _components_engine(engine):
+        return _psca_run_components(problem, sample, steps, n_steps, tol, record_objective,
+                                    trace, max_iter, schedule)
     kw = prior_arrays(problem, n, m)
     t0 = torch.cuda.Event(enable_timing=True) if torch.cuda.is_available() else None
     t1 = torch.cuda.Event(enable_timing=True) if torch.cuda.is_available() else None
     if t0 is not None:
         t0.record()
     gains = np.asarray(sample.gains, dtype=float) if problem.known_pathloss else None
+    launch_times = None
     if use_large_path(sample.pilot_len):
         from .large import psca_run_large
         r = psca_run_large(problem.kind, np.asarray(sample.pilots), gains,
@@ -237,11 +396,17 @@ def psca_run(problem, sample, schedule: StepSchedule | None = None, max_iter: in
         its_t, un_t, obj_t, x_t, cond = (r["iterates"], r["update_norm"], r["objective"],
                                          r["x"], r["cond_est"])
     else:
-        res = device.solve(problem.kind, np.asarray(sample.pilots)[None],
-                           np.asarray(sample.emp_cov)[None], np.array([sample.noise_power], float),
-                           m, steps, gains=gains[None] if gains is not None else None,
-                           max_iter=n_steps, tol=tol, record_objective=record_objective,
-                           record_iterates=True, **kw)
+        device.profile_begin()
+        try:
+            res = device.solve(problem.kind, np.asarray(sample.pilots)[None],
+                               np.asarray(sample.emp_cov)[None],
+                               np.array([sample.noise_power], float), m, steps,
+                               gains=gains[None] if gains is not None else None,
+                               max_iter=n_steps, tol=tol, record_objective=record_objective,
+                               record_iterates=True, fault_iter=fault_iter, **kw)
+            launch_times = device.profile_launches()
+        finally:
+            device.profile_end()
         status = int(res["status"][0].item())
         k_done = int(res["n_iter"][0].item())
         its_t, un_t = res["iterates"][0, :k_done + 1], res["update_norm"][0, :k_done]
@@ -256,9 +421,9 @@ def psca_run(problem, sample, schedule: StepSchedule | None = None, max_iter: in
         trace.objective = [float(v) for v in obj_t.cpu().numpy()]
     torch.cuda.synchronize()
     per = (t0.elapsed_time(t1) * 1e-3 / max(k_done, 1)) if t0 is not None else 0.0
-    trace.wall_times = [per] * k_done
+    trace.wall_times = _iteration_times(launch_times, k_done, per)
     if status == device.STATUS_CHOL_FAIL:
-        trace.meta["abort"] = ABORT_COND.format(cond)
+        trace.meta["abort"] = _conditioning_message(problem, sample, x_t, cond)
     elif status == device.STATUS_QFLOOR:
         trace.meta["abort"] = ABORT_QFLOOR
     trace.final = x_t.cpu().numpy().copy()

@@ -211,3 +211,79 @@ class EffPathlossPrior:
 
     def _hermite_coeffs(self):
         return float(self._pg(self.g_low)), float(self._dpg(self.g_low))
+
+
+# ---------------------------------------------------------------------------
+# Prior penalty terms at an iterate (priors.py:145-159, 313-399).  Evaluated
+# on the GPU by psca_prior_terms -- the same device code the solver runs at
+# every iterate -- for numpy or CUDA-tensor inputs (numpy in, numpy out).
+# ---------------------------------------------------------------------------
+
+def _device_prior_args(prior, n: int, n_antennas: int) -> tuple[str, dict]:
+    if isinstance(prior, EffPathlossPrior) or hasattr(prior, "g_low"):
+        p = np.broadcast_to(np.asarray(prior.p, dtype=float), (n,)).copy()
+        return "map-ur", {"prior_p": p, "eff_prior": prior}
+    if hasattr(prior, "c2"):
+        pr = prior if isinstance(prior, PairwiseMvbPrior) else PairwiseMvbPrior(prior.c1, prior.c2)
+        return "map-k", {"prior_c1": np.broadcast_to(pr.c1, (n,)).astype(float),
+                         "prior_c2": pr.csr_arrays()}
+    return "map-k", {"prior_lin": known_prior_gradient(prior, n_antennas, n)}
+
+
+def _prior_terms(x, prior, n_antennas: int, value=False, density=False):
+    import torch
+    from . import device
+    xt = x if isinstance(x, torch.Tensor) else None
+    xa = np.atleast_1d(np.asarray(x, dtype=float)) if xt is None else None
+    X = device._dev(device._torch(), xt if xt is not None else xa, torch.float64,
+                    torch.device("cuda", torch.cuda.current_device()))
+    single = X.dim() == 1
+    X2 = X.reshape(1, -1) if single else X
+    kind, kw = _device_prior_args(prior, X2.shape[1], n_antennas)
+    g, v, d = device.prior_terms_t(kind, X2, n_antennas, want_value=value, want_density=density,
+                                   **kw)
+    if xt is not None:
+        return g, v, d
+    cvt = (lambda t: None if t is None else (t[0] if single else t).cpu().numpy())
+    return cvt(g), cvt(v), cvt(d)
+
+
+def _check_range(gamma, prior):
+    """gamma in [0, g_high (1 + 1e-12)] or DomainError (priors.py:300-304)."""
+    g = np.asarray(gamma, dtype=float) if not hasattr(gamma, "cpu") else gamma.cpu().numpy()
+    if np.any(g < 0.0) or np.any(g > prior.g_high * (1.0 + 1e-12)):
+        raise DomainError("gamma outside [0, g_high]")
+
+
+def log_prior_grad_known(alpha, prior, n_antennas: int):
+    """-(1/M) d log p(alpha) / d alpha_n (priors.py:154-159), on the device."""
+    return _prior_terms(alpha, prior, n_antennas)[0]
+
+
+def log_prior_value_known(alpha, prior, n_antennas: int) -> float:
+    """-(1/M) log p(alpha) up to the normaliser (priors.py:145-151), on the device."""
+    return float(_prior_terms(alpha, prior, n_antennas, value=True)[1])
+
+
+def log_prior_grad_unknown(gamma, prior, n_antennas: int):
+    """-(1/M) clip(p'/p) with the dead-zone push (priors.py:377-399), on the device."""
+    _check_range(gamma, prior)
+    return _prior_terms(gamma, prior, n_antennas)[0]
+
+
+def log_prior_value_unknown(gamma, prior, n_antennas: int) -> float:
+    """-(1/M) sum log max(p^eps(gamma), 1e-300) (priors.py:370-374), on the device."""
+    _check_range(gamma, prior)
+    return float(_prior_terms(gamma, prior, n_antennas, value=True)[1])
+
+
+def pdf_eff_smooth(gamma, prior, n: int | None = None):
+    """Smoothed effective-pathloss density (priors.py:313-336), on the device."""
+    _check_range(gamma, prior)
+    g = np.atleast_1d(np.asarray(gamma, dtype=float))
+    pr = prior
+    if n is not None:
+        pr = dataclasses.replace(prior, p=np.full(g.shape[-1], float(np.asarray(prior.p)[n])),
+                                 dead_zone_grad=prior.dead_zone_grad)
+    out = _prior_terms(g, pr, 1, density=True)[2]
+    return float(out[0]) if np.ndim(gamma) == 0 else out

@@ -47,10 +47,11 @@ def _c_offsets(struct: str, fields, tmp_path) -> dict:
 
 def test_solve_args_struct_matches_header_layout(tmp_path):
     """The ctypes mirrors match the C compiler's layout of include/psca.h field by field."""
-    from paper_2503_15259_b200.device import EffPriorC, SolveArgsC
+    from paper_2503_15259_b200.device import CoordArgsC, EffPriorC, PriorArgsC, SolveArgsC
     from paper_2503_15259_b200.large import LargeArgsC
     assert ctypes.sizeof(EffPriorC) == 10 * 8
-    for cls, name in ((SolveArgsC, "psca_solve_args"), (LargeArgsC, "psca_large_args")):
+    for cls, name in ((SolveArgsC, "psca_solve_args"), (LargeArgsC, "psca_large_args"),
+                      (PriorArgsC, "psca_prior_args"), (CoordArgsC, "psca_coord_args")):
         fields = [f[0] for f in cls._fields_]
         c = _c_offsets(name, fields, tmp_path)
         for f in fields:
@@ -64,6 +65,22 @@ def test_workspace_query_rejects_bad_arguments():
     a = device.SolveArgsC(kind=7, B=1, N=10, L=4, n_antennas=8, max_iter=1)
     assert lib.psca_solve_workspace_bytes(ctypes.byref(a)) == 0
     assert lib.psca_solve(ctypes.byref(a), None, 0, None) == -1
+
+
+def test_misaligned_complex_arrays_rejected():
+    """complex128 inputs must be 16-byte aligned (psca.h): no kernel sees a shifted view."""
+    from paper_2503_15259_b200 import device
+    lib = device.load()
+    base = 1 << 20        # never dereferenced: the argument check rejects first
+    a = device.SolveArgsC(kind=2, B=1, N=40, L=8, n_antennas=8, max_iter=1, pilots=base + 8,
+                          emp_cov=base, noise=base, x_out=base, status=base, n_iter=base,
+                          steps=base, update_norm=base)
+    assert lib.psca_solve_workspace_bytes(ctypes.byref(a)) == 0
+    assert lib.psca_solve(ctypes.byref(a), None, 0, None) == -1
+    a.pilots, a.emp_cov = base, base + 8
+    assert lib.psca_solve_workspace_bytes(ctypes.byref(a)) == 0
+    a.emp_cov = base
+    assert lib.psca_solve_workspace_bytes(ctypes.byref(a)) > 0
 
 
 def test_problem_and_schedule_validation():
