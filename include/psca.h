@@ -292,6 +292,10 @@ int psca_profile_begin(void);
 int psca_profile_end(double* column_ms, int* column_launches, double* factor_ms,
                      int* factor_launches);
 
+/* Experiment builds only (-DPSCA_PROBE=1): copy the clock64 phase probes of
+ * the last instrumented launch (n <= 32 values) to host memory `out`. */
+int psca_debug_probes(long long* out, int n);
+
 /* on = 1: subsequent psca_solve calls on this thread issue every launch on
  * the caller's stream (no half-batch split over internal streams), so the
  * per-launch profile times are serialised kernel times; 0 restores the

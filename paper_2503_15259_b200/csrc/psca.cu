@@ -36,6 +36,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "psca.h"
@@ -102,6 +103,28 @@ struct ProfScope {
         }
     }
 };
+
+// Optional clock64 phase probes (build with -DPSCA_PROBE=1; experiment only):
+// thread 0 of block PSCA_PROBE_BLOCK records clock64() at numbered points of a
+// kernel; psca_debug_probes copies them out.
+#ifndef PSCA_PROBE
+#define PSCA_PROBE 0
+#endif
+#ifndef PSCA_PROBE_BLOCK
+#define PSCA_PROBE_BLOCK 0
+#endif
+__device__ long long g_probe[32];
+#if PSCA_PROBE
+#define PROBE(i)                                                                   \
+    do {                                                                           \
+        if (blockIdx.x == PSCA_PROBE_BLOCK && blockIdx.y == 0 && threadIdx.x == 0) \
+            g_probe[i] = clock64();                                                \
+    } while (0)
+#else
+#define PROBE(i) \
+    do {         \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // geometry
@@ -611,6 +634,7 @@ struct FacArgs {
     const double2* in_mat2;     // FAC_OBJECTIVE: sigma_inv
     double2* out_mat;           // FAC_INVERSE / FAC_ASSEMBLE output [B][L][L]
     double* out_vec;            // FAC_INVERSE: logdet, FAC_OBJECTIVE: value
+    double2* pfrag;             // warp-sweep factor path: [B][NBLK][32] P lower fragments
 };
 
 // Gauss-Jordan sweep inversion of a Hermitian PD matrix held in X (row
@@ -1199,6 +1223,7 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
 #include "psca_large.cuh"
 #include "psca_bcd.cuh"
 #include "psca_components.cuh"
+#include "psca_facw.cuh"
 
 // ---------------------------------------------------------------------------
 // empirical covariance (HERK): Sigma_hat = Y Y^H / M
@@ -1429,8 +1454,42 @@ int small_factor_threads() {
     return nt;
 }
 
+bool warp_factor_disabled() {
+    static const bool off = [] {
+        const char* e = getenv("PSCA_FAC_WARP");
+        return e && e[0] == '0';
+    }();
+    return off;
+}
+
+// batched factor stage as fac_sweep_w (one warp per instance) + fac_prod_t
+template <int NRB>
+cudaError_t launch_factor_w(const FacArgs& fa, cudaStream_t st) {
+    using S = TWS<NRB>;
+    cudaError_t err = cudaSuccess;
+    {
+        ProfScope prof(st, 1);
+        fac_sweep_w<NRB><<<(fa.B + S::IPC - 1) / S::IPC, 32 * S::IPC, S::SMEM, st>>>(fa);
+        ++g_launches;
+        if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+    if (fa.k_new >= fa.T) return cudaSuccess;   // no further column pass: no products
+    const size_t sm = (size_t)2 * (4 * NRB) * (4 * NRB + 1) * 16;
+    auto kfn = fac_prod_t<NRB, 128>;
+    if ((err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
+        cudaSuccess)
+        return err;
+    ProfScope prof(st, 1);
+    kfn<<<fa.B, 128, sm, st>>>(fa);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 template <int NRB>
 cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
+    if constexpr (NRB <= 10) {
+        if (fa.pfrag) return launch_factor_w<NRB>(fa, st);
+    }
     if (fa.B < sm_count()) {
         switch (small_factor_threads()) {
             case 512: return launch_factor_nt<NRB, 512>(fa, g, st);
@@ -1640,6 +1699,7 @@ FacArgs sub_fac(const FacArgs& f, int b0, int Bh, const Geo& g) {
     if (f.scratch) r.scratch = f.scratch + (size_t)b0 * 2 * g.LP * (g.LP + 1);
     if (f.pgrad) r.pgrad = f.pgrad + (size_t)b0 * N;
     if (f.dmat) r.dmat = f.dmat + (size_t)b0 * dmat_stride(g, L);
+    if (f.pfrag) r.pfrag = f.pfrag + (size_t)b0 * g.NBLK * 32;
     return r;
 }
 
@@ -1653,8 +1713,17 @@ struct SolveLayout {
     int* counter;
     double2* dmat;
     double2* scratch;
+    double2* pfrag;
     size_t total;
 };
+
+// the warp-per-instance factor (fac_sweep_w + fac_prod_t): compiled shapes up
+// to L = 40, one column chunk per instance, batches of at least one CTA per SM
+bool use_warp_factor(const psca_solve_args* a, const Geo& g, int n_chunks) {
+    return !warp_factor_disabled() && !generic_forced() && n_chunks == 1 &&
+           a->B >= sm_count() && (g.NRB == 2 || g.NRB == 3 || g.NRB == 4 || g.NRB == 5 ||
+                                  g.NRB == 6 || g.NRB == 8 || g.NRB == 10);
+}
 
 SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, void* ws) {
     Carve cv{static_cast<char*>(ws)};
@@ -1669,6 +1738,8 @@ SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, v
     s.counter = cv.take<int>(sizeof(int));
     s.dmat = cv.take<double2>((size_t)a->B * dmat_stride(g, a->L) * 16);
     s.scratch = cv.take<double2>(fac_scratch_bytes(g, a->B));
+    s.pfrag = cv.take<double2>(use_warp_factor(a, g, n_chunks) ? (size_t)a->B * g.NBLK * 32 * 16 : 0);
+    if (!use_warp_factor(a, g, n_chunks)) s.pfrag = nullptr;
     s.total = cv.off;
     return s;
 }
@@ -1865,6 +1936,13 @@ int psca_profile_end(double* column_ms, int* column_launches, double* factor_ms,
     return PSCA_OK;
 }
 
+int psca_debug_probes(long long* out, int n) {
+    if (n > 32) n = 32;
+    return cudaMemcpyFromSymbol(out, g_probe, (size_t)n * sizeof(long long)) == cudaSuccess
+               ? PSCA_OK
+               : PSCA_E_CUDA;
+}
+
 int psca_set_serial(int on) {
     g_serial = on != 0;
     return PSCA_OK;
@@ -1954,6 +2032,7 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
     fa.inst = lay.inst; fa.status = a->status; fa.n_iter = a->n_iter; fa.cond_est = a->cond_est;
     fa.update_norm = a->update_norm; fa.objective = ca.record_objective ? a->objective : nullptr;
     fa.scratch = lay.scratch;
+    fa.pfrag = lay.pfrag;
 
     double* xc = a->x_out;
     double* xn = lay.x_alt;

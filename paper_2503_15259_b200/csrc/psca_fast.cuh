@@ -36,6 +36,12 @@
 #ifndef PSCA_BLOCK_SWEEP
 #define PSCA_BLOCK_SWEEP 1
 #endif
+#ifndef PSCA_DSWEEP
+#define PSCA_DSWEEP 1    // sweep with the matrix in DMMA fragments (dmma_sweep)
+#endif
+#ifndef PSCA_USWEEP
+#define PSCA_USWEEP 1    // block sweep with U_j = M conj(C_j) shared per column
+#endif
 #ifndef PSCA_ADJ_INV
 #define PSCA_ADJ_INV 1   // 2x2 pivot block inverse as adj(K)/det(K)
 #endif
@@ -524,6 +530,365 @@ __device__ __forceinline__ void lower_block(int t, int& bi, int& bj) {
 }
 
 // ---------------------------------------------------------------------------
+// dmma_sweep: the Hermitian sweep operator (2x2 block pivots, the same pivots
+// as LDL^H) with the matrix held in DMMA accumulator fragments.
+//
+// The lower triangle of the LP x LP matrix is tiled like the rebuild blocks:
+// tile (bi, bj) = 4 complex rows x 8 complex columns, stored as one m8n8k4 C
+// fragment in the real 2x2 expansion (lane (r8, c4) holds component r8 & 1 of
+// entries (4 bi + r8 / 2, 8 bj + 2 c4 + h), h = 0, 1).  Warp w owns the tiles
+// w, w + NW, ... (row-major lower order).  Step K = {k, k+1}:
+//   phase U  thread j < LP forms U_j = M conj(C_j) (M = K^-1 = adj(K)/det(K),
+//            C_j = (a_jk, a_j,k+1), K entries zeroed) into SMEM;
+//   phase V  every owned tile takes ONE DMMA: acc += (-C^) U with C^ the real
+//            expansion of the two staged columns (A operand, k = 4 = 2
+//            complex) and U as B operand -- the rank-2 trailing update
+//            a_ij -= C_i U_j; lanes on the K rows / columns are replaced by
+//            U_j (row K), conj(U_i) (column K) and -M (the K block); the next
+//            pivot block's columns and K' itself are staged from the
+//            fragments.
+// Compared with per-thread 2x2 blocks (8 shared-memory loads of 16 bytes per
+// block per step, the factor kernel's limiter), a tile costs two 8-byte
+// operand loads and one DMMA per step.  SMEM scratch (ub, cs) lives in X,
+// which is free while the matrix is in registers; on return X holds
+// P = Sigma^-1 (full Hermitian, zero padding) unless a pivot failed.
+// ---------------------------------------------------------------------------
+template <int NRB, int NTH>
+struct TSW {
+    static constexpr int LP = 4 * NRB;
+    static constexpr int LPC = LP + ((NRB & 1) ? 0 : 4);   // staged-column stride (banks)
+    static constexpr int NTL = rebuild_block_count(NRB);    // lower tiles
+    static constexpr int NW = NTH / 32;
+    static constexpr int TPW = (NTL + NW - 1) / NW;         // tiles per warp (max)
+};
+
+template <int NRB, int NTH>
+__device__ __forceinline__ bool dmma_sweep(double2* X, int ld, int L, bool want_logdet,
+                                           double& logdet) {
+    using S = TSW<NRB, NTH>;
+    constexpr int LP = S::LP, LPC = S::LPC;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const int p = r8 & 1, q = c4 & 1, kc = c4 >> 1;
+    __shared__ double kv[2][4];
+    __shared__ double msh[4];
+    // owned tiles: row / column tile, and the step-independent operand offsets
+    // (doubles) of this lane's A (staged columns) and B (U) fragment elements;
+    // slots past the warp's count point at offset 0 and never match a pivot
+    int tbi[S::TPW], tbj[S::TPW], aoff[S::TPW], boff[S::TPW];
+#pragma unroll
+    for (int t = 0; t < S::TPW; ++t) {
+        tbi[t] = -64;
+        tbj[t] = -64;
+        aoff[t] = 0;
+        boff[t] = 0;
+    }
+    {
+        int idx = 0, nt = 0;
+#pragma unroll 1
+        for (int i = 0; i < NRB; ++i) {
+            const int jmax = (4 * i + 3) / 8;
+            for (int j = 0; j <= jmax; ++j, ++idx) {
+                if ((idx % S::NW) == warp) {
+#pragma unroll
+                    for (int t = 0; t < S::TPW; ++t)
+                        if (t == nt) {
+                            tbi[t] = i;
+                            tbj[t] = j;
+                            aoff[t] = 2 * (kc * LPC + 4 * i + (r8 >> 1)) + (p ^ q);
+                            boff[t] = 2 * (kc * LPC + 8 * j + r8) + q;
+                        }
+                    ++nt;
+                }
+            }
+        }
+    }
+    // load the lower triangle (zero above the diagonal and in the padding;
+    // odd L: the padding pivot L is an identity row, no effect on the L x L part)
+    double acc[S::TPW][2];
+    const double* Xd = reinterpret_cast<const double*>(X);
+#pragma unroll
+    for (int t = 0; t < S::TPW; ++t) {
+        const int l = 4 * tbi[t] + (r8 >> 1);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int m = 8 * tbj[t] + 2 * c4 + h;
+            double v = 0.0;
+            if (tbi[t] >= 0 && l < L && m < L && m <= l) v = Xd[2 * (l * ld + m) + p];
+            if ((L & 1) && l == L && m == L && p == 0) v = 1.0;
+            acc[t][h] = v;
+        }
+    }
+    __syncthreads();   // X is scratch from here on
+    double2* ub = X;                  // [2][LPC]: U(kc, j)
+    double2* cs = X + 2 * LPC;        // [2 phases][2][LPC]: C(l, kc)
+    const double* Ud = reinterpret_cast<const double*>(ub);
+    const double* Csd = reinterpret_cast<const double*>(cs);
+    // stage the columns of pivot block {k2, k2 + 1} from the fragments into
+    // phase dst (and K' into kv[dst]); only tiles holding those rows / columns
+    auto stage = [&](int k2, int dst) {
+        double* Cn = reinterpret_cast<double*>(cs + dst * 2 * LPC);
+        const int kr = k2 >> 2, kcl = k2 >> 3;
+#pragma unroll
+        for (int t = 0; t < S::TPW; ++t) {
+            if (tbi[t] == kr || tbj[t] == kcl) {
+                const int l = 4 * tbi[t] + (r8 >> 1);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = 8 * tbj[t] + 2 * c4 + h;
+                    const double v = acc[t][h];
+                    const bool il = (l == k2 || l == k2 + 1), im = (m == k2 || m == k2 + 1);
+                    if (il && im) {
+                        if (m <= l) {
+                            if (l == k2 && m == k2 && p == 0) kv[dst][0] = v;
+                            if (l == k2 + 1 && m == k2) kv[dst][1 + p] = v;
+                            if (l == k2 + 1 && m == k2 + 1 && p == 0) kv[dst][3] = v;
+                            if (m == l && p == 0) {   // K' rows of the staged columns: zero
+                                reinterpret_cast<double2*>(Cn)[l] = make_double2(0.0, 0.0);
+                                reinterpret_cast<double2*>(Cn)[LPC + l] = make_double2(0.0, 0.0);
+                            }
+                        }
+                    } else if (im && l > k2 + 1) {
+                        Cn[2 * ((m - k2) * LPC + l) + p] = v;              // a_lm
+                    } else if (il && m < k2) {
+                        Cn[2 * ((l - k2) * LPC + m) + p] = p ? -v : v;     // conj(a_lm)
+                    }
+                }
+            }
+        }
+    };
+    stage(0, 0);
+    __syncthreads();
+    logdet = 0.0;
+    bool ok = true;
+    const int LE = (L + 1) & ~1;
+    const unsigned long long sgn = (p == 0 && q == 1) ? 0ull : 0x8000000000000000ull;
+    for (int k = 0; k < LE; k += 2) {
+        const int ph = (k >> 1) & 1;
+        const double2* cc = cs + ph * 2 * LPC;
+        const double* Cd = Csd + ph * 4 * LPC;
+        PROBE(10 + (k >> 1));
+        const double ka = kv[ph][0], kbr = kv[ph][1], kbi = kv[ph][2], kcc = kv[ph][3];
+        const double det = fma(ka, kcc, -fma(kbr, kbr, kbi * kbi));
+        if (!(ka > 0.0) || !(det > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (want_logdet) logdet += log(det);
+        if (tid < LP) {
+            const double dinv = __drcp_rn(det);
+            const double m00 = kcc * dinv;
+            const double m11 = ka * dinv;
+            const double2 m10 = make_double2(-kbr * dinv, -kbi * dinv);
+            const double2 m01 = make_double2(m10.x, -m10.y);
+            const double2 pp = cc[tid], qq = cc[LPC + tid];
+            ub[tid] = make_double2(fma(m01.x, qq.x, fma(m01.y, qq.y, m00 * pp.x)),
+                                   fma(m01.y, qq.x, fma(-m01.x, qq.y, -m00 * pp.y)));
+            ub[LPC + tid] = make_double2(fma(m11, qq.x, fma(m10.x, pp.x, m10.y * pp.y)),
+                                         fma(-m11, qq.y, fma(m10.y, pp.x, -m10.x * pp.y)));
+            if (tid == 0) {
+                msh[0] = m00;
+                msh[1] = m11;
+                msh[2] = m10.x;
+                msh[3] = m10.y;
+            }
+        }
+        __syncthreads();
+        // rank-2 trailing update: one DMMA per tile
+#pragma unroll
+        for (int t = 0; t < S::TPW; ++t) dmma(acc[t], xsign(Cd[aoff[t]], sgn), Ud[boff[t]]);
+        // the K rows / columns
+        const int kr = k >> 2, kcl = k >> 3;
+#pragma unroll
+        for (int t = 0; t < S::TPW; ++t) {
+            if (tbi[t] == kr || tbj[t] == kcl) {
+                const int l = 4 * tbi[t] + (r8 >> 1);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = 8 * tbj[t] + 2 * c4 + h;
+                    const bool il = (l == k || l == k + 1), im = (m == k || m == k + 1);
+                    if (il && im) {
+                        if (m <= l) {
+                            double v;
+                            if (l == k) v = p ? 0.0 : -msh[0];
+                            else if (m == k) v = p ? -msh[3] : -msh[2];
+                            else v = p ? 0.0 : -msh[1];
+                            acc[t][h] = v;
+                        }
+                    } else if (il) {
+                        acc[t][h] = Ud[2 * ((l - k) * LPC + m) + p];          // U_m
+                    } else if (im) {
+                        const double u = Ud[2 * ((m - k) * LPC + l) + p];     // conj(U_l)
+                        acc[t][h] = p ? -u : u;
+                    }
+                }
+            }
+        }
+        if (k + 2 < LE) stage(k + 2, ph ^ 1);
+        __syncthreads();
+    }
+    if (!ok) return false;
+    // P = -(swept): full Hermitian into X (zero padding rows / columns)
+    double* Xw = reinterpret_cast<double*>(X);
+#pragma unroll
+    for (int t = 0; t < S::TPW; ++t) {
+        if (tbi[t] >= 0) {
+            const int l = 4 * tbi[t] + (r8 >> 1);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int m = 8 * tbj[t] + 2 * c4 + h;
+                if (m <= l && l < LP) {
+                    double v = (l < L && m < L) ? -acc[t][h] : 0.0;
+                    if (m == l) {
+                        Xw[2 * (l * ld + m) + p] = p ? 0.0 : v;
+                    } else {
+                        Xw[2 * (l * ld + m) + p] = v;
+                        Xw[2 * (m * ld + l) + p] = p ? -v : v;
+                    }
+                }
+            }
+        }
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// products_pass: X holds P = Sigma^-1 (full Hermitian, zero padding, row
+// stride LP + 1) and Sigma_hat is being staged into G (cp.async, or Es null:
+// read from L2).  trace(P Sigma_hat) when the objective is recorded, then
+// G = Sigma_hat P and A = P G on DMMA and the packed P'/A' fragments of the
+// next column pass into od.  Ends synchronised.
+// ---------------------------------------------------------------------------
+template <int NRB, int NTH>
+__device__ __forceinline__ void products_pass(const FacArgs& a, int b, double2* X, double2* G,
+                                              const double2* Es, double* od, double* sred,
+                                              double& trace) {
+    const int tid = threadIdx.x;
+    const int L = a.L;
+    constexpr int LP = 4 * NRB;
+    const int ld = LP + 1;
+    cp_async_wait<0>();   // Sigma_hat staged by the caller (stage_emp), if in SMEM
+    __syncthreads();
+    PROBE(7);
+    const double2* Eg = a.emp_cov + (size_t)b * L * L;   // used when Es == nullptr
+    auto Ev = [&](int i, int c) -> double2 {
+        return Es ? Es[i * ld + c] : __ldg(Eg + (size_t)i * L + c);
+    };
+    trace = 0.0;
+    if (a.record_objective) {
+        double s = 0.0;
+        for (int e = tid; e < L * L; e += NTH) {
+            const int i = e / L, j = e - i * L;
+            const double2 pv = X[i * ld + j], ev = Ev(j, i);
+            s = fma(pv.x, ev.x, fma(-pv.y, ev.y, s));
+        }
+        trace = block_sum(s, sred);
+    }
+    // ---- G = Sigma_hat P and A = P G on DMMA ----------------------------------
+    // Complex products in the real 2x2 expansion, first real column of each
+    // complex column only: C^[2l+p][m] = sum_{kc,q} A^[2l+p][2kc+q] Bc[2kc+q][m]
+    // with A^ = [[re,-im],[im,re]] and Bc[2kc+q][m] = component q of B(kc,m),
+    // so C^[2l+p][m] = component p of (A B)(l,m).  Tile = 8 real rows (4
+    // complex rows, ri) x 8 complex columns (cj), k-step = 2 complex columns.
+    // A warp owns a row tile and keeps one accumulator chain per column tile
+    // (the A fragment is shared), reading A^ from Sigma_hat (L2) or P (SMEM)
+    // and Bc from SMEM.
+    {
+        constexpr int NCJ = (LP + 7) / 8;
+        constexpr int NKS = LP / 2;
+        constexpr int NWF = NTH / 32;
+        const int lane = tid & 31, warp = tid >> 5;
+        const int r8 = lane >> 2, c4 = lane & 3;
+        const int p = r8 & 1, q = c4 & 1;
+        const unsigned long long sg = (p == 0 && q == 1) ? 0x8000000000000000ull : 0ull;
+        const double* Xd = reinterpret_cast<const double*>(X);
+        double* Gd = reinterpret_cast<double*>(G);
+        // G = Sigma_hat P, all tiles
+        for (int ri = warp; ri < NRB; ri += NWF) {
+            const int l = 4 * ri + (r8 >> 1);
+            double acc[NCJ][2];
+#pragma unroll
+            for (int j = 0; j < NCJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+            const double* erow = Es ? reinterpret_cast<const double*>(Es + (size_t)l * ld)
+                                    : reinterpret_cast<const double*>(Eg + (size_t)l * L);
+#pragma unroll 4
+            for (int ks = 0; ks < NKS; ++ks) {
+                const int kc = 2 * ks + (c4 >> 1);
+                const double av = (l < L && kc < L) ? xsign(erow[2 * kc + (p ^ q)], sg) : 0.0;
+                const double* brow = Xd + 2 * (kc * ld) + q;
+#pragma unroll
+                for (int j = 0; j < NCJ; ++j) {
+                    const int m = 8 * j + r8;
+                    const double bv = (m < LP) ? brow[2 * m] : 0.0;
+                    dmma(acc[j], av, bv);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NCJ; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int m = 8 * j + 2 * c4 + h;
+                    if (m < LP) Gd[2 * (l * ld + m) + p] = acc[j][h];
+                }
+        }
+        __syncthreads();
+        // A = P G, lower tiles only (column tiles cj with 8 cj <= 4 ri + 3), and
+        // the fragment pack: entry (l, m), m <= 4 ri + 3, gets P'/A' = 2x the
+        // lower values, the real diagonal, zero above the diagonal
+        PROBE(8);
+        const double* Gc = reinterpret_cast<const double*>(G);
+        for (int t = warp; t < NRB; t += NWF) {
+            const int ri = NRB - 1 - t;             // longest rows first
+            const int ncj = (4 * ri + 3) / 8 + 1;
+            const int l = 4 * ri + (r8 >> 1);
+            double acc[NCJ][2];
+#pragma unroll
+            for (int j = 0; j < NCJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+            const double* prow = Xd + 2 * (l * ld);
+#pragma unroll 4
+            for (int ks = 0; ks < NKS; ++ks) {
+                const int kc = 2 * ks + (c4 >> 1);
+                const double av = xsign(prow[2 * kc + (p ^ q)], sg);
+                const double* brow = Gc + 2 * (kc * ld) + q;
+#pragma unroll
+                for (int j = 0; j < NCJ; ++j) {
+                    if (j < ncj) {
+                        const int m = 8 * j + r8;
+                        const double bv = (m < LP) ? brow[2 * m] : 0.0;
+                        dmma(acc[j], av, bv);
+                    }
+                }
+            }
+            const int i4 = l >> 2;
+#pragma unroll
+            for (int j = 0; j < NCJ; ++j) {
+                if (j < ncj) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int m = 8 * j + 2 * c4 + h;
+                        if (m <= 4 * ri + 3) {
+                            const double f = (m < l) ? 2.0 : ((m == l && p == 0) ? 1.0 : 0.0);
+                            const double pv = f * Xd[2 * (l * ld + m) + p];
+                            const double avv = f * acc[j][h];
+                            const int blk = i4 * (i4 + 1) + (m >> 1);
+                            const int ent = (l & 3) * 2 + (m & 1);
+                            double2* o = reinterpret_cast<double2*>(od) + (size_t)blk * FRAG_SLOTS + 3 * ent;
+                            if (p == 0) {
+                                o[0] = make_double2(pv, avv);
+                            } else {
+                                o[1] = make_double2(pv, avv);
+                                o[2] = make_double2(-pv, -avv);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
 // factor_pass: X holds Sigma (L x L Hermitian, row stride ld = LP + 1) on
 // entry.  Hermitian sweep-operator Gauss-Jordan on the lower triangle only:
 // sweeping pivot k maps a_kk -> -1/d, a_ik, a_kj -> a/d, a_ij -> a_ij -
@@ -556,6 +921,17 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         }
         frob = sqrt(block_sum(s, sred));
     }
+    PROBE(4);
+#if PSCA_DSWEEP
+    {
+        const bool ok = dmma_sweep<NRB, NTH>(X, ld, L, a.record_objective, logdet);
+        PROBE(5);
+        if (!ok) {
+            __syncthreads();
+            return false;
+        }
+    }
+#else
     // ---- lower 2x2 blocks of this thread ---------------------------------------
     int bi[F::SL], bj[F::SL];
     double2 v[F::SL][2][2];
@@ -575,7 +951,156 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                 if ((L & 1) && i == L && j == L) v[u][di][dj] = make_double2(1.0, 0.0);
             }
     }
-#if PSCA_BLOCK_SWEEP
+#if PSCA_BLOCK_SWEEP && PSCA_USWEEP
+    // ---- 2x2 block pivots K = {k, k+1} (k even), pivot-column products shared.
+    // Staged per step (ping-pong): the two columns of K for every row with the
+    // K entries zeroed (cs0, cs1), and K itself (kv: a = a_kk, b = a_k+1,k,
+    // c = a_k+1,k+1).  With M = K^-1 and C_j = (a_jk, a_j,k+1):
+    //   phase U  thread j < LP forms U_j = M conj(C_j) once per column into
+    //            SMEM (ub0 / ub1; X is free during the sweep) -- 12 FP64
+    //            operations per column instead of 24 per owned 2x2 block;
+    //   phase V  every owned block is updated a_ij -= C_i U_j (8 DFMA per
+    //            entry); the K rows become U_j, the K columns conj(U_i), the
+    //            K block -M; the next pivot block's columns are staged.
+    // The pivots are those of the scalar sweep (a, then c - |b|^2 / a), so
+    // PD-ness and log|Sigma| are unchanged.  Two barriers per step.
+    __shared__ double kv[2][4];
+    __shared__ double msh[4];
+    double2* ub0 = X;
+    double2* ub1 = X + LP;
+    {
+        double2* cs0 = cbuf;
+        double2* cs1 = cbuf + LP;
+        for (int e = tid; e < LP; e += NTH) {
+            cs0[e] = (e < L && e >= 2) ? X[e * ld] : make_double2(0.0, 0.0);
+            cs1[e] = (e < L && e >= 2) ? X[e * ld + 1] : make_double2(0.0, 0.0);
+        }
+        if (tid == 0) {
+            kv[0][0] = X[0].x;
+            const double2 bb = (L > 1) ? X[ld] : make_double2(0.0, 0.0);
+            kv[0][1] = bb.x;
+            kv[0][2] = bb.y;
+            kv[0][3] = (L > 1) ? X[ld + 1].x : 1.0;
+        }
+    }
+    __syncthreads();   // X (Sigma) is in registers now; ub0 / ub1 may reuse it
+    logdet = 0.0;
+    bool ok = true;
+    const bool want_logdet = a.record_objective;
+    const int LE = (L + 1) & ~1;
+    for (int k = 0; k < LE; k += 2) {
+        const int ph = (k >> 1) & 1;
+        const double2* c0 = cbuf + ph * 2 * LP;
+        const double2* c1 = c0 + LP;
+        double2* n0 = cbuf + (ph ^ 1) * 2 * LP;
+        double2* n1 = n0 + LP;
+        if (k == 10) PROBE(10);
+        const double ka = kv[ph][0], kbr = kv[ph][1], kbi = kv[ph][2], kc = kv[ph][3];
+        // M = K^-1 = adj(K) / det(K), det = a c - |b|^2 = a d1; K is PD iff
+        // a > 0 and det > 0 (uniform: every thread reads the same kv)
+        const double det = fma(ka, kc, -fma(kbr, kbr, kbi * kbi));
+        if (!(ka > 0.0) || !(det > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (want_logdet) logdet += log(det);
+        if (k == 10) PROBE(11);
+        if (tid < LP) {
+            const double dinv = __drcp_rn(det);
+            const double m00 = kc * dinv;
+            const double m11 = ka * dinv;
+            const double2 m10 = make_double2(-kbr * dinv, -kbi * dinv);
+            const double2 m01 = make_double2(m10.x, -m10.y);
+            const double2 pp = c0[tid], qq = c1[tid];
+            ub0[tid] = make_double2(fma(m01.x, qq.x, fma(m01.y, qq.y, m00 * pp.x)),
+                                    fma(m01.y, qq.x, fma(-m01.x, qq.y, -m00 * pp.y)));
+            ub1[tid] = make_double2(fma(m11, qq.x, fma(m10.x, pp.x, m10.y * pp.y)),
+                                    fma(-m11, qq.y, fma(m10.y, pp.x, -m10.x * pp.y)));
+            if (tid == 0) {
+                msh[0] = m00;
+                msh[1] = m11;
+                msh[2] = m10.x;
+                msh[3] = m10.y;
+            }
+        }
+        if (k == 10) PROBE(12);
+        __syncthreads();
+        if (k == 10) PROBE(13);
+        const int kb = k >> 1;
+#pragma unroll
+        for (int u = 0; u < F::SL; ++u) {
+            if (bi[u] < 0) continue;
+            const int i0 = 2 * bi[u], j0 = 2 * bj[u];
+            if (bi[u] == kb && bj[u] == kb) {
+                v[u][0][0] = make_double2(-msh[0], 0.0);
+                v[u][1][0] = make_double2(-msh[2], -msh[3]);
+                v[u][1][1] = make_double2(-msh[1], 0.0);
+            } else if (bj[u] == kb) {
+                // rows i not in K, columns K: (a_ik, a_ik+1) <- C_i M = conj(U_i)
+#pragma unroll
+                for (int di = 0; di < 2; ++di) {
+                    const double2 x0 = ub0[i0 + di], x1 = ub1[i0 + di];
+                    v[u][di][0] = make_double2(x0.x, -x0.y);
+                    v[u][di][1] = make_double2(x1.x, -x1.y);
+                }
+            } else if (bi[u] == kb) {
+                // rows K, columns j < k: (a_kj, a_k+1,j) <- M conj(C_j) = U_j
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) {
+                    v[u][0][dj] = ub0[j0 + dj];
+                    v[u][1][dj] = ub1[j0 + dj];
+                }
+            } else {
+                double2 ua[2], ubv[2];
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) {
+                    ua[dj] = ub0[j0 + dj];
+                    ubv[dj] = ub1[j0 + dj];
+                }
+#pragma unroll
+                for (int di = 0; di < 2; ++di) {
+                    const double2 pp = c0[i0 + di], qq = c1[i0 + di];   // C_i
+#pragma unroll
+                    for (int dj = 0; dj < 2; ++dj) {
+                        const double2 o = v[u][di][dj];
+                        double nx = fma(-pp.x, ua[dj].x, fma(pp.y, ua[dj].y, o.x));
+                        double ny = fma(-pp.x, ua[dj].y, fma(-pp.y, ua[dj].x, o.y));
+                        nx = fma(-qq.x, ubv[dj].x, fma(qq.y, ubv[dj].y, nx));
+                        ny = fma(-qq.x, ubv[dj].y, fma(-qq.y, ubv[dj].x, ny));
+                        v[u][di][dj] = make_double2(nx, ny);
+                    }
+                }
+            }
+            // stage K' = {k+2, k+3}: its columns for every row, K' zeroed
+            if (bi[u] == kb + 1 && bj[u] == kb + 1) {
+                kv[ph ^ 1][0] = v[u][0][0].x;
+                kv[ph ^ 1][1] = v[u][1][0].x;
+                kv[ph ^ 1][2] = v[u][1][0].y;
+                kv[ph ^ 1][3] = v[u][1][1].x;
+#pragma unroll
+                for (int di = 0; di < 2; ++di) {
+                    n0[i0 + di] = make_double2(0.0, 0.0);
+                    n1[i0 + di] = make_double2(0.0, 0.0);
+                }
+            } else if (bj[u] == kb + 1) {
+#pragma unroll
+                for (int di = 0; di < 2; ++di) {
+                    n0[i0 + di] = v[u][di][0];
+                    n1[i0 + di] = v[u][di][1];
+                }
+            } else if (bi[u] == kb + 1) {
+#pragma unroll
+                for (int dj = 0; dj < 2; ++dj) {
+                    n0[j0 + dj] = make_double2(v[u][0][dj].x, -v[u][0][dj].y);
+                    n1[j0 + dj] = make_double2(v[u][1][dj].x, -v[u][1][dj].y);
+                }
+            }
+        }
+        if (k == 10) PROBE(14);
+        __syncthreads();
+        if (k == 10) PROBE(15);
+    }
+#elif PSCA_BLOCK_SWEEP
     // ---- 2x2 block pivots K = {k, k+1} (k even): one barrier per two pivots.
     // Staged per step (ping-pong): the two columns of K for every row with the
     // K entries zeroed (cs0, cs1), and K itself (kv: a = a_kk, b = a_k+1,k,
@@ -787,6 +1312,7 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
         __syncthreads();
     }
 #endif
+    PROBE(5);
     if (!ok) {
         __syncthreads();
         return false;
@@ -808,123 +1334,9 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                 }
             }
     }
-    cp_async_wait<0>();   // Sigma_hat staged by the caller (stage_emp), if in SMEM
-    __syncthreads();
-    const double2* Eg = a.emp_cov + (size_t)b * L * L;   // used when Es == nullptr
-    auto Ev = [&](int i, int c) -> double2 {
-        return Es ? Es[i * ld + c] : __ldg(Eg + (size_t)i * L + c);
-    };
-    trace = 0.0;
-    if (a.record_objective) {
-        double s = 0.0;
-        for (int e = tid; e < L * L; e += NTH) {
-            const int i = e / L, j = e - i * L;
-            const double2 pv = X[i * ld + j], ev = Ev(j, i);
-            s = fma(pv.x, ev.x, fma(-pv.y, ev.y, s));
-        }
-        trace = block_sum(s, sred);
-    }
-    // ---- G = Sigma_hat P and A = P G on DMMA ----------------------------------
-    // Complex products in the real 2x2 expansion, first real column of each
-    // complex column only: C^[2l+p][m] = sum_{kc,q} A^[2l+p][2kc+q] Bc[2kc+q][m]
-    // with A^ = [[re,-im],[im,re]] and Bc[2kc+q][m] = component q of B(kc,m),
-    // so C^[2l+p][m] = component p of (A B)(l,m).  Tile = 8 real rows (4
-    // complex rows, ri) x 8 complex columns (cj), k-step = 2 complex columns.
-    // A warp owns a row tile and keeps one accumulator chain per column tile
-    // (the A fragment is shared), reading A^ from Sigma_hat (L2) or P (SMEM)
-    // and Bc from SMEM.
-    {
-        constexpr int NCJ = (LP + 7) / 8;
-        constexpr int NKS = LP / 2;
-        constexpr int NWF = NTH / 32;
-        const int lane = tid & 31, warp = tid >> 5;
-        const int r8 = lane >> 2, c4 = lane & 3;
-        const int p = r8 & 1, q = c4 & 1;
-        const unsigned long long sg = (p == 0 && q == 1) ? 0x8000000000000000ull : 0ull;
-        const double* Xd = reinterpret_cast<const double*>(X);
-        double* Gd = reinterpret_cast<double*>(G);
-        // G = Sigma_hat P, all tiles
-        for (int ri = warp; ri < NRB; ri += NWF) {
-            const int l = 4 * ri + (r8 >> 1);
-            double acc[NCJ][2];
-#pragma unroll
-            for (int j = 0; j < NCJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-            const double* erow = Es ? reinterpret_cast<const double*>(Es + (size_t)l * ld)
-                                    : reinterpret_cast<const double*>(Eg + (size_t)l * L);
-#pragma unroll 4
-            for (int ks = 0; ks < NKS; ++ks) {
-                const int kc = 2 * ks + (c4 >> 1);
-                const double av = (l < L && kc < L) ? xsign(erow[2 * kc + (p ^ q)], sg) : 0.0;
-                const double* brow = Xd + 2 * (kc * ld) + q;
-#pragma unroll
-                for (int j = 0; j < NCJ; ++j) {
-                    const int m = 8 * j + r8;
-                    const double bv = (m < LP) ? brow[2 * m] : 0.0;
-                    dmma(acc[j], av, bv);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < NCJ; ++j)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int m = 8 * j + 2 * c4 + h;
-                    if (m < LP) Gd[2 * (l * ld + m) + p] = acc[j][h];
-                }
-        }
-        __syncthreads();
-        // A = P G, lower tiles only (column tiles cj with 8 cj <= 4 ri + 3), and
-        // the fragment pack: entry (l, m), m <= 4 ri + 3, gets P'/A' = 2x the
-        // lower values, the real diagonal, zero above the diagonal
-        const double* Gc = reinterpret_cast<const double*>(G);
-        for (int t = warp; t < NRB; t += NWF) {
-            const int ri = NRB - 1 - t;             // longest rows first
-            const int ncj = (4 * ri + 3) / 8 + 1;
-            const int l = 4 * ri + (r8 >> 1);
-            double acc[NCJ][2];
-#pragma unroll
-            for (int j = 0; j < NCJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-            const double* prow = Xd + 2 * (l * ld);
-#pragma unroll 4
-            for (int ks = 0; ks < NKS; ++ks) {
-                const int kc = 2 * ks + (c4 >> 1);
-                const double av = xsign(prow[2 * kc + (p ^ q)], sg);
-                const double* brow = Gc + 2 * (kc * ld) + q;
-#pragma unroll
-                for (int j = 0; j < NCJ; ++j) {
-                    if (j < ncj) {
-                        const int m = 8 * j + r8;
-                        const double bv = (m < LP) ? brow[2 * m] : 0.0;
-                        dmma(acc[j], av, bv);
-                    }
-                }
-            }
-            const int i4 = l >> 2;
-#pragma unroll
-            for (int j = 0; j < NCJ; ++j) {
-                if (j < ncj) {
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int m = 8 * j + 2 * c4 + h;
-                        if (m <= 4 * ri + 3) {
-                            const double f = (m < l) ? 2.0 : ((m == l && p == 0) ? 1.0 : 0.0);
-                            const double pv = f * Xd[2 * (l * ld + m) + p];
-                            const double avv = f * acc[j][h];
-                            const int blk = i4 * (i4 + 1) + (m >> 1);
-                            const int ent = (l & 3) * 2 + (m & 1);
-                            double2* o = reinterpret_cast<double2*>(od) + (size_t)blk * FRAG_SLOTS + 3 * ent;
-                            if (p == 0) {
-                                o[0] = make_double2(pv, avv);
-                            } else {
-                                o[1] = make_double2(pv, avv);
-                                o[2] = make_double2(-pv, -avv);
-                            }
-                        }
-                    }
-                }
-            }
-        }
-    }
-    __syncthreads();
+#endif  // PSCA_DSWEEP
+    PROBE(6);
+    products_pass<NRB, NTH>(a, b, X, G, Es, od, sred, trace);
     return true;
 }
 
@@ -1011,10 +1423,13 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
     const int LP = geo.LP;
     const int ld = LP + 1;
     if (a.status[b] != PSCA_RUNNING) return;
+    PROBE(0);
     if (a.k_new > 0) {
         if (fac_finalize(a, b, &s_flag)) return;
     }
+    PROBE(1);
     const double prior_value = fac_prior_terms(a, b, sred);
+    PROBE(2);
     double2* sm = reinterpret_cast<double2*>(smem_raw);
     double2* rowb = sm;             // [2][LP] pivot column ping-pong
     double2* colb = sm + 2 * LP;    // (unused)
@@ -1029,6 +1444,7 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
     stage_emp(a, b, G, ld);
     if (NTH >= 512) assemble_sigma_seq(a, geo, b, X, ld, a.k_new == 0);
     else assemble_sigma<8, 1>(a, geo, b, X, ld, a.k_new == 0);
+    PROBE(3);
     double frob, logdet, trace;
     double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
     if (!factor_pass<NRB, NTH>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet,
@@ -1039,6 +1455,7 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
         }
         return;
     }
+    PROBE(9);
     if (tid == 0) {
         double* in = a.inst + (size_t)b * 4;
         in[0] = frob;

@@ -98,6 +98,7 @@ _SIGS = {
     "psca_profile_end": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int),
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
     "psca_set_serial": (ctypes.c_int, [ctypes.c_int]),
+    "psca_debug_probes": (ctypes.c_int, [ctypes.POINTER(ctypes.c_longlong), ctypes.c_int]),
     "psca_profile_launches": (ctypes.c_int, [ctypes.POINTER(ctypes.c_double),
                                              ctypes.POINTER(ctypes.c_int), ctypes.c_int]),
     "psca_solve_workspace_bytes": (ctypes.c_size_t, [ctypes.POINTER(SolveArgsC)]),
