@@ -107,10 +107,18 @@ size_t psca_solve_workspace_bytes(const psca_solve_args* a);
  *  unroll.forward, unroll.py:69-73). */
 int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Sigma_hat = Y Y^H / n_antennas  (sysmodel.py:244-248 empirical_cov).
+/* Sigma_hat = Y Y^H / n_antennas  (sysmodel.py:244-248 empirical_cov), on DMMA.
  * y: [B][L][Mc] complex128 -> out: [B][L][L] complex128. */
 int psca_empirical_cov(const double* y, int B, int L, int Mc, int n_antennas, double* out,
                        void* stream);
+
+/* Received signal of a scene batch: Y = S[:, active] diag(sqrt(g[active])) H + Z
+ * (sysmodel.py:230-241; the draws stay on the host -- the Philox streams are
+ * the scene contract -- and the GEMM runs on DMMA).  pilots [B][L][N],
+ * active [B][K] (int32 device indices), gains [B][N], h [B][K][M], z [B][L][M]
+ * complex128 -> y [B][L][M]. */
+int psca_received(const double* pilots, const int* active, const double* gains, const double* h,
+                  const double* z, int B, int L, int N, int K, int M, double* y, void* stream);
 
 /* Sigma = S diag(w) S^H + sigma^2 I  (covlinalg.py:43-57 cov_unknown; cov_known
  * :60-67 passes w = alpha*g).  pilots [B][L][N], w [B][N], noise [B] -> out [B][L][L]. */
@@ -205,13 +213,18 @@ int psca_coord_step(const psca_coord_args* a, void* stream);
  *     psca_large_begin                         x = 0, Sigma_0 = sigma^2 I, factor
  *     for k: psca_large_columns(k)             this rank's columns: quad forms,
  *                                              update, Sigma-increment partial
- *            [all-reduce the exchange buffers: dsig (sum), red[0] (sum),
- *             red[1] (min) -- ncclAllReduce over NVLink when sharded]
+ *            [all-reduce the exchange block: dsig and red[0..1] (one SUM over
+ *             dsig_len + 2 contiguous doubles), red[2] (MIN) -- ncclAllReduce
+ *             over NVLink when sharded]
  *            psca_large_factor(k)              finalise iteration k (q-floor,
  *                                              update norm, tol), factor k+1
- *            stop when *flag (device int) != 0
- * x after iteration k is x_b for even k, x_a for odd k (x_a holds x_0 = 0).
- * Replaces the same psca_run loop (estimators.py:259-286) for large L. */
+ *            the loop may run on after a stop: every kernel is gated on the
+ *            device stop flag, so *flag (device int) needs checking only now
+ *            and then (no host synchronisation per iteration)
+ * red[0] = sum dx^2, red[1] = this shard's prior penalty (objective only),
+ * red[2] = min q.  x after iteration k is x_b for even k, x_a for odd k (x_a
+ * holds x_0 = 0).  Replaces the same psca_run loop (estimators.py:259-286)
+ * for large L. */
 typedef struct {
     int kind, N, L, n_antennas, max_iter, record_objective;
     double tol, noise;
@@ -234,8 +247,9 @@ typedef struct {
 
 size_t psca_large_workspace_bytes(const psca_large_args* a);
 /* Device addresses (inside the workspace) of the per-iteration exchange
- * buffers: dsig (dsig_len doubles, summed over ranks) and red (red[0] summed,
- * red[1] min-reduced over ranks). */
+ * block: dsig (dsig_len doubles) immediately followed by red (red == dsig +
+ * dsig_len): dsig, red[0] and red[1] are summed over ranks, red[2] is
+ * min-reduced. */
 int psca_large_exchange(const psca_large_args* a, void* workspace, double** dsig,
                         size_t* dsig_len, double** red);
 /* Device address of the stop flag (int, 0 = continue) inside the workspace;

@@ -1224,41 +1224,11 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
 #include "psca_bcd.cuh"
 #include "psca_components.cuh"
 #include "psca_facw.cuh"
+#include "psca_scene.cuh"
 
 // ---------------------------------------------------------------------------
 // empirical covariance (HERK): Sigma_hat = Y Y^H / M
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) herk_kernel(const double2* __restrict__ y, int L, int Mc,
-                                                  int n_antennas,
-                                                  double2* __restrict__ out) {
-    const int b = blockIdx.y;
-    const int e = blockIdx.x * NT + threadIdx.x;
-    const int npair = L * (L + 1) / 2;
-    if (e >= npair) return;
-    // decode lower-triangle pair (l >= m), row-major
-    int l = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    while (l * (l + 1) / 2 > e) --l;
-    while ((l + 1) * (l + 2) / 2 <= e) ++l;
-    const int m = e - l * (l + 1) / 2;
-    const double2* yl = y + ((size_t)b * L + l) * Mc;
-    const double2* ym = y + ((size_t)b * L + m) * Mc;
-    double2 s = make_double2(0.0, 0.0);
-    for (int c = 0; c < Mc; ++c) {
-        double2 u = __ldg(yl + c), v = __ldg(ym + c);
-        // u * conj(v)
-        s.x = fma(u.x, v.x, fma(u.y, v.y, s.x));
-        s.y = fma(u.y, v.x, fma(-u.x, v.y, s.y));
-    }
-    s.x = s.x / (double)n_antennas;
-    s.y = s.y / (double)n_antennas;
-    double2* o = out + (size_t)b * L * L;
-    if (l == m) {
-        o[l * L + l] = make_double2(s.x, 0.0);
-    } else {
-        o[l * L + m] = s;
-        o[m * L + l] = make_double2(s.x, -s.y);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // host helpers
@@ -1819,8 +1789,10 @@ LargeLayout large_layout(const psca_large_args* a, void* ws) {
     l.pgrad = cv.take<double>((size_t)a->N * 8);
     l.red_part = cv.take<double>((size_t)l.n_red * 2 * 8);
     l.dsig_part = cv.take<double2>((size_t)l.ks * l.NBLK * 32 * 16);
-    l.dsig = cv.take<double2>((size_t)l.NBLK * 32 * 16);
-    l.red = cv.take<double>(4 * 8);
+    // dsig and red are one contiguous exchange block: [dsig | red[0] red[1]]
+    // all-reduced with SUM in one call, red[2] with MIN (psca_large_exchange)
+    l.dsig = cv.take<double2>((size_t)l.NBLK * 32 * 16 + 4 * 8);
+    l.red = reinterpret_cast<double*>(l.dsig + (size_t)l.NBLK * 32);
     l.dmat = cv.take<double2>((size_t)a->L * a->L * 16);
     l.Xg = cv.take<double2>((size_t)l.LP * l.LP * 16);
     l.Gg = cv.take<double2>((size_t)l.LP * l.LP * 16);
@@ -2113,15 +2085,33 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
 int psca_empirical_cov(const double* y, int B, int L, int Mc, int n_antennas, double* out,
                        void* stream) {
     if (!y || !out || B < 0 || L < 1 || Mc < 0 || n_antennas < 1) return PSCA_E_ARG;
+    if (!aligned16(y) || !aligned16(out)) return PSCA_E_ARG;
     if (B == 0) return PSCA_OK;
     g_launches = 0;
-    const int npair = L * (L + 1) / 2;
-    dim3 grid((npair + NT - 1) / NT, B);
-    herk_kernel<<<grid, NT, 0, static_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<const double2*>(y), L, Mc, n_antennas,
-        reinterpret_cast<double2*>(out));
+    const int ntiles = rebuild_block_count((L + 3) / 4);
+    dim3 grid((ntiles + 7) / 8, B);
+    herk_dmma_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const double2*>(y), L, Mc, n_antennas, reinterpret_cast<double2*>(out));
     ++g_launches;
-    return cudaGetLastError() == cudaSuccess ? PSCA_OK : PSCA_E_CUDA;
+    return ok_or_record(cudaGetLastError()) ? PSCA_OK : PSCA_E_CUDA;
+}
+
+int psca_received(const double* pilots, const int* active, const double* gains, const double* h,
+                  const double* z, int B, int L, int N, int K, int M, double* y, void* stream) {
+    if (!pilots || !active || !gains || !h || !z || !y || B < 0 || L < 1 || N < 1 || K < 0 ||
+        M < 1)
+        return PSCA_E_ARG;
+    if (!aligned16(pilots) || !aligned16(h) || !aligned16(z) || !aligned16(y)) return PSCA_E_ARG;
+    if (B == 0) return PSCA_OK;
+    g_launches = 0;
+    const int ntiles = ((L + 3) / 4) * ((M + 7) / 8);
+    dim3 grid((ntiles + 7) / 8, B);
+    received_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const double2*>(pilots), active, gains,
+        reinterpret_cast<const double2*>(h), reinterpret_cast<const double2*>(z), L, N, K, M,
+        reinterpret_cast<double2*>(y));
+    ++g_launches;
+    return ok_or_record(cudaGetLastError()) ? PSCA_OK : PSCA_E_CUDA;
 }
 
 size_t psca_cov_workspace_bytes(int B, int N, int L) {
@@ -2317,7 +2307,7 @@ int psca_large_exchange(const psca_large_args* a, void* workspace, double** dsig
     if (check_large_args(a) != PSCA_OK || !workspace) return PSCA_E_ARG;
     LargeLayout l = large_layout(a, workspace);
     if (dsig) *dsig = reinterpret_cast<double*>(l.dsig);
-    if (dsig_len) *dsig_len = (size_t)l.NBLK * 32 * 2;
+    if (dsig_len) *dsig_len = (size_t)l.NBLK * 32 * 2;   // red follows dsig directly
     if (red) *red = l.red;
     return PSCA_OK;
 }
@@ -2335,6 +2325,7 @@ int psca_large_begin(const psca_large_args* a, void* workspace, size_t workspace
     cudaMemsetAsync(a->n_iter, 0, sizeof(int), st);
     cudaMemsetAsync(l.flag, 0, sizeof(int), st);
     cudaMemsetAsync(l.inst, 0, 4 * 8, st);
+    cudaMemsetAsync(l.red, 0, 4 * 8, st);
     cudaMemsetAsync(l.Xg, 0, (size_t)l.LP * l.LP * 16, st);
     cudaMemsetAsync(a->update_norm, 0, (size_t)(a->max_iter > 0 ? a->max_iter : 1) * 8, st);
     if (a->iterates) cudaMemsetAsync(a->iterates, 0, (size_t)a->N * 8, st);

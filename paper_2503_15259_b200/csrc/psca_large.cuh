@@ -65,7 +65,7 @@ struct LargeArgs {
     double2* dsig_part;         // [ks][NBLK][32]
     int ks, n_rtiles_lower;
     double2* dsig;              // [NBLK][32]   exchange buffer (all-reduced over ranks)
-    double* red;                // [4]          exchange: dx2 (sum), min q (min)
+    double* red;                // [4] exchange: dx2 (sum), prior partial (sum), min q (min)
     double2* dmat;              // [L][L] D
     double2* Xg;                // [LP][LP] Sigma, then P
     double2* Gg;                // [LP][LP]
@@ -82,6 +82,7 @@ __device__ __forceinline__ int lblock_base(int i) {   // rebuild C-block index o
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT, 2) quad_large(LargeArgs a) {
+    if (a.flag[0]) return;   // stopped: the step loop may run on without a host check
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* sm = reinterpret_cast<double2*>(smem_raw);
     constexpr int SB = QL_KC * QL_NC;          // S chunk
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(NT, 2) quad_large(LargeArgs a) {
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT) update_large(LargeArgs a) {
+    if (a.flag[0]) return;   // stopped: the step loop may run on without a host check
     __shared__ double sred[2 * NWARP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = blockIdx.x * NT + tid;
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(NT) rebuild_large(LargeArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* WS = reinterpret_cast<double2*>(smem_raw);   // [32 rows][32 slots]
     double2* SP = WS + 32 * RL_NC;                         // [64 rows][32 slots]
+    if (a.flag[0]) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r8 = lane >> 2, c4 = lane & 3;
     int rt = 0, cg = 0;
@@ -339,6 +342,7 @@ __global__ void __launch_bounds__(NT) rebuild_large(LargeArgs a) {
 
 // sums of the split partials -> exchange buffers (fixed orders)
 __global__ void __launch_bounds__(NT) reduce_large(LargeArgs a) {
+    if (a.flag[0]) return;   // stopped: the step loop may run on without a host check
     const int nblk32 = rebuild_block_count(a.NRB) * 32;
     const int e = blockIdx.x * NT + threadIdx.x;
     if (e < nblk32) {
@@ -356,8 +360,8 @@ __global__ void __launch_bounds__(NT) reduce_large(LargeArgs a) {
             s += a.red_part[2 * b];
             m = (a.red_part[2 * b + 1] < m) ? a.red_part[2 * b + 1] : m;
         }
-        a.red[0] = s;
-        a.red[1] = m;
+        a.red[0] = s;   // red[1] (prior partial) is left to prior_large
+        a.red[2] = m;
     }
 }
 
@@ -371,14 +375,15 @@ __global__ void finalize_large(LargeArgs a) {
     int flag = 0;
     if (a.status[0] != PSCA_RUNNING) {
         flag = 1;
-    } else if (a.red[1] < 0.5 * a.L / in[0]) {
+    } else if (a.red[2] < 0.5 * a.L / in[0]) {
         a.status[0] = PSCA_QFLOOR;
         a.n_iter[0] = k;
         flag = 1;
     } else {
         const double un = sqrt(a.red[0]);
         a.update_norm[k] = un;
-        if (a.objective) a.objective[k] = in[1] + in[2] + in[3];
+        // the prior penalty at x_k is the all-reduced red[1] (sum over column shards)
+        if (a.objective) a.objective[k] = in[1] + in[2] + a.red[1];
         a.n_iter[0] = k + 1;
         if (un < a.tol) {
             a.status[0] = PSCA_CONVERGED;
@@ -866,8 +871,9 @@ __global__ void __launch_bounds__(NT) prior_large(LargeArgs a, const double* xv)
     }
     if (gridDim.x == 1 && a.record_objective) {
         acc = block_sum(acc, sred);
+        // this shard's penalty: summed over the ranks with the next exchange
         if (threadIdx.x == 0)
-            a.inst[3] = (a.kind == PSCA_MAP_K) ? acc : (a.kind == PSCA_MAP_UR ? -acc / a.n_antennas : 0.0);
+            a.red[1] = (a.kind == PSCA_MAP_K) ? acc : (a.kind == PSCA_MAP_UR ? -acc / a.n_antennas : 0.0);
     }
 }
 

@@ -107,6 +107,10 @@ _SIGS = {
     "psca_empirical_cov": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                           ctypes.c_void_p]),
+    "psca_received": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                     ctypes.c_void_p]),
     "psca_cov_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "psca_cov_unknown": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
@@ -311,6 +315,39 @@ def empirical_cov(y, n_antennas: int):
            "psca_empirical_cov")
     res = out.cpu().numpy()
     return res[0] if single else res
+
+
+def received_t(S, active, gains, H, Z):
+    """Y = S[:, active] diag(sqrt(g[active])) H + Z on the device (psca_received).
+
+    S (B,L,N) c128, active (B,K) int, gains (B,N), H (B,K,M) c128, Z (B,L,M) c128,
+    all CUDA tensors (converted / made contiguous here); returns Y (B,L,M)."""
+    torch = _torch()
+    lib = load()
+    dev = S.device
+    S = S.to(torch.complex128).contiguous()
+    A = active.to(device=dev, dtype=torch.int32).contiguous()
+    g = gains.to(device=dev, dtype=torch.float64).contiguous()
+    H = H.to(device=dev, dtype=torch.complex128).contiguous()
+    Z = Z.to(device=dev, dtype=torch.complex128).contiguous()
+    B, L, N = S.shape
+    K, M = H.shape[1], H.shape[2]
+    Y = torch.empty((B, L, M), dtype=torch.complex128, device=dev)
+    _check(lib.psca_received(_ptr(S), _ptr(A), _ptr(g), _ptr(H), _ptr(Z), B, L, N, K, M,
+                             _ptr(Y), _stream(torch)), "psca_received")
+    return Y
+
+
+def empirical_cov_t(Y, n_antennas: int):
+    """Sigma_hat = Y Y^H / M for a device tensor Y (B,L,M); returns (B,L,L)."""
+    torch = _torch()
+    lib = load()
+    Y = Y.to(torch.complex128).contiguous()
+    B, L, Mc = Y.shape
+    out = torch.empty((B, L, L), dtype=torch.complex128, device=Y.device)
+    _check(lib.psca_empirical_cov(_ptr(Y), B, L, Mc, int(n_antennas), _ptr(out), _stream(torch)),
+           "psca_empirical_cov")
+    return out
 
 
 def cov_unknown_t(S, W, Nz):

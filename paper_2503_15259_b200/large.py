@@ -7,17 +7,20 @@ C ABI ``psca_large_*`` entry points (csrc/psca_large.cuh):
     stepper.begin()                       x = 0, Sigma_0 = sigma^2 I, factor
     for k in range(T):
         stepper.columns(k)                this rank's columns: quad forms, update,
-                                          partial Sigma increment, (dx2, min q)
-        all_reduce(increment, SUM); all_reduce(dx2, SUM); all_reduce(min q, MIN)
+                                          partial Sigma increment, dx2, prior, min q
+        all_reduce([increment | dx2 | prior], SUM); all_reduce(min q, MIN)
         stepper.factor(k)                 finalise k, factor Sigma_{k+1}
-        if stepper.stopped(): break
+        every 8 iterations: if stepper.stopped(): break
 
 With ``group=None`` (one GPU) the all-reduces are skipped.  With a
 torch.distributed process group (NCCL, one process per GPU) each rank holds
 a contiguous block of columns (devices) of the one instance; the exchange is
-one all-reduce of the L x L partial increment (about 0.5 MiB at L = 256 in
-C-fragment form) plus two scalars per iteration.  The factorisation is
-replicated, so every rank holds identical P'/A' fragments.
+ONE sum all-reduce of a contiguous block -- the L x L partial increment
+(about 0.5 MiB at L = 256 in C-fragment form), sum dx^2 and the shard's prior
+penalty -- and one min all-reduce of min q per iteration.  The factorisation
+is replicated, so every rank holds identical P'/A' fragments.  Every kernel of
+the step is gated on the device stop flag, so the loop checks the flag on the
+host only every ``check_every`` iterations (no per-iteration synchronisation).
 
 ``ShardedDriver`` only talks to a stepper object; tests drive it with a numpy
 stepper over gloo (tests/test_sharded_cpu.py) to check the protocol.
@@ -123,7 +126,9 @@ class GpuLargeStepper:
                                                    ctypes.byref(dsig), ctypes.byref(n),
                                                    ctypes.byref(red)), "psca_large_exchange")
         base = self.ws.data_ptr()
-        self.dsig = self.ws[dsig.value - base: dsig.value - base + 8 * n.value].view(f64)
+        assert red.value == dsig.value + 8 * n.value, "exchange block must be contiguous"
+        self.xsum = self.ws[dsig.value - base: dsig.value - base + 8 * (n.value + 2)].view(f64)
+        self.dsig = self.xsum[:n.value]
         self.red = self.ws[red.value - base: red.value - base + 32].view(f64)
         fp = ctypes.c_void_p()
         device._check(self.lib.psca_large_flag(ctypes.byref(self.args), self._ws(),
@@ -150,8 +155,8 @@ class GpuLargeStepper:
         self._call("psca_large_factor", ctypes.c_int(k))
 
     def exchange(self):
-        """(sum-reduced tensor, sum-reduced scalar, min-reduced scalar) for the all-reduce."""
-        return self.dsig, self.red[0:1], self.red[1:2]
+        """(sum-reduced block [increment | dx2 | prior], min-reduced [min q]) views."""
+        return self.xsum, self.red[2:3]
 
     def stopped(self) -> bool:
         return bool(self.flag.item())
@@ -170,10 +175,11 @@ class GpuLargeStepper:
 class ShardedDriver:
     """PSCA step loop with optional column sharding over a process group."""
 
-    def __init__(self, stepper, group=None, dist=None):
+    def __init__(self, stepper, group=None, dist=None, check_every: int = 8):
         self.stepper = stepper
         self.group = group
         self.dist = dist
+        self.check_every = max(1, int(check_every))
         if group is not None and dist is None:
             import torch.distributed as dist_mod
             self.dist = dist_mod
@@ -184,13 +190,14 @@ class ShardedDriver:
         for k in range(max_iter):
             st.columns(k)
             if self.group is not None:
-                inc, dx2, minq = st.exchange()
+                xsum, minq = st.exchange()
                 d = self.dist
-                d.all_reduce(inc, op=d.ReduceOp.SUM, group=self.group)
-                d.all_reduce(dx2, op=d.ReduceOp.SUM, group=self.group)
+                d.all_reduce(xsum, op=d.ReduceOp.SUM, group=self.group)
                 d.all_reduce(minq, op=d.ReduceOp.MIN, group=self.group)
             st.factor(k)
-            if st.stopped():
+            # the stop flag is replicated on every rank (it follows from reduced
+            # values), so all ranks leave at the same k
+            if (k + 1) % self.check_every == 0 and k + 1 < max_iter and st.stopped():
                 break
         return st.result()
 

@@ -76,8 +76,9 @@ def _cn(rng: np.random.Generator, shape) -> np.ndarray:
     return z * np.sqrt(0.5)
 
 
-def make_scene(cfg: SceneConfig, instance: int, pilot_len: int | None = None) -> Sample:
-    """Instance ``instance`` of configuration ``cfg`` (deterministic)."""
+def draw_scene(cfg: SceneConfig, instance: int, pilot_len: int | None = None) -> dict:
+    """The host random draws of instance ``instance`` (the scene contract: one
+    Philox stream per instance, draw order pilots, distances, active set, H, Z)."""
     l = cfg.pilot_len if pilot_len is None else pilot_len
     n, m, k = cfg.n_devices, cfg.n_antennas, cfg.n_active
     seed = np.random.SeedSequence([cfg.config_id, l, instance])
@@ -86,15 +87,52 @@ def make_scene(cfg: SceneConfig, instance: int, pilot_len: int | None = None) ->
     u = rng.random(n)
     d = np.sqrt(D_INNER_KM ** 2 + u * (D_OUTER_KM ** 2 - D_INNER_KM ** 2))
     active = np.sort(rng.choice(n, size=k, replace=False))
-    g = gains_from_distance(d)
-    alpha = np.zeros(n)
-    alpha[active] = 1.0
     h = _cn(rng, (k, m))
     z = _cn(rng, (l, m))
+    return {"pilots": pilots, "gains": gains_from_distance(d), "active": active, "h": h, "z": z}
+
+
+def make_scene(cfg: SceneConfig, instance: int, pilot_len: int | None = None) -> Sample:
+    """Instance ``instance`` of configuration ``cfg`` (deterministic; host arithmetic,
+    used by the golden-fixture generator and as the CPU-side reference of
+    ``make_batch_device``)."""
+    f = draw_scene(cfg, instance, pilot_len)
+    pilots, g, active, h, z = f["pilots"], f["gains"], f["active"], f["h"], f["z"]
+    n, m = cfg.n_devices, cfg.n_antennas
+    alpha = np.zeros(n)
+    alpha[active] = 1.0
     y = (pilots[:, active] * np.sqrt(g[active])) @ h + z
     emp = (y @ y.conj().T) / m
     return Sample(pilots=pilots, gains=g, activities=alpha, eff_pathloss=alpha * g,
                   received=y, emp_cov=emp, noise_power=1.0)
+
+
+def make_batch_device(cfg: SceneConfig, instances, draws=None) -> dict:
+    """A batch of instances with the covariances formed on the GPU.
+
+    The random draws stay on the host (``draw_scene``; pass ``draws`` to reuse
+    draws made elsewhere, e.g. in worker processes); Y = S_A diag(sqrt(g_A)) H + Z
+    and Sigma_hat = Y Y^H / M run on the FP64 tensor pipe (psca_received,
+    psca_empirical_cov).  Returns device tensors pilots, gains, emp_cov, noise,
+    received and the host activities."""
+    import torch
+    from . import device
+    if draws is None:
+        draws = [draw_scene(cfg, int(i)) for i in instances]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    st = lambda key, dt: torch.from_numpy(np.ascontiguousarray(   # noqa: E731
+        np.stack([f[key] for f in draws]).astype(dt))).to(dev)
+    S, g, H, Z = (st("pilots", np.complex128), st("gains", np.float64), st("h", np.complex128),
+                  st("z", np.complex128))
+    A = st("active", np.int32)
+    Y = device.received_t(S, A, g, H, Z)
+    E = device.empirical_cov_t(Y, cfg.n_antennas)
+    act = np.zeros((len(draws), cfg.n_devices))
+    for b, f in enumerate(draws):
+        act[b, f["active"]] = 1.0
+    return {"pilots": S, "gains": g, "emp_cov": E, "received": Y,
+            "noise": torch.ones(len(draws), dtype=torch.float64, device=dev),
+            "activities": act, "n_antennas": cfg.n_antennas}
 
 
 def net_steps(n_blocks: int, seed: int = 2) -> np.ndarray:
