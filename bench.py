@@ -149,6 +149,50 @@ def generate(name: str, ids: list[int], workers: int):
     return out
 
 
+def _draw_chunk(args):
+    name, ids = args
+    from paper_2503_15259_b200 import scenes
+    cfg = scenes.BASELINE_CONFIGS[name]
+    return [scenes.draw_scene(cfg, i) for i in ids]
+
+
+def generate_device(name: str, ids: list[int], workers: int):
+    """Seeded scenes with the covariances formed on the GPU: the Philox draws in
+    host processes, Y = S_A diag(sqrt(g_A)) H + Z and Sigma_hat = Y Y^H / M on
+    DMMA (scenes.make_batch_device).  Returns (device batch, host arrays for
+    the e2e arm, timing dict)."""
+    import multiprocessing as mp
+    import numpy as np
+    import torch
+    from paper_2503_15259_b200 import scenes
+    cfg = scenes.BASELINE_CONFIGS[name]
+    t0 = time.perf_counter()
+    chunks = [ids[i:i + 64] for i in range(0, len(ids), 64)]
+    if workers > 1 and len(chunks) > 1:
+        with mp.get_context("fork").Pool(min(workers, len(chunks))) as pool:
+            parts = pool.map(_draw_chunk, [(name, c) for c in chunks])
+    else:
+        parts = [_draw_chunk((name, c)) for c in chunks]
+    draws = [d for part in parts for d in part]
+    t_draw = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dev = scenes.make_batch_device(cfg, ids, draws=draws)
+    e1.record()
+    torch.cuda.synchronize()
+    host = {"pilots": np.stack([d["pilots"] for d in draws]),
+            "gains": np.stack([d["gains"] for d in draws]),
+            "emp_cov": dev["emp_cov"].cpu().numpy(), "noise": dev["noise"].cpu().numpy(),
+            "activities": dev["activities"], "n_antennas": cfg.n_antennas}
+    timing = {"host_draws_s": t_draw, "host_draw_workers": workers,
+              "device_cov_ms": e0.elapsed_time(e1),
+              "note": "Philox draws on the host (the scene contract), Y and Sigma_hat on the "
+                      "FP64 tensor pipe incl. the host-to-device copy of the draws "
+                      "(psca_received + psca_empirical_cov); outside the timed solve region"}
+    return dev, host, timing
+
+
 # ---------------------------------------------------------------------------
 # CPU baseline (oracle, one process per core, OPENBLAS_NUM_THREADS=1)
 # ---------------------------------------------------------------------------
@@ -435,14 +479,15 @@ def ours_arm(args):
     cfg, problem = wl.cfg, wl.problem
     B, iters = wl.batch, wl.iters
     ids = list(range(rank * B, (rank + 1) * B))
-    host = generate(wl.scene_name, ids, os.cpu_count() or 1)
+    devb, host, gen_timing = generate_device(wl.scene_name, ids, os.cpu_count() or 1)
     dev = torch.device("cuda", torch.cuda.current_device())
     pil_h = torch.from_numpy(host["pilots"]).pin_memory()
     emp_h = torch.from_numpy(host["emp_cov"]).pin_memory()
     noi_h = torch.from_numpy(host["noise"]).pin_memory()
     gain_h = torch.from_numpy(host["gains"]).pin_memory() if wl.known else None
-    pil_d, emp_d, noi_d = (t.to(dev) for t in (pil_h, emp_h, noi_h))
-    gain_d = gain_h.to(dev) if gain_h is not None else None
+    pil_d, emp_d, noi_d = devb["pilots"], devb["emp_cov"], devb["noise"]
+    gain_d = devb["gains"] if wl.known else None
+    del devb
     m = int(host["n_antennas"])
 
     def barrier():
@@ -577,6 +622,7 @@ def ours_arm(args):
             "psca_iters_per_s": value * iters,
             "ms_per_iteration": ms / args.steps / iters,
             "roofline": roofline,
+            "generation": gen_timing,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
@@ -607,13 +653,22 @@ def c4_arm(args):
     from paper_2503_15259_b200 import estimators, large, scenes
     cfg = scenes.BASELINE_CONFIGS["c4"]
     T = args.iters or cfg.n_iter
-    s = scenes.make_scene(cfg, 0)
     sl = large.column_shard(cfg.n_devices, rank, world)
     steps = estimators.default_steps(T)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    S = torch.from_numpy(np.ascontiguousarray(s.pilots[:, sl])).to(dev)
-    g = torch.from_numpy(np.ascontiguousarray(s.gains[sl])).to(dev)
-    E = torch.from_numpy(s.emp_cov).to(dev)
+    # scene: host Philox draws, Y (256 x 2500 x 512 complex GEMM) and Sigma_hat on DMMA
+    t0 = time.perf_counter()
+    draws = [scenes.draw_scene(cfg, 0)]
+    t_draw = time.perf_counter() - t0
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    dv = scenes.make_batch_device(cfg, [0], draws=draws)
+    g1.record()
+    torch.cuda.synchronize()
+    gen_timing = {"host_draws_s": t_draw, "device_cov_ms": g0.elapsed_time(g1)}
+    S = dv["pilots"][0][:, sl].contiguous()
+    g = dv["gains"][0][sl].contiguous()
+    E = dv["emp_cov"][0].contiguous()
+    del dv, draws
 
     def run():
         st = large.GpuLargeStepper("ml-k", S, g, E, 1.0, cfg.n_antennas, steps, max_iter=T)
@@ -654,6 +709,9 @@ def c4_arm(args):
                                    "the Sigma increment per iteration",
                        "parallelism": f"column shards x{world}"},
             "algorithmic_tflops": flops / (ms * 1e-3) / 1e12,
+            "algorithmic_note": "24 N L^2 per iteration (SURVEY.md 8(d)) over the device "
+                                "time of the whole step loop",
+            "generation": gen_timing,
             "gpu_launches": launches, "status": res["status"], "n_iter": res["n_iter"]}),
             flush=True)
     if group is not None:

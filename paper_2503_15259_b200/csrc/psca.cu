@@ -1762,6 +1762,7 @@ struct LargeLayout {
     double2* Ag;
     double* inst;
     int* flag;
+    double* frob_part;
     int LP, NRB, NBLK, n_red, ks, ntiles;
     size_t total;
 };
@@ -1798,6 +1799,7 @@ LargeLayout large_layout(const psca_large_args* a, void* ws) {
     l.Gg = cv.take<double2>((size_t)l.LP * l.LP * 16);
     l.Ag = cv.take<double2>((size_t)l.LP * l.LP * 16);
     l.inst = cv.take<double>(4 * 8);
+    l.frob_part = cv.take<double>(FROB_CTAS * 8);
     l.flag = cv.take<int>(sizeof(int));
     l.total = cv.off;
     return l;
@@ -1820,7 +1822,7 @@ LargeArgs large_kargs(const psca_large_args* a, const LargeLayout& l, int k) {
     g.frags = l.frags; g.q_part = l.q_part; g.r_part = l.r_part; g.v = l.v; g.pgrad = l.pgrad;
     g.red_part = l.red_part; g.n_red = l.n_red; g.dsig_part = l.dsig_part; g.ks = l.ks;
     g.n_rtiles_lower = l.ntiles; g.dsig = l.dsig; g.red = l.red; g.dmat = l.dmat; g.Xg = l.Xg;
-    g.Gg = l.Gg; g.Ag = l.Ag; g.inst = l.inst; g.flag = l.flag;
+    g.Gg = l.Gg; g.Ag = l.Ag; g.inst = l.inst; g.flag = l.flag; g.frob_part = l.frob_part;
     return g;
 }
 
@@ -1852,15 +1854,15 @@ int large_factor_chain(const LargeArgs& g, const LargeLayout& l, const double* x
         PSCA_K((prior_large<<<1, NT, 0, st>>>(g, x_new)));
     PSCA_K((assemble_large<<<(nblk32 + NT - 1) / NT, NT, 0, st>>>(g)));
     PSCA_K((finish_sigma_large<<<(l.LP * l.LP + NT - 1) / NT, NT, 0, st>>>(g)));
-    PSCA_K((frob_large<<<1, NT, 0, st>>>(g)));
+    PSCA_K((frob_large<<<FROB_CTAS, NT, 0, st>>>(g)));
     {
         const size_t sm = (size_t)8 * l.LP * 16;   // [2 phases][4 pivot columns][LP]
         PSCA_K((gj_cluster<<<GJ_CL, GJ_NT, sm, st>>>(g)));
     }
     if (g.record_objective) PSCA_K((trace_large<<<1, NT, 0, st>>>(g)));
-    const int nbl = l.LP / 2;
-    PSCA_K((gemm_large<0><<<(nbl * nbl + NT - 1) / NT, NT, 0, st>>>(g)));
-    PSCA_K((gemm_large<1><<<(nbl * (nbl + 1) / 2 + NT - 1) / NT, NT, 0, st>>>(g)));
+    const int nrt = l.LP / 4;
+    PSCA_K((gemm_large<0><<<(nrt * (l.LP / 8) + NWARP - 1) / NWARP, NT, 0, st>>>(g)));
+    PSCA_K((gemm_large<1><<<(rebuild_block_count(nrt) + NWARP - 1) / NWARP, NT, 0, st>>>(g)));
     const int nb8 = l.NRB * (l.NRB + 1) * 8;
     PSCA_K((pack_large<<<(nb8 + NT - 1) / NT, NT, 0, st>>>(g)));
     return PSCA_OK;

@@ -36,6 +36,8 @@ constexpr int RL_NC = 32;    // columns per rebuild chunk
 constexpr int GJ_CL = 8;     // CTAs per GJ cluster
 constexpr int GJ_NT = 512;   // threads per GJ CTA
 
+constexpr int FROB_CTAS = 64;   // frob_large partial sums
+
 struct LargeArgs {
     int kind, N, L, LP, NRB, T, n_antennas, record_objective, k;
     double tol, noise;
@@ -72,6 +74,7 @@ struct LargeArgs {
     double2* Ag;                // [LP][LP]
     double* inst;               // [4] frob, logdet, trace, prior value
     int* flag;                  // [1] finalize decision
+    double* frob_part;          // [FROB_CTAS] partial sums of |Sigma_ij|^2
 };
 
 __device__ __forceinline__ int lblock_base(int i) {   // rebuild C-block index of (i, 0)
@@ -371,7 +374,12 @@ __global__ void __launch_bounds__(NT) reduce_large(LargeArgs a) {
 __global__ void finalize_large(LargeArgs a) {
     // flag: 0 continue, 1 stop (frozen / done)
     const int k = a.k;
-    const double* in = a.inst;
+    double* in = a.inst;
+    {
+        double s = 0.0;
+        for (int c = 0; c < FROB_CTAS; ++c) s += a.frob_part[c];
+        in[0] = sqrt(s);
+    }
     int flag = 0;
     if (a.status[0] != PSCA_RUNNING) {
         flag = 1;
@@ -445,17 +453,21 @@ __global__ void __launch_bounds__(NT) finish_sigma_large(LargeArgs a) {
 }
 
 // Frobenius norm of Sigma and (optionally) the prior terms; one CTA
+// ||Sigma||_F: FROB_CTAS partial sums (row slices), combined in fixed order by
+// finalize_large of the next iteration (the q-floor is its only reader)
 __global__ void __launch_bounds__(NT) frob_large(LargeArgs a) {
     __shared__ double sred[SRED];
     if (a.flag[0]) return;
     double s = 0.0;
-    for (int e = threadIdx.x; e < a.L * a.L; e += NT) {
-        const int i = e / a.L, j = e % a.L;
+    const int rows = (a.L + FROB_CTAS - 1) / FROB_CTAS;
+    const int r0 = blockIdx.x * rows, r1 = min(a.L, r0 + rows);
+    for (int e = threadIdx.x; e < (r1 - r0) * a.L; e += NT) {
+        const int i = r0 + e / a.L, j = e % a.L;
         const double2 v = a.Xg[(size_t)i * a.LP + j];
         s = fma(v.x, v.x, fma(v.y, v.y, s));
     }
     s = block_sum(s, sred);
-    if (threadIdx.x == 0) a.inst[0] = sqrt(s);
+    if (threadIdx.x == 0) a.frob_part[blockIdx.x] = s;
 }
 
 // Sweep-operator Gauss-Jordan on an 8-CTA cluster (see header comment).
@@ -790,49 +802,57 @@ gj_cluster(LargeArgs a) {
 }
 
 // G = Sigma_hat P (all 2x2 blocks, MODE 0) or A = P G (lower 2x2 blocks, MODE 1)
+// G = Sigma_hat P (MODE 0, all tiles) and A = P G (MODE 1, lower tiles) on
+// DMMA: one warp per 4 x 8 complex output tile in the real 2x2 expansion
+// (see factor_pass), k-steps of 2 complex columns, two accumulator chains
 template <int MODE>
 __global__ void __launch_bounds__(NT) gemm_large(LargeArgs a) {
     if (a.flag[0] || a.status[0] != PSCA_RUNNING) return;
-    const int L = a.L, LP = a.LP, nbl = LP / 2;
-    const int t = blockIdx.x * NT + threadIdx.x;
-    int bi, bj;
+    const int L = a.L, LP = a.LP;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * NWARP + warp;
+    const int nrt = LP / 4, nct = LP / 8;
+    int ti, tj;
     if (MODE == 0) {
-        if (t >= nbl * nbl) return;
-        bi = t / nbl;
-        bj = t % nbl;
+        if (tile >= nrt * nct) return;
+        ti = tile / nct;
+        tj = tile - ti * nct;
     } else {
-        if (t >= nbl * (nbl + 1) / 2) return;
-        lower_block(t, bi, bj);
-    }
-    const int i0 = 2 * bi, j0 = 2 * bj;
-    double2 c[2][2];
-#pragma unroll
-    for (int di = 0; di < 2; ++di)
-#pragma unroll
-        for (int dj = 0; dj < 2; ++dj) c[di][dj] = make_double2(0.0, 0.0);
-    for (int k = 0; k < L; ++k) {
-        double2 x0, x1, y0, y1;
-        if (MODE == 0) {
-            x0 = (i0 < L) ? __ldg(a.emp_cov + (size_t)i0 * L + k) : make_double2(0.0, 0.0);
-            x1 = (i0 + 1 < L) ? __ldg(a.emp_cov + (size_t)(i0 + 1) * L + k) : make_double2(0.0, 0.0);
-            y0 = a.Xg[(size_t)k * LP + j0];
-            y1 = a.Xg[(size_t)k * LP + j0 + 1];
-        } else {
-            x0 = a.Xg[(size_t)i0 * LP + k];
-            x1 = a.Xg[(size_t)(i0 + 1) * LP + k];
-            y0 = a.Gg[(size_t)k * LP + j0];
-            y1 = a.Gg[(size_t)k * LP + j0 + 1];
+        if (tile >= rebuild_block_count(nrt)) return;
+        int i = 0, base = 0;
+        while (base + (4 * i + 3) / 8 + 1 <= tile) {
+            base += (4 * i + 3) / 8 + 1;
+            ++i;
         }
-        c[0][0] = cfma(x0, y0, c[0][0]);
-        c[0][1] = cfma(x0, y1, c[0][1]);
-        c[1][0] = cfma(x1, y0, c[1][0]);
-        c[1][1] = cfma(x1, y1, c[1][1]);
+        ti = i;
+        tj = tile - base;
     }
-    double2* out = (MODE == 0) ? a.Gg : a.Ag;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const int p = r8 & 1, q = c4 & 1;
+    const unsigned long long sg = (p == 0 && q == 1) ? 0x8000000000000000ull : 0ull;
+    const int l = 4 * ti + (r8 >> 1);
+    const int mb = 8 * tj + r8;
+    const double* Ad = reinterpret_cast<const double*>(MODE == 0 ? a.emp_cov : a.Xg);
+    const int lda = (MODE == 0) ? L : LP;
+    const double* Bd = reinterpret_cast<const double*>(MODE == 0 ? a.Xg : a.Gg);
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int kmax = (MODE == 0) ? L : LP;
+    const int nks = (kmax + 1) / 2;
+#pragma unroll 4
+    for (int ks = 0; ks < nks; ++ks) {
+        const int kc = 2 * ks + (c4 >> 1);
+        const double av = (l < (MODE == 0 ? L : LP) && kc < kmax)
+                              ? xsign(__ldg(Ad + 2 * ((size_t)l * lda + kc) + (p ^ q)), sg)
+                              : 0.0;
+        const double bv = (kc < kmax) ? Bd[2 * ((size_t)kc * LP + mb) + q] : 0.0;
+        dmma(acc[ks & 1], av, bv);
+    }
+    double* out = reinterpret_cast<double*>(MODE == 0 ? a.Gg : a.Ag);
 #pragma unroll
-    for (int di = 0; di < 2; ++di)
-#pragma unroll
-        for (int dj = 0; dj < 2; ++dj) out[(size_t)(i0 + di) * LP + j0 + dj] = c[di][dj];
+    for (int h = 0; h < 2; ++h) {
+        const int m = 8 * tj + 2 * c4 + h;
+        out[2 * ((size_t)l * LP + m) + p] = acc[0][h] + acc[1][h];
+    }
 }
 
 // trace(P Sigma_hat) for the objective; one CTA
