@@ -1223,8 +1223,8 @@ __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
 #include "psca_large.cuh"
 #include "psca_bcd.cuh"
 #include "psca_components.cuh"
-#include "psca_facw.cuh"
 #include "psca_scene.cuh"
+#include "psca_facw.cuh"
 
 // ---------------------------------------------------------------------------
 // empirical covariance (HERK): Sigma_hat = Y Y^H / M
@@ -1943,11 +1943,12 @@ size_t psca_solve_workspace_bytes(const psca_solve_args* a) {
     return solve_layout(a, g, resolved_chunks(a), nullptr).total;
 }
 
-int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes, void* stream) {
-    int rc = check_solve_args(a);
-    if (rc != PSCA_OK) return rc;
+// the whole launch sequence of one solve on stream st (psca_solve below wraps
+// it with the CUDA-graph cache)
+static int solve_enqueue(const psca_solve_args* a, void* workspace, size_t workspace_bytes,
+                         cudaStream_t st) {
+    int rc = PSCA_OK;
     g_launches = 0;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     const Geo g = make_geo(a->L, solve_nrb(a->L));
     const int n_chunks = resolved_chunks(a);
     SolveLayout lay = solve_layout(a, g, n_chunks, workspace);
@@ -2082,6 +2083,90 @@ int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes
             return PSCA_E_CUDA;
     }
     return cudaGetLastError() == cudaSuccess ? PSCA_OK : PSCA_E_CUDA;
+}
+
+// CUDA-graph cache of the launch sequence (latency-bound small batches, e.g.
+// BASELINE c0's 201 launches per solve): keyed by the full argument struct and
+// the workspace, a solve seen twice with identical arguments is captured once
+// (on a private stream, thread-local capture) and then replayed with one
+// cudaGraphLaunch.  Off while per-launch profiling is on, or with
+// PSCA_NO_GRAPH=1.  The first sight of an argument set launches directly (so
+// every kernel attribute is set outside capture).
+struct GraphEntry {
+    psca_solve_args args;
+    void* ws;
+    size_t ws_bytes;
+    int dev;
+    int launches;
+    int path;
+    cudaGraphExec_t exec;
+};
+thread_local std::vector<GraphEntry> g_graphs;
+thread_local cudaStream_t g_capture_stream = nullptr;
+constexpr size_t GRAPH_CACHE = 8;
+
+static bool graph_eligible(const psca_solve_args* a) {
+    static const bool off = [] {
+        const char* e = getenv("PSCA_NO_GRAPH");
+        return e && e[0] == '1';
+    }();
+    return !off && !g_prof.on && a->B > 0 && a->B < sm_count() && a->fault_iter <= 0;
+}
+
+int psca_solve(const psca_solve_args* a, void* workspace, size_t workspace_bytes, void* stream) {
+    int rc = check_solve_args(a);
+    if (rc != PSCA_OK) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!graph_eligible(a)) return solve_enqueue(a, workspace, workspace_bytes, st);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    GraphEntry* hit = nullptr;
+    for (GraphEntry& e : g_graphs)
+        if (e.ws == workspace && e.ws_bytes == workspace_bytes && e.dev == dev &&
+            std::memcmp(&e.args, a, sizeof(*a)) == 0)
+            hit = &e;
+    if (hit && hit->exec) {
+        if (!ok_or_record(cudaGraphLaunch(hit->exec, st))) return PSCA_E_CUDA;
+        g_launches = hit->launches;
+        g_last_path = hit->path;
+        return PSCA_OK;
+    }
+    if (!hit) {   // first sight: direct launches, remember the argument set
+        rc = solve_enqueue(a, workspace, workspace_bytes, st);
+        if (rc != PSCA_OK) return rc;
+        if (g_graphs.size() >= GRAPH_CACHE) {
+            if (g_graphs.front().exec) cudaGraphExecDestroy(g_graphs.front().exec);
+            g_graphs.erase(g_graphs.begin());
+        }
+        g_graphs.push_back(GraphEntry{*a, workspace, workspace_bytes, dev, 0, 0, nullptr});
+        return PSCA_OK;
+    }
+    // second sight: capture the sequence on a private stream, then replay it on st
+    if (!g_capture_stream &&
+        !ok_or_record(cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking)))
+        return PSCA_E_CUDA;
+    if (!ok_or_record(cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeThreadLocal)))
+        return PSCA_E_CUDA;
+    rc = solve_enqueue(a, workspace, workspace_bytes, g_capture_stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(g_capture_stream, &graph);
+    cudaGetLastError();   // a failed capture is not an error of the solve
+    if (rc != PSCA_OK || ce != cudaSuccess || !graph) {
+        if (graph) cudaGraphDestroy(graph);
+        return solve_enqueue(a, workspace, workspace_bytes, st);
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+        cudaGetLastError();
+        return solve_enqueue(a, workspace, workspace_bytes, st);
+    }
+    hit->exec = exec;
+    hit->launches = g_launches;
+    hit->path = g_last_path;
+    if (!ok_or_record(cudaGraphLaunch(exec, st))) return PSCA_E_CUDA;
+    return PSCA_OK;
 }
 
 int psca_empirical_cov(const double* y, int B, int L, int Mc, int n_antennas, double* out,

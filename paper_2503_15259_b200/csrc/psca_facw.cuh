@@ -205,6 +205,114 @@ __device__ __forceinline__ void dispatch_col(int j, F&& f) {
     }
 }
 
+// The sweep of one instance by one warp, the matrix in acc (lower 4 x 8
+// complex tiles, DMMA C-fragment layout); wsm = this warp's TWS::WARP_SMEM
+// bytes of shared scratch.  Returns false when a pivot block is not PD.
+template <int NRB>
+__device__ __forceinline__ bool warp_sweep(double (&acc)[rebuild_block_count(NRB)][2],
+                                           unsigned char* wsm, int L, bool want_logdet,
+                                           double& logdet) {
+    using S = TWS<NRB>;
+    constexpr int LP = S::LP, LPC = S::LPC, NTL = S::NTL;
+    const int lane = threadIdx.x & 31;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const int p = r8 & 1, q = c4 & 1, kc = c4 >> 1;
+    double2* ub = reinterpret_cast<double2*>(wsm);                                // [2][LPC]
+    double2* cs = ub + 2 * LPC;                                                   // [2][2][LPC]
+    double* kv = reinterpret_cast<double*>(cs + 4 * LPC);                         // [2][4]
+    const double* Ud = reinterpret_cast<const double*>(ub);
+    const int abase = 2 * (kc * LPC + (r8 >> 1)) + (p ^ q);
+    const int bbase = 2 * (kc * LPC + r8) + q;
+    // Rows of the pivot block are never zeroed in the staged columns: their A
+    // operand lanes are masked in the DMMA and their U_j is zero by definition.
+    const int rl = r8 >> 1;
+    const SwLane sw{rl, c4, p};
+    auto stage = [&](int k2, int dst) {
+        double* Cn = reinterpret_cast<double*>(cs + dst * 2 * LPC);
+        double* kd = kv + dst * 4;
+        const int dl = rl - (k2 & 3);
+        const bool rlane = (unsigned)dl < 2u, clane = c4 == ((k2 & 7) >> 1);
+        const int kcl = k2 >> 3;
+        dispatch_col<S::NCJ>(kcl, [&](auto J) { stage_col<NRB, J.value>(acc, sw, clane, k2, Cn, LPC); });
+        dispatch_row<NRB>(k2 >> 2, [&](auto I) {
+            stage_row<NRB, I.value>(acc, sw, rlane, dl, k2, kcl, clane, Cn, kd, LPC);
+        });
+    };
+    stage(0, 0);
+    __syncwarp();
+    logdet = 0.0;
+    bool ok = true;
+    const int LE = (L + 1) & ~1;
+    const unsigned long long sgn = (p == 0 && q == 1) ? 0ull : 0x8000000000000000ull;
+    double* nm = kv + 8;   // -M as 2x2 complex: Ud[12 LPC + 8 + 2 (2 dl + h) + p]
+    for (int k = 0; k < LE; k += 2) {
+        const int ph = (k >> 1) & 1;
+        const double2* cc = cs + ph * 2 * LPC;
+        const double* Cd = reinterpret_cast<const double*>(cc);
+        const double ka = kv[ph * 4 + 0], kbr = kv[ph * 4 + 1], kbi = kv[ph * 4 + 2],
+                     kcc = kv[ph * 4 + 3];
+        const double det = fma(ka, kcc, -fma(kbr, kbr, kbi * kbi));
+        if (!(ka > 0.0) || !(det > 0.0)) {
+            ok = false;
+            break;
+        }
+        if (want_logdet) logdet += log(det);
+        {
+            const double dinv = __drcp_rn(det);
+            const double m00 = kcc * dinv;
+            const double m11 = ka * dinv;
+            const double2 m10 = make_double2(-kbr * dinv, -kbi * dinv);
+            const double2 m01 = make_double2(m10.x, -m10.y);
+#pragma unroll
+            for (int j = lane; j < LP; j += 32) {
+                double2 u0 = make_double2(0.0, 0.0), u1 = make_double2(0.0, 0.0);
+                if (j != k && j != k + 1) {   // U_K = 0 (C_K is K itself, not zeroed)
+                    const double2 pp = cc[j], qq = cc[LPC + j];
+                    u0 = make_double2(fma(m01.x, qq.x, fma(m01.y, qq.y, m00 * pp.x)),
+                                      fma(m01.y, qq.x, fma(-m01.x, qq.y, -m00 * pp.y)));
+                    u1 = make_double2(fma(m11, qq.x, fma(m10.x, pp.x, m10.y * pp.y)),
+                                      fma(-m11, qq.y, fma(m10.y, pp.x, -m10.x * pp.y)));
+                }
+                ub[j] = u0;
+                ub[LPC + j] = u1;
+            }
+            if (lane < 8) {   // -M: (dl, h) = (0,0) (0,1) (1,0) (1,1), component p = lane & 1
+                const int e = lane >> 1, pp = lane & 1;
+                const double re = e == 0 ? m00 : (e == 1 ? m01.x : (e == 2 ? m10.x : m11));
+                const double im = (e == 1) ? m01.y : (e == 2 ? m10.y : 0.0);
+                nm[lane] = -(pp ? im : re);
+            }
+        }
+        __syncwarp();
+        const int kr = k >> 2, kcl = k >> 3, dl = rl - (k & 3);
+        const bool rlane = (unsigned)dl < 2u, clane = c4 == ((k & 7) >> 1);
+        // rank-2 trailing update: one DMMA per tile (operands shared per row /
+        // column tile; the K rows' A lanes masked)
+        {
+            double af[NRB], bfr[S::NCJ];
+#pragma unroll
+            for (int i = 0; i < NRB; ++i)
+                af[i] = (i == kr && rlane) ? 0.0 : xsign(Cd[abase + 8 * i], sgn);
+#pragma unroll
+            for (int j = 0; j < S::NCJ; ++j) bfr[j] = Ud[bbase + 16 * j];
+            int ti = 0, tj = 0;
+#pragma unroll
+            for (int t = 0; t < NTL; ++t) {
+                dmma(acc[t], af[ti], bfr[tj]);
+                TILE_NEXT(ti, tj)
+            }
+        }
+        // the K columns (conj(U_l)), then the K rows (U_m) and the K block (-M)
+        dispatch_col<S::NCJ>(kcl, [&](auto J) { fix_col<NRB, J.value>(acc, sw, clane, Ud, LPC); });
+        dispatch_row<NRB>(kr, [&](auto I) {
+            fix_row<NRB, I.value>(acc, sw, rlane, dl, kcl, clane, Ud, LPC, 12 * LPC + 8);
+        });
+        if (k + 2 < LE) stage(k + 2, ph ^ 1);
+        __syncwarp();
+    }
+    return ok;
+}
+
 template <int NRB>
 __global__ void __launch_bounds__(128, 3) fac_sweep_w(FacArgs a) {
     using S = TWS<NRB>;
@@ -314,100 +422,10 @@ __global__ void __launch_bounds__(128, 3) fac_sweep_w(FacArgs a) {
         frob = sqrt(s);
     }
 
-    // ---- Hermitian sweep operator, 2x2 block pivots (see dmma_sweep) -----------
-    double2* ub = reinterpret_cast<double2*>(smem_raw + warp * S::WARP_SMEM);   // [2][LPC]
-    double2* cs = ub + 2 * LPC;                                                   // [2][2][LPC]
-    double* kv = reinterpret_cast<double*>(cs + 4 * LPC);                         // [2][4]
-    const double* Ud = reinterpret_cast<const double*>(ub);
-    const int abase = 2 * (kc * LPC + (r8 >> 1)) + (p ^ q);
-    const int bbase = 2 * (kc * LPC + r8) + q;
-    // Rows of the pivot block are never zeroed in the staged columns: their A
-    // operand lanes are masked in the DMMA and their U_j is zero by definition.
-    const int rl = r8 >> 1;
-    const SwLane sw{rl, c4, p};
-    auto stage = [&](int k2, int dst) {
-        double* Cn = reinterpret_cast<double*>(cs + dst * 2 * LPC);
-        double* kd = kv + dst * 4;
-        const int dl = rl - (k2 & 3);
-        const bool rlane = (unsigned)dl < 2u, clane = c4 == ((k2 & 7) >> 1);
-        const int kcl = k2 >> 3;
-        dispatch_col<S::NCJ>(kcl, [&](auto J) { stage_col<NRB, J.value>(acc, sw, clane, k2, Cn, LPC); });
-        dispatch_row<NRB>(k2 >> 2, [&](auto I) {
-            stage_row<NRB, I.value>(acc, sw, rlane, dl, k2, kcl, clane, Cn, kd, LPC);
-        });
-    };
-    stage(0, 0);
-    __syncwarp();
-    double logdet = 0.0;
-    bool ok = true;
-    const int LE = (L + 1) & ~1;
-    const unsigned long long sgn = (p == 0 && q == 1) ? 0ull : 0x8000000000000000ull;
-    double* nm = kv + 8;   // -M as 2x2 complex: Ud[12 LPC + 8 + 2 (2 dl + h) + p]
-    for (int k = 0; k < LE; k += 2) {
-        const int ph = (k >> 1) & 1;
-        const double2* cc = cs + ph * 2 * LPC;
-        const double* Cd = reinterpret_cast<const double*>(cc);
-        const double ka = kv[ph * 4 + 0], kbr = kv[ph * 4 + 1], kbi = kv[ph * 4 + 2],
-                     kcc = kv[ph * 4 + 3];
-        const double det = fma(ka, kcc, -fma(kbr, kbr, kbi * kbi));
-        if (!(ka > 0.0) || !(det > 0.0)) {
-            ok = false;
-            break;
-        }
-        if (a.record_objective) logdet += log(det);
-        {
-            const double dinv = __drcp_rn(det);
-            const double m00 = kcc * dinv;
-            const double m11 = ka * dinv;
-            const double2 m10 = make_double2(-kbr * dinv, -kbi * dinv);
-            const double2 m01 = make_double2(m10.x, -m10.y);
-#pragma unroll
-            for (int j = lane; j < LP; j += 32) {
-                double2 u0 = make_double2(0.0, 0.0), u1 = make_double2(0.0, 0.0);
-                if (j != k && j != k + 1) {   // U_K = 0 (C_K is K itself, not zeroed)
-                    const double2 pp = cc[j], qq = cc[LPC + j];
-                    u0 = make_double2(fma(m01.x, qq.x, fma(m01.y, qq.y, m00 * pp.x)),
-                                      fma(m01.y, qq.x, fma(-m01.x, qq.y, -m00 * pp.y)));
-                    u1 = make_double2(fma(m11, qq.x, fma(m10.x, pp.x, m10.y * pp.y)),
-                                      fma(-m11, qq.y, fma(m10.y, pp.x, -m10.x * pp.y)));
-                }
-                ub[j] = u0;
-                ub[LPC + j] = u1;
-            }
-            if (lane < 8) {   // -M: (dl, h) = (0,0) (0,1) (1,0) (1,1), component p = lane & 1
-                const int e = lane >> 1, pp = lane & 1;
-                const double re = e == 0 ? m00 : (e == 1 ? m01.x : (e == 2 ? m10.x : m11));
-                const double im = (e == 1) ? m01.y : (e == 2 ? m10.y : 0.0);
-                nm[lane] = -(pp ? im : re);
-            }
-        }
-        __syncwarp();
-        const int kr = k >> 2, kcl = k >> 3, dl = rl - (k & 3);
-        const bool rlane = (unsigned)dl < 2u, clane = c4 == ((k & 7) >> 1);
-        // rank-2 trailing update: one DMMA per tile (operands shared per row /
-        // column tile; the K rows' A lanes masked)
-        {
-            double af[NRB], bfr[S::NCJ];
-#pragma unroll
-            for (int i = 0; i < NRB; ++i)
-                af[i] = (i == kr && rlane) ? 0.0 : xsign(Cd[abase + 8 * i], sgn);
-#pragma unroll
-            for (int j = 0; j < S::NCJ; ++j) bfr[j] = Ud[bbase + 16 * j];
-            int ti = 0, tj = 0;
-#pragma unroll
-            for (int t = 0; t < NTL; ++t) {
-                dmma(acc[t], af[ti], bfr[tj]);
-                TILE_NEXT(ti, tj)
-            }
-        }
-        // the K columns (conj(U_l)), then the K rows (U_m) and the K block (-M)
-        dispatch_col<S::NCJ>(kcl, [&](auto J) { fix_col<NRB, J.value>(acc, sw, clane, Ud, LPC); });
-        dispatch_row<NRB>(kr, [&](auto I) {
-            fix_row<NRB, I.value>(acc, sw, rlane, dl, kcl, clane, Ud, LPC, 12 * LPC + 8);
-        });
-        if (k + 2 < LE) stage(k + 2, ph ^ 1);
-        __syncwarp();
-    }
+    // ---- Hermitian sweep operator, 2x2 block pivots, in the fragments ----------
+    double logdet;
+    const bool ok = warp_sweep<NRB>(acc, smem_raw + warp * S::WARP_SMEM, L, a.record_objective,
+                                    logdet);
     if (!ok) {
         if (lane == 0) {
             a.status[b] = PSCA_CHOL_FAIL;

@@ -37,7 +37,7 @@
 #define PSCA_BLOCK_SWEEP 1
 #endif
 #ifndef PSCA_DSWEEP
-#define PSCA_DSWEEP 1    // sweep with the matrix in DMMA fragments (dmma_sweep)
+#define PSCA_DSWEEP 0    // 1: factor_pass sweeps in DMMA fragments (dmma_sweep); 0: USWEEP
 #endif
 #ifndef PSCA_USWEEP
 #define PSCA_USWEEP 1    // block sweep with U_j = M conj(C_j) shared per column

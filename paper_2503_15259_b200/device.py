@@ -254,15 +254,27 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
                   torch.zeros(1, dtype=torch.float64, device=dev))
     if out is None:
         out = {}
+    # output buffers are reused from ``out`` when the shapes match, so repeated
+    # solves with the same inputs present identical arguments to psca_solve
+    # (whose CUDA-graph cache then replays the launch sequence)
+    bufs = out.get("_bufs") or {}
+
+    def buf(name, shape, dtype):
+        t = bufs.get(name)
+        if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != dev:
+            t = torch.empty(shape, dtype=dtype, device=dev)
+            bufs[name] = t
+        return t
+
     x = out.get("x")
     if x is None or tuple(x.shape) != (B, N) or x.device != dev:
         x = torch.empty((B, N), dtype=torch.float64, device=dev)
-    un = torch.empty((B, max(T, 1)), dtype=torch.float64, device=dev)
-    obj = torch.empty((B, max(T, 1)), dtype=torch.float64, device=dev) if record_objective else None
-    its = torch.empty((B, T + 1, N), dtype=torch.float64, device=dev) if record_iterates else None
-    status = torch.empty(B, dtype=torch.int32, device=dev)
-    n_iter = torch.empty(B, dtype=torch.int32, device=dev)
-    cond = torch.empty(B, dtype=torch.float64, device=dev)
+    un = buf("un", (B, max(T, 1)), torch.float64)
+    obj = buf("obj", (B, max(T, 1)), torch.float64) if record_objective else None
+    its = buf("its", (B, T + 1, N), torch.float64) if record_iterates else None
+    status = buf("status", (B,), torch.int32)
+    n_iter = buf("n_iter", (B,), torch.int32)
+    cond = buf("cond", (B,), torch.float64)
     args = SolveArgsC(
         kind=KIND_CODES[kind], B=B, N=N, L=L, n_antennas=int(n_antennas), max_iter=T,
         tol=float(tol), record_objective=int(bool(record_objective)), n_chunks=int(n_chunks),
@@ -289,6 +301,7 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
                           _stream(torch)), "psca_solve")
     return {"x": x, "update_norm": un[:, :T], "objective": obj[:, :T] if obj is not None else None,
             "iterates": its, "status": status, "n_iter": n_iter, "cond_est": cond, "_ws": ws,
+            "_bufs": bufs,
             "launches": lib.psca_last_launch_count(),
             "path": {0: "two-kernel", 1: "persistent", 2: "two-kernel-split"}.get(
                 lib.psca_last_path(), "?")}

@@ -535,7 +535,7 @@ def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=
         with torch.cuda.stream(comp):
             res = psca_run_batch(problem, Sd, Ed, nd, n_antennas, gains=gd, schedule=schedule,
                                  max_iter=max_iter, tol=tol, n_chunks=nck, out=outs[k])
-            outs[k] = {"x": res["x"], "_ws": res.get("_ws")}
+            outs[k] = {"x": res["x"], "_ws": res.get("_ws"), "_bufs": res.get("_bufs")}
             x_h[lo:hi].copy_(res["x"], non_blocking=True)
             st_h[lo:hi].copy_(res["status"], non_blocking=True)
             ni_h[lo:hi].copy_(res["n_iter"], non_blocking=True)
