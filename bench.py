@@ -358,12 +358,16 @@ def dist_setup(args):
     return world, rank, local
 
 
+REF_PER_CORE = 4
+
+
 def reference_arm(args):
     """The reference algorithm's CPU implementation (the oracle port) on all host cores.
 
-    Each step: every core solves one instance of the workload (scene generation
-    untimed, as the GPU arms exclude it); the step's time is the slowest core's
-    solve time, so value = instances / sum of step times."""
+    Each step: every core solves PER_CORE instances of the workload (scene
+    generation untimed, as the GPU arms exclude it); the step's time is the
+    slowest core's solve time, so value = instances / sum of step times.  Several
+    instances per core per step keep the slowest-core term close to the mean."""
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return 0
@@ -379,8 +383,9 @@ def reference_arm(args):
                                    for w in range(workers)])
         n, wall = 0, 0.0
         for st in range(args.steps):
-            res = pool.map(_cpu_worker, [(w, workers, 0, wl.name, wl.iters, 1,
-                                          30_000_000 + st * workers) for w in range(workers)])
+            res = pool.map(_cpu_worker, [(w, workers, 0, wl.name, wl.iters, REF_PER_CORE,
+                                          30_000_000 + st * workers * REF_PER_CORE)
+                                         for w in range(workers)])
             n += sum(r[0] for r in res)
             wall += max(r[1] for r in res)
     value = n / wall
@@ -389,11 +394,11 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": wl.config_block(workers, per_gpu=False),
+        "config": wl.config_block(workers * REF_PER_CORE, per_gpu=False),
         "psca_iters_per_s": value * wl.iters,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"each step: {workers} {wl.name} instances (T={wl.iters}), one "
-                                   "per host core, numpy/OpenBLAS oracle (restatement of the "
+                         "sample": f"each step: {workers * REF_PER_CORE} {wl.name} instances "
+                                   f"(T={wl.iters}), {REF_PER_CORE} per host core, numpy/OpenBLAS oracle (restatement of the "
                                    "reference; the reference is pure Python and cannot be "
                                    "installed on the box); scene generation excluded, step time "
                                    "= slowest core's solve"},

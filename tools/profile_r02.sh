@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round-2 evidence run on one B200 (run from the repo root under gpurun):
+#   1. parity report of the scale / baseline / reference-trace GPU tests
+#   2. ncu launch list of one serial c1 solve (4096-instance launches)
+#   3. ncu --set full of the column kernel, the factor sweep and the products
+# Output in gpurun_out/.
+set -u
+o=gpurun_out
+mkdir -p $o
+rm -f $o/r02_parity.json
+PSCA_PARITY_REPORT=$o/r02_parity.json timeout 900 python -m pytest -q -m gpu \
+  tests/test_gpu_scale.py tests/test_gpu_baseline.py tests/test_gpu_parity.py > $o/parity_tests.log 2>&1
+echo "parity tests rc=$?"
+B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-executed"
+export PSCA_NO_SPLIT=1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+  --clock-control none -k regex:"column_kernel|fac_|factor" -c 320 --csv \
+  --log-file $o/r02_launches_c1.csv $B > $o/ncu_launch.log 2>&1
+echo "launch list rc=$?"
+for k in column_kernel_w fac_sweep_w fac_prod_t; do
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k --launch-skip 20 -c 1 \
+    -o $o/r02_$k -f $B > $o/ncu_full_$k.log 2>&1
+  echo "full $k rc=$?"
+done
