@@ -97,6 +97,11 @@ typedef struct {
      * that opens iteration k-1 report PSCA_CHOL_FAIL for every instance still
      * running (cond_est = +inf), exactly as a non-positive pivot would. */
     int fault_iter;
+    /* Per-instance step schedules: 0 = every instance uses steps[0..max_iter);
+     * otherwise instance b uses steps[b*steps_stride + k] (steps_stride >=
+     * max_iter).  Lets one batched forward evaluate several candidate PSCA-Net
+     * step vectors at once (unroll.py:131-172 evaluates them one by one). */
+    int steps_stride;
 } psca_solve_args;
 
 /* Workspace (device bytes) psca_solve needs for these arguments. */

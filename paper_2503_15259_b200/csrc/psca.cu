@@ -316,7 +316,8 @@ struct ColArgs {
     double2* sig_part;          // [B][chunks][NBLK][32] double2
     double* red_part;           // [B][chunks][4]
     const int* status;          // [B]
-    const double* steps;        // [T]
+    const double* steps;        // [T], or [B][T] when steps_stride = T
+    int steps_stride;           // 0: one schedule for the batch; T: per instance
     const double* prior_lin;    // [N]
     const double* prior_p;      // [N]
     int pairwise;               // map-k with a pairwise prior: gradient term from pgrad
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(NT, (MAXBW <= 16) ? 2 : 1) column_kernel(ColAr
     double p_dx2 = 0.0, p_minq = INFINITY, p_prior = 0.0;
     const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
     const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
-    const double rho = (MODE == COL_SOLVE) ? a.steps[a.k] : 0.0;
+    const double rho = (MODE == COL_SOLVE) ? a.steps[(size_t)b * a.steps_stride + a.k] : 0.0;
 
     const int ntiles = (n_end - n_begin + NCT - 1) / NCT;
     if (ntiles > 0) load_tile(S0, sb, a.N, a.L, geo.LP8, n_begin);
@@ -606,7 +607,8 @@ struct FacArgs {
     int B, N, L, nrb, T, n_chunks, k_new, kind, n_antennas, record_objective;
     int incremental;            // Sigma - sigma^2 I = D, D_{k+1} = (1-rho_k) D_k + increment
     double tol;
-    const double* steps;        // [T] (incremental: rho_k)
+    const double* steps;        // [T] or [B][T] (incremental: rho_k)
+    int steps_stride;           // 0 or T (per-instance schedules)
     double2* dmat;              // incremental: [B][L][L] D_k (lower triangle used)
     const double* noise;        // [B]
     const double2* emp_cov;     // [B][L][L]
@@ -780,7 +782,7 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
     const int L = a.L;
     double* Xd = reinterpret_cast<double*>(X);
     double2* D = a.incremental ? a.dmat + (size_t)b * dmat_stride(geo, L) : nullptr;
-    const double omr = (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[a.k_new - 1]) : 0.0;
+    const double omr = (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[(size_t)b * a.steps_stride + a.k_new - 1]) : 0.0;
     const double s2 = a.noise[b];
     const double2* sp = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
     const size_t cs = (size_t)geo.NBLK * 32;
@@ -867,7 +869,7 @@ __device__ void assemble_sigma_seq(const FacArgs& a, const Geo& geo, int b, doub
     const int L = a.L;
     double* Xd = reinterpret_cast<double*>(X);
     double2* D = a.incremental ? a.dmat + (size_t)b * dmat_stride(geo, L) : nullptr;
-    const double omr = (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[a.k_new - 1]) : 0.0;
+    const double omr = (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[(size_t)b * a.steps_stride + a.k_new - 1]) : 0.0;
     const double s2 = a.noise[b];
     const double2* sp = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
     const size_t cs = (size_t)geo.NBLK * 32;
@@ -1736,6 +1738,7 @@ int check_solve_args(const psca_solve_args* a) {
     }
     if (a->kind == PSCA_MAP_UR && !a->prior_p) return PSCA_E_ARG;
     if (a->max_iter > 0 && (!a->steps || !a->update_norm)) return PSCA_E_ARG;
+    if (a->steps_stride != 0 && a->steps_stride < a->max_iter) return PSCA_E_ARG;
     return PSCA_OK;
 }
 
@@ -1978,7 +1981,7 @@ static int solve_enqueue(const psca_solve_args* a, void* workspace, size_t works
     ca.pilots = reinterpret_cast<const double2*>(a->pilots);
     ca.gains = a->gains; ca.iterates = a->iterates; ca.frags = lay.frags;
     ca.sig_part = lay.sig_part; ca.red_part = lay.red_part; ca.status = a->status;
-    ca.steps = a->steps; ca.prior_lin = a->prior_lin; ca.prior_p = a->prior_p; ca.eff = a->eff;
+    ca.steps = a->steps; ca.steps_stride = a->steps_stride; ca.prior_lin = a->prior_lin; ca.prior_p = a->prior_p; ca.eff = a->eff;
     ca.pgrad = lay.pgrad;
     ca.pairwise = (a->kind == PSCA_MAP_K && a->prior_c2_indptr) ? 1 : 0;
     // incremental rebuild needs the compiled column kernel (psca_fast.cuh)
@@ -1999,7 +2002,7 @@ static int solve_enqueue(const psca_solve_args* a, void* workspace, size_t works
         fa.c1 = a->prior_c1; fa.c2_ptr = a->prior_c2_indptr; fa.c2_idx = a->prior_c2_indices;
         fa.c2_val = a->prior_c2_data;
     }
-    fa.incremental = ca.incremental; fa.steps = a->steps; fa.dmat = lay.dmat;
+    fa.incremental = ca.incremental; fa.steps = a->steps; fa.steps_stride = a->steps_stride; fa.dmat = lay.dmat;
     fa.kind = a->kind; fa.n_antennas = a->n_antennas;
     fa.record_objective = ca.record_objective; fa.tol = a->tol;
     fa.noise = a->noise; fa.emp_cov = reinterpret_cast<const double2*>(a->emp_cov);

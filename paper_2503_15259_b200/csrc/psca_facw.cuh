@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(128, 3) fac_sweep_w(FacArgs a) {
         double2* D = a.incremental ? a.dmat + (size_t)b * dmat_stride(make_geo(L, NRB), L)
                                    : nullptr;
         const double omr =
-            (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[a.k_new - 1]) : 0.0;
+            (a.incremental && a.k_new > 0) ? __dsub_rn(1.0, a.steps[(size_t)b * a.steps_stride + a.k_new - 1]) : 0.0;
         // one column chunk per instance on this path (use_warp_factor)
         const double2* sp = a.sig_part + (size_t)b * NTL * 32;
         const double s2 = a.noise[b];

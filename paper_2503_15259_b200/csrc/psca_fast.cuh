@@ -201,7 +201,7 @@ __device__ __forceinline__ void col_pass(const ColArgs& a, int b, int k,
 
     const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
     const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
-    const double rho = a.steps[k];
+    const double rho = a.steps[(size_t)b * a.steps_stride + k];
     const double omr = __dsub_rn(1.0, rho);
 
     auto issue_tile = [&](double2* buf, int col0) {
@@ -1549,7 +1549,7 @@ __global__ void __launch_bounds__(NT, 2) psca_persistent_t(ColArgs ca, FacArgs f
                 acc_to_sigma<NRB>(acc, slot, nbw, X, ld, L,
                                   fa.incremental ? reinterpret_cast<double*>(fa.dmat + (size_t)b * dmat_stride(geo, L))
                                                  : nullptr,
-                                  __dsub_rn(1.0, fa.steps[k]));
+                                  __dsub_rn(1.0, fa.steps[(size_t)b * fa.steps_stride + k]));
                 finish_sigma(X, ld, L, fa.noise[b]);
                 ok = factor_pass<NRB, NT>(fa, geo, b, X, Gm, rowb, colb, Es, reinterpret_cast<double*>(FR),
                                      sred, frob, logdet, trace);

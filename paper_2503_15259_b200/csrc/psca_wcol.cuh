@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
     const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
     const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
     const int k = a.k;
-    const double rho = a.steps[k];
+    const double rho = a.steps[(size_t)b * a.steps_stride + k];
     const double omr = __dsub_rn(1.0, rho);
     const double* x_cur = a.x_cur + bN;
     double* x_next = a.x_next + bN;

@@ -48,6 +48,7 @@ class SolveArgsC(ctypes.Structure):
         ("objective", ctypes.c_void_p), ("iterates", ctypes.c_void_p),
         ("status", ctypes.c_void_p), ("n_iter", ctypes.c_void_p), ("cond_est", ctypes.c_void_p),
         ("fault_iter", ctypes.c_int),
+        ("steps_stride", ctypes.c_int),
     ]
 
 
@@ -215,7 +216,8 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
     """Run the batched PSCA solve on the current CUDA device / stream.
 
     pilots (B,L,N) complex128, emp_cov (B,L,L) complex128, noise (B,) float64,
-    gains (B,N) float64 for known-pathloss kinds, steps (T,) float64.
+    gains (B,N) float64 for known-pathloss kinds, steps (T,) float64 (one
+    schedule for the batch) or (B, T) (one schedule per instance).
     A pairwise MAP-K prior passes prior_c1 (N,) and prior_c2 = (indptr,
     indices, data) of its CSR interaction matrix instead of prior_lin.
     Inputs may be numpy arrays or torch tensors (moved to the device if
@@ -235,9 +237,16 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
     B, L, N = S.shape
     E = _dev(torch, emp_cov, torch.complex128, dev)
     sig2 = _dev(torch, noise, torch.float64, dev).reshape(B)
-    st = _dev(torch, steps, torch.float64, dev).reshape(-1)
-    T = int(st.numel()) if max_iter is None else int(max_iter)
-    if st.numel() < T:
+    st = _dev(torch, steps, torch.float64, dev)
+    stride = 0
+    if st.dim() == 2:
+        if st.shape[0] != B:
+            raise ValueError("per-instance steps must be (B, T)")
+        st = st.contiguous()
+        stride = int(st.shape[1])
+    st = st.reshape(-1)
+    T = (stride or int(st.numel())) if max_iter is None else int(max_iter)
+    if (stride or st.numel()) < T:
         raise ValueError("need one step per iteration")
     g = _dev(torch, gains, torch.float64, dev) if gains is not None else None
     pl = _dev(torch, prior_lin, torch.float64, dev) if prior_lin is not None else None
@@ -290,7 +299,8 @@ def solve(kind: str, pilots, emp_cov, noise, n_antennas: int, steps, *, gains=No
         x_out=x.data_ptr(), update_norm=un.data_ptr(),
         objective=obj.data_ptr() if obj is not None else 0,
         iterates=its.data_ptr() if its is not None else 0, status=status.data_ptr(),
-        n_iter=n_iter.data_ptr(), cond_est=cond.data_ptr(), fault_iter=int(fault_iter))
+        n_iter=n_iter.data_ptr(), cond_est=cond.data_ptr(), fault_iter=int(fault_iter),
+        steps_stride=stride)
     nbytes = lib.psca_solve_workspace_bytes(ctypes.byref(args))
     if nbytes == 0 and B > 0:
         raise PscaNativeError("psca_solve rejected the arguments (shape/kind/pointers)")

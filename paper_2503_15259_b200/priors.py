@@ -90,36 +90,47 @@ class PairwiseMvbPrior:
                 c2.data.astype(np.float64))
 
 
+class _GroupCountLaw:
+    """Exchangeable pairwise model of one group of G devices, reduced to the
+    active count k = 0..G: log P(k) = log C(G, k) + a k + b k(k-1)/2 - log Z.
+    Its sufficient statistics are (k, pairs(k)); under the true group law
+    (every device active with prob. p, all together) their means are G p and
+    C(G, 2) p."""
+
+    def __init__(self, g: int, p: float):
+        self.count = np.arange(g + 1)
+        self.pairs = self.count * (self.count - 1) / 2.0
+        lg = math.lgamma
+        self.log_mult = np.array([lg(g + 1) - lg(c + 1) - lg(g - c + 1) for c in self.count])
+        self.target = (g * p, g * (g - 1) / 2.0 * p)
+
+    def neg_loglik(self, nat):
+        """-(E_true[log P]) and its gradient in the natural parameters (a, b)."""
+        import scipy.special
+        a, b = nat
+        z = self.log_mult + a * self.count + b * self.pairs
+        log_norm = scipy.special.logsumexp(z)
+        prob = np.exp(z - log_norm)
+        tk, tp = self.target
+        return (-(tk * a + tp * b - log_norm),
+                -np.array([tk - float(prob @ self.count), tp - float(prob @ self.pairs)]))
+
+
 def fit_group_coefficients(group_size: int, p: float, cap: float) -> tuple[float, float]:
-    """Exchangeable pairwise fit of the group law (priors.py:109-139): within a
-    group the model p.m.f. depends on the active count k only,
-    P(k) ~ C(G,k) exp(a k + b k(k-1)/2); (a, b) maximise the expected
-    log-likelihood G p a + C(G,2) p b - log Z(a, b) under the true law
-    (E a_n = E a_n a_m = p), box-constrained by the cap."""
+    """(a, b) of the pairwise MVB prior for one group (reference
+    priors.py:109-139): the maximum-expected-likelihood fit of
+    ``_GroupCountLaw`` by box-constrained L-BFGS-B from (logit p, 0), with
+    |a| <= cap and |b| <= 2 cap + 8.  A single-device group is independent:
+    a = logit p clipped to the cap, b = 0."""
     import scipy.optimize
-    import scipy.special
-    g = group_size
-    if g == 1:
-        return float(np.clip(math.log(p / (1.0 - p)), -cap, cap)), 0.0
-    k = np.arange(g + 1)
-    log_binom = np.array([math.lgamma(g + 1) - math.lgamma(i + 1) - math.lgamma(g - i + 1)
-                          for i in k])
-    pairs = k * (k - 1) / 2.0
-    n_pairs = g * (g - 1) / 2.0
-
-    def objective(theta):
-        a, b = theta
-        logits = log_binom + a * k + b * pairs
-        logz = scipy.special.logsumexp(logits)
-        w = np.exp(logits - logz)
-        val = -(g * p * a + n_pairs * p * b - logz)
-        grad = -np.array([g * p - float(w @ k), n_pairs * p - float(w @ pairs)])
-        return val, grad
-
-    res = scipy.optimize.minimize(objective, x0=np.array([math.log(p / (1 - p)), 0.0]),
-                                  jac=True, method="L-BFGS-B",
+    logit = math.log(p / (1.0 - p))
+    if group_size == 1:
+        return float(np.clip(logit, -cap, cap)), 0.0
+    law = _GroupCountLaw(group_size, p)
+    fit = scipy.optimize.minimize(law.neg_loglik, x0=np.array([logit, 0.0]), jac=True,
+                                  method="L-BFGS-B",
                                   bounds=[(-cap, cap), (-2 * cap - 8, 2 * cap + 8)])
-    return float(res.x[0]), float(res.x[1])
+    return float(fit.x[0]), float(fit.x[1])
 
 
 def known_prior_gradient(prior, n_antennas: int, n: int) -> np.ndarray:

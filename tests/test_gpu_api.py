@@ -215,3 +215,56 @@ def test_known_prior_terms(cuda_device, golden_components):
                                -(pw.c1 + pw.c2 @ a) / 16, rtol=1e-14, atol=1e-16)
     assert priors.log_prior_value_known(a, pw, 16) == pytest.approx(
         -(pw.c1 @ a + 0.5 * a @ (pw.c2 @ a)) / 16, rel=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# per-instance step schedules (psca_solve_args.steps_stride)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind", ["ml-k", "map-k", "ml-ud", "map-ur"])
+@pytest.mark.parametrize("n_chunks", [1, 0])
+def test_per_instance_steps_match_separate_solves(cuda_device, kind, n_chunks):
+    """One call with a (B, T) step matrix == B calls with one schedule each, bit
+    for bit on the same column kernel (what the PSCA-Net trainer's batched
+    probe groups rely on)."""
+    import torch
+    from paper_2503_15259_b200 import device, estimators as est, sysmodel
+    cfg = _cfg(n=60, l=12, m=32)
+    samples = sysmodel.gen_dataset(cfg, 3, 11)
+    prob = _problems(cfg)[kind]
+    rng = np.random.default_rng(5)
+    T = 7
+    steps = rng.uniform(0.05, 1.0, (6, T))
+    # every sample twice, with two different schedules
+    idx = [0, 1, 2, 0, 1, 2]
+    pil = np.stack([samples[i].pilots for i in idx])
+    cov = np.stack([samples[i].emp_cov for i in idx])
+    noise = np.array([samples[i].noise_power for i in idx])
+    gains = np.stack([samples[i].gains for i in idx])
+    kw = est.prior_arrays(prob, cfg.n_devices, cfg.n_antennas)
+    g = gains if prob.known_pathloss else None
+    res = device.solve(kind, pil, cov, noise, cfg.n_antennas, steps, gains=g, max_iter=T,
+                       n_chunks=n_chunks, **kw)
+    x = res["x"].cpu().numpy()
+    un = res["update_norm"].cpu().numpy()
+    for b in range(6):
+        one = device.solve(kind, pil[b:b + 1], cov[b:b + 1], noise[b:b + 1], cfg.n_antennas,
+                           steps[b], gains=None if g is None else g[b:b + 1], max_iter=T,
+                           n_chunks=1 if n_chunks == 1 else n_chunks, **kw)
+        if n_chunks == 1:
+            assert np.array_equal(one["x"].cpu().numpy()[0], x[b])
+            assert np.array_equal(one["update_norm"].cpu().numpy()[0], un[b])
+        else:
+            assert max_rel(one["x"].cpu().numpy()[0], x[b]) < 1e-10
+    # the two schedules of the same sample really differ
+    assert not np.array_equal(x[0], x[3])
+    torch.cuda.synchronize()
+
+
+def test_per_instance_steps_rejects_short_stride(cuda_device):
+    from paper_2503_15259_b200 import device
+    cfg = _cfg(n=40, l=8)
+    _, s = _sample(2)
+    with pytest.raises(ValueError):
+        device.solve("ml-ud", s.pilots[None], s.emp_cov[None], np.array([1.0]), cfg.n_antennas,
+                     np.full((2, 5), 0.5), max_iter=5)

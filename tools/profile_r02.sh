@@ -19,6 +19,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 echo "launch list rc=$?"
 for k in column_kernel_w fac_sweep_w fac_prod_t; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k --launch-skip 20 -c 1 \
-    -o $o/r02_$k -f $B > $o/ncu_full_$k.log 2>&1
+    -o /tmp/r02_$k -f $B > $o/ncu_full_$k.log 2>&1
   echo "full $k rc=$?"
+  # reports are large: export the pages here and keep only the text
+  ncu -i /tmp/r02_$k.ncu-rep --page raw --csv > $o/r02_${k}_raw.csv 2>/dev/null
+  ncu -i /tmp/r02_$k.ncu-rep --page details > $o/r02_${k}_details.txt 2>/dev/null
+  python tools/ncu_lines.py /tmp/r02_$k.ncu-rep 40 > $o/r02_${k}_lines.txt 2>/dev/null
 done
