@@ -416,8 +416,11 @@ def executed_column_flops(wl, problem, pil_d, emp_d, noi_d, gain_d, m):
     block for the two quadratic forms (lower block triangle of P' and A') and,
     for its moving columns (non-zero rebuild weight rho cand g: exactly the
     devices with x_{k+1} != (1 - rho_k) x_k), NBLK DMMAs per pair of listed
-    columns in rounds of 16 (psca_wcol.cuh wc_rebuild).  Returns
-    (flops per column launch, quad share, mean moving columns per iteration)."""
+    columns in rounds of 16 (psca_wcol.cuh wc_rebuild) -- unless the list has at
+    most MOV_CAP = 160 entries on the warp factor path (L <= 40): those increments
+    are summed by the instance's factor warp (fac_sweep_w, deferred rebuild) and
+    are not column-kernel work.  Returns (flops per column launch, quad share,
+    mean moving columns per iteration, share of instance-iterations deferred)."""
     import torch
     from paper_2503_15259_b200 import device, estimators
     cfg = wl.cfg
@@ -430,20 +433,27 @@ def executed_column_flops(wl, problem, pil_d, emp_d, noi_d, gain_d, m):
     its = res["iterates"]
     n_iter = res["n_iter"].to(torch.int64)
     quad_blk = 2 * nrb * (nrb + 1) * (-(-N // 8))
-    quad_total, rebuild_total, moving_total = 0, 0, 0
+    defer = nrb <= 10 and B >= device.sm_count() and os.environ.get("PSCA_DEFER_REBUILD") != "0"
+    mov_cap = 160
+    quad_total, rebuild_total, moving_total, deferred, live_total = 0, 0, 0, 0, 0
     for k in range(T):
         live = n_iter > k
         omr = 1.0 - float(wl.steps[k])
         mv = (its[:, k + 1] != omr * its[:, k]).sum(dim=1).to(torch.int64)
         mv = torch.where(live, mv, torch.zeros_like(mv))
+        moving_total += int(mv.sum())
+        live_total += int(live.sum())
+        if defer:
+            deferred += int((live & (mv <= mov_cap)).sum())
+            mv = torch.where(mv <= mov_cap, torch.zeros_like(mv), mv)
         full, rest = mv // 16, mv % 16
         rebuild_total += int((nblk * (8 * full + (rest + 1) // 2)).sum())
         quad_total += int(live.sum()) * quad_blk
-        moving_total += int(mv.sum())
     del its, res
     torch.cuda.empty_cache()
     flops = DMMA_FLOPS * (quad_total + rebuild_total) / T
-    return flops, quad_total / max(quad_total + rebuild_total, 1), moving_total / (B * T)
+    return (flops, quad_total / max(quad_total + rebuild_total, 1), moving_total / (B * T),
+            deferred / max(live_total, 1))
 
 
 def serial_launch_times(run):
@@ -540,10 +550,10 @@ def ours_arm(args):
     algo_tflops = algo_launch / (col_ms * 1e-3) / 1e12
     executed = None
     if not args.no_executed and out.get("path") != "persistent" and B >= 2 * device.sm_count():
-        ex_launch, quad_share, moving = executed_column_flops(wl, problem, pil_d, emp_d, noi_d,
-                                                              gain_d, m)
+        ex_launch, quad_share, moving, deferred = executed_column_flops(
+            wl, problem, pil_d, emp_d, noi_d, gain_d, m)
         executed = {"flops_per_launch": ex_launch, "quad_share": quad_share,
-                    "moving_columns_per_iteration": moving}
+                    "moving_columns_per_iteration": moving, "deferred_share": deferred}
     if executed is not None:
         ach = executed["flops_per_launch"] / (col_ms * 1e-3) / 1e12
         nrb = next(r for r in (2, 3, 4, 5, 6, 8, 10, 12, 16, 20) if 4 * r >= cfg.pilot_len)
@@ -552,11 +562,14 @@ def ours_arm(args):
             "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
             "flops_per_unit": "EXECUTED FP64 DMMA flops (m8n8k4 = 512 flops): 2 NRB(NRB+1) "
                               "per 8-column block for the quadratic forms + NBLK per pair of "
-                              "moving columns for the rebuild, counted exactly from an "
+                              "moving columns for the rebuilds the column CTA does itself "
+                              "(lists longer than 160; shorter lists are summed by the factor "
+                              "warp and not counted here), counted exactly from an "
                               "iterate-recording pass of the same batch",
             "executed_flops_per_launch": executed["flops_per_launch"],
             "quad_share_of_executed": executed["quad_share"],
             "moving_columns_per_iteration": executed["moving_columns_per_iteration"],
+            "rebuild_deferred_share": executed["deferred_share"],
         }
     else:
         roofline = {"bound": "tensor", "kernel": "column_kernel (tile path, chunked instance)",

@@ -47,6 +47,13 @@ namespace {
 
 constexpr int NT = 256;            // threads per CTA
 constexpr int NWARP = NT / 32;
+// deferred rebuild: longest moving-column list the factor warp sums itself
+// (longer lists are summed by the column CTA; 96, 160 and 256 measured equal at c1,
+// 160 and 256 better at c2 / c3 where more columns move)
+#ifndef PSCA_MOV_CAP
+#define PSCA_MOV_CAP 160
+#endif
+constexpr int MOV_CAP = PSCA_MOV_CAP;
 constexpr int NCT = 32;            // device columns per SMEM tile
 constexpr int NCB = NCT / 8;       // 8-column blocks per tile
 constexpr int FAC_SMEM_MAX_LP = 80;
@@ -267,8 +274,9 @@ __device__ double block_sum(double v, double* sred) {
 // effective-pathloss prior (priors.py:246-281, 313-399); mirrors the numpy
 // operation order so rounding matches the reference closely
 // ---------------------------------------------------------------------------
-__device__ void eff_density(double gm, double p, const psca_eff_prior& e, double& dens,
-                            double& der) {
+// eps3 = pow(e.eps, 3.0), hoisted by callers that evaluate many devices
+__device__ void eff_density3(double gm, double p, const psca_eff_prior& e, double eps3,
+                             double& dens, double& der) {
     const double eps = e.eps, gl = e.g_low;
     dens = 0.0;
     der = 0.0;
@@ -277,13 +285,13 @@ __device__ void eff_density(double gm, double p, const psca_eff_prior& e, double
         double t1 = (1.0 - p) * (1.0 + 2.0 * gb / eps);
         double t2 = (gb - eps) / eps;
         dens = t1 * (t2 * t2);
-        der = 6.0 * (1.0 - p) * gb * (gb - eps) / pow(eps, 3.0);
+        der = 6.0 * (1.0 - p) * gb * (gb - eps) / eps3;
     } else if (gm >= gl - eps && gm < gl) {  // Hermite bridge
         double t = gm - gl;
         double u = (t + eps) / eps;
         double u2 = u * u;
         dens = p * (e.cv * (1.0 - 2.0 * t / eps) * u2 + e.cw * t * u2);
-        der = p * (-6.0 * e.cv * t * (t + eps) / pow(eps, 3.0) +
+        der = p * (-6.0 * e.cv * t * (t + eps) / eps3 +
                    e.cw * (t + eps) * (3.0 * t + eps) / (eps * eps));
     } else if (gm >= gl) {  // exact tail p * p_G
         double base = gm / e.p_lin;
@@ -296,6 +304,10 @@ __device__ void eff_density(double gm, double p, const psca_eff_prior& e, double
         dens = p * pg;
         der = p * dpg;
     }
+}
+__device__ void eff_density(double gm, double p, const psca_eff_prior& e, double& dens,
+                            double& der) {
+    eff_density3(gm, p, e, pow(e.eps, 3.0), dens, der);
 }
 
 // ---------------------------------------------------------------------------
@@ -326,6 +338,12 @@ struct ColArgs {
     double* q_out;              // COL_QUAD: [B][N]
     double* r_out;
     const double* w_in;         // COL_REBUILD: [B][N]
+    // deferred rebuild (warp factor path): an instance with at most mov_cap moving
+    // columns leaves its list here and fac_sweep_w sums the increment itself
+    int* mov_cnt;               // [B] list length, or -1: sig_part holds the increment
+    int* mov_col;               // [B][mov_cap]
+    double* mov_w;              // [B][mov_cap]
+    int mov_cap;
 };
 
 __device__ __forceinline__ void load_tile(double2* buf, const double2* __restrict__ sb, int N,
@@ -637,6 +655,12 @@ struct FacArgs {
     double2* out_mat;           // FAC_INVERSE / FAC_ASSEMBLE output [B][L][L]
     double* out_vec;            // FAC_INVERSE: logdet, FAC_OBJECTIVE: value
     double2* pfrag;             // warp-sweep factor path: [B][NBLK][32] P lower fragments
+    const double2* pilots;      // deferred rebuild: [B][L][N] and the column kernel's lists
+    const int* mov_cnt;
+    const int* mov_col;
+    const double* mov_w;
+    int mov_cap;
+    int prior_ext;              // pgrad at the new iterate was written by prior_grad_kernel
 };
 
 // Gauss-Jordan sweep inversion of a Hermitian PD matrix held in X (row
@@ -1047,8 +1071,62 @@ __device__ double fac_prior_terms_at(const FacArgs& a, int b, const double* xv, 
 }
 
 __device__ double fac_prior_terms(const FacArgs& a, int b, double* sred) {
+    if (a.prior_ext) return 0.0;
     const size_t bN = (size_t)b * a.N;
     return fac_prior_terms_at(a, b, (a.k_new == 0 ? a.x_cur : a.x_next) + bN, sred);
+}
+
+// Prior gradient at the new iterate, one thread per (instance, device): the
+// per-device map-ur term (priors.py:383-399; pow / log per device) and the
+// pairwise map-k row sums (priors.py:145-159) are element-wise work, so the
+// compiled factor kernels leave them to this full-grid launch (no objective
+// recorded: the penalty value needs no reduction) instead of looping over N
+// inside one warp / CTA per instance.  Same expressions as fac_prior_terms_at.
+__global__ void __launch_bounds__(256) prior_grad_kernel(FacArgs a) {
+    const size_t i = (size_t)blockIdx.x * 256 + threadIdx.x;
+    const bool in = i < (size_t)a.B * a.N;
+    const int b = in ? (int)(i / a.N) : 0;
+    const int n = in ? (int)(i - (size_t)b * a.N) : 0;
+    const bool live = in && a.status[b] == PSCA_RUNNING;
+    const double* xv = (a.k_new == 0 ? a.x_cur : a.x_next) + (size_t)b * a.N;
+    if (a.kind == PSCA_MAP_K) {
+        if (!live) return;
+        double s = 0.0;
+        for (int j = a.c2_ptr[n]; j < a.c2_ptr[n + 1]; ++j)
+            s = __dadd_rn(s, __dmul_rn(a.c2_val[j], xv[a.c2_idx[j]]));
+        a.pgrad[i] = __ddiv_rn(-__dadd_rn(a.c1[n], s), (double)a.n_antennas);
+        return;
+    }
+    // map-ur: pow(eps, 3) once per CTA (same call, same value).  Compacting the
+    // exact-tail devices (three pow calls each) into a dense second pass was
+    // measured slower (0.183 vs 0.144 ms per 4 M devices): the divisions of the
+    // common branches dominate, not the tail.
+    __shared__ double s_eps3;
+    if (threadIdx.x == 0) s_eps3 = pow(a.eff.eps, 3.0);
+    __syncthreads();
+    if (!live) return;
+    const double x = xv[n];
+    double dens, der;
+    eff_density3(x, a.prior_p[n], a.eff, s_eps3, dens, der);
+    const double mag = a.eff.dead_zone_grad;
+    double gr;
+    if (dens <= 1e-300) {
+        gr = ((x <= a.eff.g_low / 2.0) ? 1.0 : -1.0) * (mag / a.n_antennas);
+    } else {
+        gr = -np_clip(der / dens, -mag, mag) / a.n_antennas;
+    }
+    a.pgrad[i] = gr;
+}
+
+// launches prior_grad_kernel when the factor launch that follows may skip its
+// own prior loop (returns the FacArgs to launch with)
+inline bool prior_grad_wanted(const FacArgs& fa) {
+    static const bool off = [] {
+        const char* e = getenv("PSCA_PRIOR_KERNEL");
+        return e && e[0] == '0';
+    }();
+    return !off && !fa.record_objective && fa.k_new < fa.T &&
+           (fa.kind == PSCA_MAP_UR || (fa.kind == PSCA_MAP_K && fa.c2_ptr));
 }
 
 template <int MODE>
@@ -1314,6 +1392,11 @@ cudaError_t launch_column_t(const ColArgs& ca, int n_chunks, cudaStream_t st) {
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
+    if (ca.dbg_delay_ns > 0) {
+        void* slots = nullptr;
+        if ((err = cudaGetSymbolAddress(&slots, g_sm_slot)) != cudaSuccess) return err;
+        if ((err = cudaMemsetAsync(slots, 0, sizeof(int) * 1024, st)) != cudaSuccess) return err;
+    }
     ProfScope prof(st, 0);
     kfn<<<dim3(n_chunks, ca.B), NT, sm, st>>>(ca);
     ++g_launches;
@@ -1338,12 +1421,22 @@ cudaError_t launch_column_w(const ColArgs& ca, int n_chunks, cudaStream_t st) {
     // the per-warp moving-column lists grow with the chunk width: very wide
     // single chunks (N beyond ~10K at L = 40, ~2.4K at L = 80) use the tile kernel
     const size_t sm = TWC<NRB>::smem(ca.chunk_cols);
-    if (tile_column_forced() || n_chunks > 1 || sm + 1024 > (size_t)227 * 1024)
+    if (tile_column_forced() || n_chunks > 1 || sm + 1024 > (size_t)227 * 1024) {
+        // the tile kernel always writes the increment: no deferred lists
+        if (ca.mov_cnt &&
+            cudaMemsetAsync(ca.mov_cnt, 0xff, sizeof(int) * (size_t)ca.B, st) != cudaSuccess)
+            return cudaGetLastError();
         return launch_column_t<NRB>(ca, n_chunks, st);
+    }
     auto kfn = column_kernel_w<NRB>;
     cudaError_t err =
         cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (err != cudaSuccess) return err;
+    if (ca.dbg_delay_ns > 0) {
+        void* slots = nullptr;
+        if ((err = cudaGetSymbolAddress(&slots, g_sm_slot)) != cudaSuccess) return err;
+        if ((err = cudaMemsetAsync(slots, 0, sizeof(int) * 1024, st)) != cudaSuccess) return err;
+    }
     ProfScope prof(st, 0);
     kfn<<<dim3(n_chunks, ca.B), NT, sm, st>>>(ca);
     ++g_launches;
@@ -1440,8 +1533,12 @@ cudaError_t launch_factor_w(const FacArgs& fa, cudaStream_t st) {
     using S = TWS<NRB>;
     cudaError_t err = cudaSuccess;
     {
+        auto sfn = fac_sweep_w<NRB>;
+        if ((err = cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)S::SMEM)) != cudaSuccess)
+            return err;
         ProfScope prof(st, 1);
-        fac_sweep_w<NRB><<<(fa.B + S::IPC - 1) / S::IPC, 32 * S::IPC, S::SMEM, st>>>(fa);
+        sfn<<<(fa.B + S::IPC - 1) / S::IPC, 32 * S::IPC, S::SMEM, st>>>(fa);
         ++g_launches;
         if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
@@ -1458,7 +1555,17 @@ cudaError_t launch_factor_w(const FacArgs& fa, cudaStream_t st) {
 }
 
 template <int NRB>
-cudaError_t launch_factor_t(const FacArgs& fa, const Geo& g, cudaStream_t st) {
+cudaError_t launch_factor_t(const FacArgs& fa0, const Geo& g, cudaStream_t st) {
+    FacArgs fa = fa0;
+    if (prior_grad_wanted(fa)) {
+        ProfScope prof(st, 2);
+        const size_t total = (size_t)fa.B * fa.N;
+        prior_grad_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(fa);
+        ++g_launches;
+        const cudaError_t perr = cudaGetLastError();
+        if (perr != cudaSuccess) return perr;
+        fa.prior_ext = 1;
+    }
     if constexpr (NRB <= 10) {
         if (fa.pfrag) return launch_factor_w<NRB>(fa, st);
     }
@@ -1650,6 +1757,11 @@ ColArgs sub_col(const ColArgs& c, int b0, int Bh, const Geo& g) {
     r.red_part = c.red_part + (size_t)b0 * c.n_chunks * 4;
     r.status = c.status + b0;
     if (c.pgrad) r.pgrad = c.pgrad + (size_t)b0 * N;
+    if (c.mov_cnt) {
+        r.mov_cnt = c.mov_cnt + b0;
+        r.mov_col = c.mov_col + (size_t)b0 * c.mov_cap;
+        r.mov_w = c.mov_w + (size_t)b0 * c.mov_cap;
+    }
     return r;
 }
 
@@ -1672,6 +1784,12 @@ FacArgs sub_fac(const FacArgs& f, int b0, int Bh, const Geo& g) {
     if (f.pgrad) r.pgrad = f.pgrad + (size_t)b0 * N;
     if (f.dmat) r.dmat = f.dmat + (size_t)b0 * dmat_stride(g, L);
     if (f.pfrag) r.pfrag = f.pfrag + (size_t)b0 * g.NBLK * 32;
+    if (f.mov_cnt) {
+        r.pilots = f.pilots + (size_t)b0 * L * N;
+        r.mov_cnt = f.mov_cnt + b0;
+        r.mov_col = f.mov_col + (size_t)b0 * f.mov_cap;
+        r.mov_w = f.mov_w + (size_t)b0 * f.mov_cap;
+    }
     return r;
 }
 
@@ -1686,6 +1804,9 @@ struct SolveLayout {
     double2* dmat;
     double2* scratch;
     double2* pfrag;
+    int* mov_cnt;
+    int* mov_col;
+    double* mov_w;
     size_t total;
 };
 
@@ -1695,6 +1816,15 @@ bool use_warp_factor(const psca_solve_args* a, const Geo& g, int n_chunks) {
     return !warp_factor_disabled() && !generic_forced() && n_chunks == 1 &&
            a->B >= sm_count() && (g.NRB == 2 || g.NRB == 3 || g.NRB == 4 || g.NRB == 5 ||
                                   g.NRB == 6 || g.NRB == 8 || g.NRB == 10);
+}
+
+// PSCA_DEFER_REBUILD=0: the column kernel always sums the increment itself
+bool deferred_rebuild_disabled() {
+    static const bool off = [] {
+        const char* e = getenv("PSCA_DEFER_REBUILD");
+        return e && e[0] == '0';
+    }();
+    return off;
 }
 
 SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, void* ws) {
@@ -1712,6 +1842,12 @@ SolveLayout solve_layout(const psca_solve_args* a, const Geo& g, int n_chunks, v
     s.scratch = cv.take<double2>(fac_scratch_bytes(g, a->B));
     s.pfrag = cv.take<double2>(use_warp_factor(a, g, n_chunks) ? (size_t)a->B * g.NBLK * 32 * 16 : 0);
     if (!use_warp_factor(a, g, n_chunks)) s.pfrag = nullptr;
+    s.mov_cnt = nullptr; s.mov_col = nullptr; s.mov_w = nullptr;
+    if (use_warp_factor(a, g, n_chunks) && !deferred_rebuild_disabled()) {
+        s.mov_w = cv.take<double>((size_t)a->B * MOV_CAP * 8);
+        s.mov_col = cv.take<int>((size_t)a->B * MOV_CAP * 4);
+        s.mov_cnt = cv.take<int>((size_t)a->B * 4);
+    }
     s.total = cv.off;
     return s;
 }
@@ -2011,6 +2147,9 @@ static int solve_enqueue(const psca_solve_args* a, void* workspace, size_t works
     fa.update_norm = a->update_norm; fa.objective = ca.record_objective ? a->objective : nullptr;
     fa.scratch = lay.scratch;
     fa.pfrag = lay.pfrag;
+    ca.mov_cnt = lay.mov_cnt; ca.mov_col = lay.mov_col; ca.mov_w = lay.mov_w; ca.mov_cap = MOV_CAP;
+    fa.mov_cnt = lay.mov_cnt; fa.mov_col = lay.mov_col; fa.mov_w = lay.mov_w; fa.mov_cap = MOV_CAP;
+    fa.pilots = ca.pilots;
 
     double* xc = a->x_out;
     double* xn = lay.x_alt;

@@ -28,15 +28,37 @@
 // overlap their dependent chains, and the products run as their own
 // throughput-bound launch.
 
+// instances (warps) per CTA and CTAs per SM of fac_sweep_w.  More resident warps
+// do not help (measured: 2 x 7 and 4 x 4 at 128 registers spill and lose 20 %,
+// 144 / 160 registers at 14 / 12 warps are equal to 4 x 3 at 168)
+#ifndef PSCA_FACW_IPC
+#define PSCA_FACW_IPC 4
+#endif
+// fully unrolled pivot loop (every tile dispatch and pivot predicate folds): 215 KB of
+// code at NRB = 10, measured slower (sweep 185 -> 219 us per 4096): off
+#ifndef PSCA_FACW_UNROLL
+#define PSCA_FACW_UNROLL 0
+#endif
+#ifndef PSCA_FACW_MINB
+#define PSCA_FACW_MINB 3
+#endif
+
 template <int NRB>
 struct TWS {
     static constexpr int LP = 4 * NRB;
     static constexpr int LPC = LP + ((NRB & 1) ? 0 : 4);   // staged-column stride (banks)
     static constexpr int NTL = rebuild_block_count(NRB);    // lower 4 x 8 tiles
     static constexpr int NCJ = (LP + 7) / 8;
-    static constexpr int IPC = 4;                           // instances (warps) per CTA
+    static constexpr int IPC = PSCA_FACW_IPC;               // instances (warps) per CTA
+    // deferred rebuild: gather ring of RST stages, two listed columns [2][LPC]
+    // each (it aliases the sweep scratch: the rebuild is over before the sweep)
+    static constexpr int RST = 8;
     // per warp: ub [2][LPC], cs [2 phases][2][LPC] (double2), kv [2][4], -M [8]
-    static constexpr size_t WARP_SMEM = (size_t)6 * LPC * 16 + 16 * 8;
+    static constexpr size_t SWEEP_SMEM = (size_t)6 * LPC * 16 + 16 * 8;
+    static constexpr size_t RING_SMEM = (size_t)RST * 2 * LPC * 16;
+    // then the list itself: MOV_CAP weights and columns
+    static constexpr size_t WARP_SMEM =
+        (SWEEP_SMEM > RING_SMEM ? SWEEP_SMEM : RING_SMEM) + (size_t)MOV_CAP * 12;
     static constexpr size_t SMEM = IPC * WARP_SMEM;
 };
 
@@ -245,7 +267,13 @@ __device__ __forceinline__ bool warp_sweep(double (&acc)[rebuild_block_count(NRB
     const int LE = (L + 1) & ~1;
     const unsigned long long sgn = (p == 0 && q == 1) ? 0ull : 0x8000000000000000ull;
     double* nm = kv + 8;   // -M as 2x2 complex: Ud[12 LPC + 8 + 2 (2 dl + h) + p]
+#if PSCA_FACW_UNROLL
+#pragma unroll
+    for (int k = 0; k < LP; k += 2) {
+        if (k >= LE) break;
+#else
     for (int k = 0; k < LE; k += 2) {
+#endif
         const int ph = (k >> 1) & 1;
         const double2* cc = cs + ph * 2 * LPC;
         const double* Cd = reinterpret_cast<const double*>(cc);
@@ -313,8 +341,106 @@ __device__ __forceinline__ bool warp_sweep(double (&acc)[rebuild_block_count(NRB
     return ok;
 }
 
+// Deferred covariance rebuild (covlinalg.py:55 over the moving columns only):
+// the column kernel left this instance's short list (column, weight); the warp
+// gathers the listed pilot columns through a cp.async ring (two columns = one
+// DMMA k-step per stage, RST stages in flight, rows >= L zero-filled) and sums
+// w s s^H into the accumulator fragments, one DMMA per tile per k-step:
+//   A[(l, p)][(c, q)] = +-S[l][c].(p ^ q)  (minus for p & q),
+//   B[(c, q)][m]      = w_c S[m][c].q
+// The list is copied to the warp's shared memory first (weights lw, columns lc,
+// behind the ring), so no registers are held across the prior terms.
 template <int NRB>
-__global__ void __launch_bounds__(128, 3) fac_sweep_w(FacArgs a) {
+__device__ __forceinline__ void mov_issue(const FacArgs& a, const double2* pil, int cnt,
+                                          const int* lc, double2* ring, int ks, int lane) {
+    using S = TWS<NRB>;
+    constexpr int LP = S::LP, LPC = S::LPC;
+    double2* st = ring + (size_t)(ks & (S::RST - 1)) * 2 * LPC;
+#pragma unroll
+    for (int u = 0; u < (2 * LP + 31) / 32; ++u) {
+        const int e = lane + 32 * u;
+        const int col = e >= LP ? 1 : 0;
+        const int row = e - col * LP;
+        const int c = 2 * ks + col;
+        if (e < 2 * LP) {
+            const bool ok = c < cnt && row < a.L;
+#ifdef PSCA_DBG_GATHER_HOT   // probe (results invalid): gather from columns 0, 1, ...
+            cp_async16(st + col * LPC + row, ok ? pil + (size_t)row * a.N + c : pil, ok ? 16 : 0);
+#else
+            cp_async16(st + col * LPC + row, ok ? pil + (size_t)row * a.N + lc[c] : pil,
+                       ok ? 16 : 0);
+#endif
+        }
+    }
+}
+
+template <int NRB>
+__device__ __forceinline__ void mov_begin(const FacArgs& a, int b, int cnt, unsigned char* wsm,
+                                          int lane) {
+    using S = TWS<NRB>;
+    double* lw = reinterpret_cast<double*>(wsm + S::RING_SMEM);
+    int* lc = reinterpret_cast<int*>(lw + MOV_CAP);
+    const size_t lo = (size_t)b * a.mov_cap;
+    for (int e = lane; e < MOV_CAP; e += 32) {
+        lc[e] = e < cnt ? a.mov_col[lo + e] : 0;
+        lw[e] = e < cnt ? a.mov_w[lo + e] : 0.0;
+    }
+    __syncwarp();
+    const double2* pil = a.pilots + (size_t)b * a.L * a.N;
+    double2* ring = reinterpret_cast<double2*>(wsm);
+    const int nks = (cnt + 1) >> 1;
+#pragma unroll 1
+    for (int ks = 0; ks < S::RST - 1; ++ks) {
+        if (ks < nks) mov_issue<NRB>(a, pil, cnt, lc, ring, ks, lane);
+        cp_async_commit();
+    }
+}
+
+template <int NRB>
+__device__ __forceinline__ void mov_rebuild(const FacArgs& a, int b, int cnt,
+                                            double (&acc)[rebuild_block_count(NRB)][2],
+                                            unsigned char* wsm, int lane) {
+    using S = TWS<NRB>;
+    constexpr int LPC = S::LPC, NTL = S::NTL, RST = S::RST;
+    const int r8 = lane >> 2, c4 = lane & 3;
+    const int p = r8 & 1, q = c4 & 1, kc = c4 >> 1;
+    const double2* pil = a.pilots + (size_t)b * a.L * a.N;
+    double2* ring = reinterpret_cast<double2*>(wsm);
+    const double* lw = reinterpret_cast<const double*>(wsm + S::RING_SMEM);
+    const int* lc = reinterpret_cast<const int*>(lw + MOV_CAP);
+    const int abase = 2 * (kc * LPC + (r8 >> 1)) + (p ^ q);
+    const int bbase = 2 * (kc * LPC + r8) + q;
+    const unsigned long long sgn = (p & q) ? 0x8000000000000000ull : 0ull;
+    const int nks = (cnt + 1) >> 1;
+#pragma unroll 1
+    for (int ks = 0; ks < nks; ++ks) {
+        if (ks + RST - 1 < nks) mov_issue<NRB>(a, pil, cnt, lc, ring, ks + RST - 1, lane);
+        cp_async_commit();
+        cp_async_wait<RST - 1>();
+        __syncwarp();
+        const double* Sd =
+            reinterpret_cast<const double*>(ring + (size_t)(ks & (RST - 1)) * 2 * LPC);
+        const double w = lw[2 * ks + kc];
+        // A operands one row tile ahead of their DMMAs (the accumulators fill
+        // the register file: no room for all NRB of them)
+        double bfr[S::NCJ];
+#pragma unroll
+        for (int j = 0; j < S::NCJ; ++j) bfr[j] = w * Sd[bbase + 16 * j];
+        double a_cur = xsign(Sd[abase], sgn);
+#pragma unroll
+        for (int i = 0; i < NRB; ++i) {
+            const double a_nxt = (i + 1 < NRB) ? xsign(Sd[abase + 8 * (i + 1)], sgn) : 0.0;
+#pragma unroll
+            for (int j = 0; j <= (4 * i + 3) / 8; ++j) dmma(acc[row_start<NRB>(i) + j], a_cur, bfr[j]);
+            a_cur = a_nxt;
+        }
+        __syncwarp();
+    }
+    cp_async_wait<0>();
+}
+
+template <int NRB>
+__global__ void __launch_bounds__(32 * PSCA_FACW_IPC, PSCA_FACW_MINB) fac_sweep_w(FacArgs a) {
     using S = TWS<NRB>;
     constexpr int LP = S::LP, LPC = S::LPC, NTL = S::NTL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -347,8 +473,13 @@ __global__ void __launch_bounds__(128, 3) fac_sweep_w(FacArgs a) {
         }
         if (flag != 0 || a.k_new >= a.T) return;
     }
+    // deferred rebuild: the list and the first gather stages go out before the
+    // prior terms, so the pilot columns arrive underneath them
+    const int mcnt = (a.mov_cnt && a.k_new > 0) ? a.mov_cnt[b] : -1;
+    unsigned char* wsm = smem_raw + warp * S::WARP_SMEM;
+    if (mcnt >= 0) mov_begin<NRB>(a, b, mcnt, wsm, lane);
     const double prior_value =
-        warp_prior_terms(a, b, (a.k_new == 0 ? a.x_cur : a.x_next) + bN, lane);
+        a.prior_ext ? 0.0 : warp_prior_terms(a, b, (a.k_new == 0 ? a.x_cur : a.x_next) + bN, lane);
 
     // ---- Sigma_k in accumulator fragments ---------------------------------------
     // tile t = (i, j): lane holds component p of entries (4 i + r8 / 2, 8 j + 2 c4 + h)
@@ -362,42 +493,75 @@ __global__ void __launch_bounds__(128, 3) fac_sweep_w(FacArgs a) {
         // one column chunk per instance on this path (use_warp_factor)
         const double2* sp = a.sig_part + (size_t)b * NTL * 32;
         const double s2 = a.noise[b];
-        constexpr int GA = 6;   // tiles per load batch (bounded register pressure)
-        int ti = 0, tj = 0;
+        // entry masks of tile t = (ti, tj): zero padding and upper part, noise on
+        // the real diagonal, identity padding pivot for odd L
+        auto finish = [&](int t, int ti, int tj, double2 sxy) {
+            const int l = 4 * ti + (r8 >> 1);
 #pragma unroll
-        for (int t0 = 0; t0 < NTL; t0 += GA) {
-            double2 sv[GA], dv[GA];
-#pragma unroll
-            for (int u = 0; u < GA; ++u) {
-                const int t = t0 + u;
-                sv[u] = make_double2(0.0, 0.0);
-                dv[u] = make_double2(0.0, 0.0);
-                if (t < NTL && !zero_weights) {
-                    sv[u] = sp[t * 32 + lane];
-                    if (D) dv[u] = D[t * 32 + lane];
-                }
+            for (int h = 0; h < 2; ++h) {
+                const int m = 8 * tj + 2 * c4 + h;
+                double v = h ? sxy.y : sxy.x;
+                if (l >= L || m >= L || m > l) v = 0.0;
+                if (m == l && l < L) v = p ? 0.0 : v + s2;
+                if ((L & 1) && l == L && m == L && p == 0) v = 1.0;
+                acc[t][h] = v;
             }
+        };
+        constexpr int GA = 6;   // tiles per load batch (bounded register pressure)
+        if (mcnt >= 0) {
+            // deferred rebuild: (1 - rho) D first (batched loads while the
+            // accumulators are still free), the listed columns on top by DMMA
 #pragma unroll
-            for (int u = 0; u < GA; ++u) {
-                const int t = t0 + u;
-                if (t < NTL) {
-                    double2 s = sv[u];
-                    if (D) {
-                        s = zero_weights ? make_double2(0.0, 0.0)
-                                         : make_double2(fma(omr, dv[u].x, s.x), fma(omr, dv[u].y, s.y));
-                        D[t * 32 + lane] = s;
-                    }
-                    const int l = 4 * ti + (r8 >> 1);
+            for (int t0 = 0; t0 < NTL; t0 += GA) {
+                double2 dv[GA];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int m = 8 * tj + 2 * c4 + h;
-                        double v = h ? s.y : s.x;
-                        if (l >= L || m >= L || m > l) v = 0.0;
-                        if (m == l && l < L) v = p ? 0.0 : v + s2;
-                        if ((L & 1) && l == L && m == L && p == 0) v = 1.0;   // identity padding pivot
-                        acc[t][h] = v;
+                for (int u = 0; u < GA; ++u)
+                    dv[u] = (t0 + u < NTL && D) ? D[(t0 + u) * 32 + lane] : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int u = 0; u < GA; ++u)
+                    if (t0 + u < NTL) {
+                        acc[t0 + u][0] = omr * dv[u].x;
+                        acc[t0 + u][1] = omr * dv[u].y;
                     }
-                    TILE_NEXT(ti, tj)
+            }
+            mov_rebuild<NRB>(a, b, mcnt, acc, wsm, lane);
+            int ti = 0, tj = 0;
+#pragma unroll
+            for (int t = 0; t < NTL; ++t) {
+                const double2 sxy = make_double2(acc[t][0], acc[t][1]);
+                if (D) D[t * 32 + lane] = sxy;
+                finish(t, ti, tj, sxy);
+                TILE_NEXT(ti, tj)
+            }
+        } else {
+            int ti = 0, tj = 0;
+#pragma unroll
+            for (int t0 = 0; t0 < NTL; t0 += GA) {
+                double2 sv[GA], dv[GA];
+#pragma unroll
+                for (int u = 0; u < GA; ++u) {
+                    const int t = t0 + u;
+                    sv[u] = make_double2(0.0, 0.0);
+                    dv[u] = make_double2(0.0, 0.0);
+                    if (t < NTL && !zero_weights) {
+                        sv[u] = sp[t * 32 + lane];
+                        if (D) dv[u] = D[t * 32 + lane];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < GA; ++u) {
+                    const int t = t0 + u;
+                    if (t < NTL) {
+                        double2 sxy = sv[u];
+                        if (D) {
+                            sxy = zero_weights ? make_double2(0.0, 0.0)
+                                               : make_double2(fma(omr, dv[u].x, sxy.x),
+                                                              fma(omr, dv[u].y, sxy.y));
+                            D[t * 32 + lane] = sxy;
+                        }
+                        finish(t, ti, tj, sxy);
+                        TILE_NEXT(ti, tj)
+                    }
                 }
             }
         }
@@ -424,8 +588,7 @@ __global__ void __launch_bounds__(128, 3) fac_sweep_w(FacArgs a) {
 
     // ---- Hermitian sweep operator, 2x2 block pivots, in the fragments ----------
     double logdet;
-    const bool ok = warp_sweep<NRB>(acc, smem_raw + warp * S::WARP_SMEM, L, a.record_objective,
-                                    logdet);
+    const bool ok = warp_sweep<NRB>(acc, wsm, L, a.record_objective, logdet);
     if (!ok) {
         if (lane == 0) {
             a.status[b] = PSCA_CHOL_FAIL;

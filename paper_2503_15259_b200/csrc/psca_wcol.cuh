@@ -167,6 +167,11 @@ __device__ __forceinline__ void wc_rebuild(const double2* WS, const double2* SP,
     }
 }
 
+// CTA-phase stagger (experiment, PSCA_DBG_DELAY_NS): the second CTA to arrive on
+// an SM in a launch starts that much later, so the co-resident pair's start /
+// rebuild phases fall into each other's column pass
+__device__ int g_sm_slot[1024];
+
 template <int NRB>
 __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a) {
     using G = TG<NRB>;
@@ -195,8 +200,27 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
 
     // the instance's P'/A' fragments: one TMA bulk copy, completion on s_bar
     __shared__ __align__(8) unsigned long long s_bar;
-    if (tid == 0) mbar_init(&s_bar, 1);
+    __shared__ int s_slot;
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        if (a.dbg_delay_ns > 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            s_slot = atomicAdd(&g_sm_slot[smid], 1);
+        }
+    }
     __syncthreads();
+    if (a.dbg_delay_ns > 0 && s_slot == 1) {
+        if (tid == 0) {
+            unsigned long long t0, t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            do {
+                __nanosleep(2000);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            } while (t1 - t0 < (unsigned long long)a.dbg_delay_ns);
+        }
+        __syncthreads();
+    }
     if (tid == 0)
         bulk_g2s(FR, a.frags + (size_t)b * G::NB * FRAG_SLOTS, (unsigned)W::FR_BYTES, &s_bar);
 
@@ -340,6 +364,23 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
         rp[3] = 0.0;
     }
     __syncthreads();
+
+    // ---- short lists: the factor warp of this instance sums the increment ----
+    // (fac_sweep_w gathers the listed columns itself, psca_facw.cuh); the list
+    // goes out in warp order, the order the CTA rebuild below would use
+    if (a.mov_cnt) {
+        const int total_mov = s_cnt[NWARP];
+        if (total_mov <= a.mov_cap) {
+            const size_t o = (size_t)b * a.mov_cap + s_cnt[warp];
+            for (int i = lane; i < cnt; i += 32) {
+                a.mov_col[o + i] = my_c[i];
+                a.mov_w[o + i] = my_v[i];
+            }
+            if (tid == 0) a.mov_cnt[b] = total_mov;
+            return;
+        }
+        if (tid == 0) a.mov_cnt[b] = -1;
+    }
 
     // ---- rebuild over the moving columns, 16 per round -----------------------
     int slot[G::MAXBW];

@@ -39,7 +39,8 @@ device.profile_end()
 device.set_serial(False)
 col = sum(ms for k, ms in recs if k == 0)
 fac = sum(ms for k, ms in recs if k != 0)
-fr = [ms for k, ms in recs if k != 0]
+fr = [ms for k, ms in recs if k == 1]
+pg = [ms for k, ms in recs if k == 2]   # prior_grad_kernel launches
 # warp factor path: per iteration a sweep launch then a product launch
 fac_even, fac_odd = sum(fr[0::2]), sum(fr[1::2])
 print(json.dumps({"env": sys.argv[4], "ms_per_solve_30it": e0.elapsed_time(e1) / 3,
