@@ -31,6 +31,13 @@
 #ifndef PSCA_WCOL_MINB
 #define PSCA_WCOL_MINB 2
 #endif
+#ifndef PSCA_WCOL_KDESC
+#define PSCA_WCOL_KDESC 0
+#endif
+// blocks per update group (4: 32 columns per update; 1: the update after every block)
+#ifndef PSCA_WCOL_UGRP
+#define PSCA_WCOL_UGRP 4
+#endif
 // rebuild gather buffers (2: the next round's loads overlap this round's DMMAs)
 #ifndef PSCA_WCOL_GBUF
 #define PSCA_WCOL_GBUF 2
@@ -87,8 +94,16 @@ __device__ __forceinline__ void wc_quad(double (&bf)[2 * NRB], const double2* __
     for (int i = NRB - 1; i >= 0; --i) {
         double tc[2] = {0.0, 0.0}, uc[2] = {0.0, 0.0};
         const double2* f = FRl + i * (i + 1) * FRAG_SLOTS;
+        // PSCA_WCOL_KDESC=1 walks the k-steps in descending order, so the fragments
+        // reloaded last are consumed last: measured equal (the other warps already
+        // cover that load), off
+#if PSCA_WCOL_KDESC
+#pragma unroll
+        for (int kk = 2 * (i + 1) - 1; kk >= 0; --kk) {
+#else
 #pragma unroll
         for (int kk = 0; kk < 2 * (i + 1); ++kk) {
+#endif
             const double2 pa = f[kk * FRAG_SLOTS];
             dmma(tc, pa.x, bf[kk]);
             dmma(uc, pa.y, bf[kk]);
@@ -97,11 +112,19 @@ __device__ __forceinline__ void wc_quad(double (&bf)[2 * NRB], const double2* __
         if (i == NRB - 1) mid();
         // S[4i + (r8 >> 1)][2 c4 + h], component r8 & 1, lives in B fragment
         // 2i + (r8 >> 2) of lane (2 c4 + h) * 4 + (r8 & 3)
+#ifdef PSCA_DBG_NO_EPI   // probe (results invalid): no shuffles for the epilogue operands
+        const double a0 = bf[2 * i], a1 = bf[2 * i + 1], b0 = a0, b1 = a1;
+#else
         const double a0 = __shfl_sync(0xffffffffu, bf[2 * i], src0);
         const double a1 = __shfl_sync(0xffffffffu, bf[2 * i + 1], src0);
         const double b0 = __shfl_sync(0xffffffffu, bf[2 * i], src0 + 4);
         const double b1 = __shfl_sync(0xffffffffu, bf[2 * i + 1], src0 + 4);
+#endif
+#ifdef PSCA_DBG_NO_BLOAD   // probe (results invalid): B fragments never reloaded
+        if (false) {
+#else
         if (nsrc) {
+#endif
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int m = 2 * (2 * i + u) + (c4 >> 1);
@@ -282,21 +305,26 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
             my_c[pos] = ncol;
         }
         cnt += __popc(mv);
-        const int c0 = ncol - lane;
         while (mv) {
             const int j = __ffs(mv) - 1;
             mv &= mv - 1;
+            const int cj = __shfl_sync(0xffffffffu, ncol, j);
             for (int m = lane; m < a.L; m += 32)
-                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(sb + (size_t)m * a.N + c0 + j));
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(sb + (size_t)m * a.N + cj));
         }
     };
 
-    // software pipeline: the update of block j runs inside the quad forms of
-    // block j + 8 (after its longest row's DMMAs are issued)
+    // software pipeline: the updates of four blocks (32 columns, one per lane:
+    // lanes 8 s .. 8 s + 7 hold the s-th block of the group) run together inside
+    // the quad forms of the following block, after its longest row's DMMAs are
+    // issued -- every FP64 instruction of the update then works on 32 columns
+    // instead of 8 (the FP64 pipe is the one the DMMAs use)
     bool pend = false;
     double pq = 0.0, pr = 0.0, px = 0.0, pgn = 1.0, ppg = 0.0;
     int pcol = 0;
     bool pvalid = false;
+    const int grp = lane >> 3;
+    int slot_in_group = 0;
     for (; jb < nblk; jb += NWARP) {
         const int jn = jb + NWARP;
         {   // L2 prefetch of the block after the next one (40 lines of 128 B)
@@ -307,9 +335,10 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)m * a.N * 16));
             }
         }
-        // the block's 8 columns: lane j < 8 -> column j
-        const int ncol = n_begin + 8 * jb + lane;
-        const bool cvalid = lane < 8 && ncol < n_end;
+        // the block's 8 columns go to the lanes of group slot_in_group
+        const bool mine = grp == slot_in_group;
+        const int ncol = n_begin + 8 * jb + (lane & 7);
+        const bool cvalid = mine && ncol < n_end;
         double x = 0.0, g = 1.0, pg = 0.0;
         if (cvalid) {
             x = x_cur[ncol];
@@ -321,20 +350,29 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
         double qa[2], ra[2];
         wc_quad<NRB>(bf, FRl, qa, ra, r8, c4, jn < nblk ? bsrc(jn) : nullptr, row2, a.L,
                      n_begin + 8 * jn + r8 < n_end, [&] {
-                         if (pend) update(pq, pr, px, pgn, ppg, pcol, pvalid);
+                         if (pend) {
+                             update(pq, pr, px, pgn, ppg, pcol, pvalid);
+                             pend = false;
+                             pvalid = false;
+                         }
                      });
-        // lane j (< 8) takes column j = 2 c4' + h from lane c4' = j >> 1
+        // lane l takes column j = l & 7 = 2 c4' + h from lane c4' = j >> 1
         const int srcl = (lane >> 1) & 3;
         const double q0 = __shfl_sync(0xffffffffu, qa[0], srcl);
         const double q1 = __shfl_sync(0xffffffffu, qa[1], srcl);
         const double r0 = __shfl_sync(0xffffffffu, ra[0], srcl);
         const double r1 = __shfl_sync(0xffffffffu, ra[1], srcl);
-        pq = (lane & 1) ? q1 : q0;
-        pr = (lane & 1) ? r1 : r0;
-        px = x; pgn = g; ppg = pg; pcol = ncol; pvalid = cvalid;
-        pend = true;
+        if (mine) {
+            pq = (lane & 1) ? q1 : q0;
+            pr = (lane & 1) ? r1 : r0;
+            px = x; pgn = g; ppg = pg; pcol = ncol; pvalid = cvalid;
+        }
+        if (++slot_in_group == PSCA_WCOL_UGRP) {
+            slot_in_group = 0;
+            pend = true;
+        }
     }
-    if (pend) update(pq, pr, px, pgn, ppg, pcol, pvalid);
+    if (pend || slot_in_group > 0) update(pq, pr, px, pgn, ppg, pcol, pvalid);
 
     // ---- per-warp partials of (sum dx^2, min q), list counts -----------------
 #pragma unroll
