@@ -248,6 +248,14 @@ typedef struct {
     int* status;            /* [1]                                             */
     int* n_iter;            /* [1]                                             */
     double* cond_est;       /* [1] or 0                                        */
+    /* map-k with a pairwise MVB prior (priors.py:56-159), as in
+     * psca_solve_args: c1 [N] and the CSR interaction matrix c2; all null for
+     * the independent prior (prior_lin).  The row sums c2 x need every
+     * device's x, so this form takes the whole instance (no column shards). */
+    const double* prior_c1;
+    const int* prior_c2_indptr;
+    const int* prior_c2_indices;
+    const double* prior_c2_data;
 } psca_large_args;
 
 size_t psca_large_workspace_bytes(const psca_large_args* a);

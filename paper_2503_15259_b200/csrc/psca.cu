@@ -1952,6 +1952,10 @@ LargeArgs large_kargs(const psca_large_args* a, const LargeLayout& l, int k) {
     g.pilots = reinterpret_cast<const double2*>(a->pilots); g.gains = a->gains;
     g.emp_cov = reinterpret_cast<const double2*>(a->emp_cov); g.steps = a->steps;
     g.prior_lin = a->prior_lin; g.prior_p = a->prior_p; g.eff = a->eff;
+    if (a->kind == PSCA_MAP_K && a->prior_c2_indptr) {
+        g.c1 = a->prior_c1; g.c2_ptr = a->prior_c2_indptr; g.c2_idx = a->prior_c2_indices;
+        g.c2_val = a->prior_c2_data;
+    }
     const bool even = ((k < 0 ? 0 : k) % 2) == 0;
     g.x_cur = even ? a->x_a : a->x_b;
     g.x_next = even ? a->x_b : a->x_a;
@@ -1974,7 +1978,14 @@ int check_large_args(const psca_large_args* a) {
         return PSCA_E_ARG;
     if (!aligned16(a->pilots) || !aligned16(a->emp_cov)) return PSCA_E_ARG;
     if ((a->kind == PSCA_ML_K || a->kind == PSCA_MAP_K) && !a->gains) return PSCA_E_ARG;
-    if (a->kind == PSCA_MAP_K && !a->prior_lin) return PSCA_E_ARG;
+    if (a->kind == PSCA_MAP_K) {
+        const bool pair = a->prior_c2_indptr || a->prior_c2_indices || a->prior_c2_data ||
+                          a->prior_c1;
+        if (pair && !(a->prior_c2_indptr && a->prior_c2_indices && a->prior_c2_data &&
+                      a->prior_c1))
+            return PSCA_E_ARG;
+        if (!pair && !a->prior_lin) return PSCA_E_ARG;
+    }
     if (a->kind == PSCA_MAP_UR && !a->prior_p) return PSCA_E_ARG;
     return PSCA_OK;
 }
@@ -1989,7 +2000,7 @@ int check_large_args(const psca_large_args* a) {
 int large_factor_chain(const LargeArgs& g, const LargeLayout& l, const double* x_new,
                        cudaStream_t st) {
     const int nblk32 = l.NBLK * 32;
-    if (g.kind == PSCA_MAP_UR || (g.kind == PSCA_MAP_K && g.record_objective))
+    if (g.kind == PSCA_MAP_UR || (g.kind == PSCA_MAP_K && (g.record_objective || g.c2_ptr)))
         PSCA_K((prior_large<<<1, NT, 0, st>>>(g, x_new)));
     PSCA_K((assemble_large<<<(nblk32 + NT - 1) / NT, NT, 0, st>>>(g)));
     PSCA_K((finish_sigma_large<<<(l.LP * l.LP + NT - 1) / NT, NT, 0, st>>>(g)));

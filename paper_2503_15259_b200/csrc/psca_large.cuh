@@ -47,6 +47,10 @@ struct LargeArgs {
     const double* steps;        // [T]
     const double* prior_lin;    // [N]
     const double* prior_p;      // [N]
+    const double* c1;           // pairwise map-k: [N], CSR c2 (null: independent prior)
+    const int* c2_ptr;
+    const int* c2_idx;
+    const double* c2_val;
     psca_eff_prior eff;
     const double* x_cur;
     double* x_next;
@@ -226,7 +230,8 @@ __global__ void __launch_bounds__(NT) update_large(LargeArgs a) {
         const double diff = __dsub_rn(q, r);
         double grad;
         if (a.kind == PSCA_ML_K) grad = __dmul_rn(g, diff);
-        else if (a.kind == PSCA_MAP_K) grad = __dadd_rn(__dmul_rn(g, diff), a.prior_lin[n]);
+        else if (a.kind == PSCA_MAP_K)
+            grad = __dadd_rn(__dmul_rn(g, diff), a.c2_ptr ? a.pgrad[n] : a.prior_lin[n]);
         else if (a.kind == PSCA_ML_UD) grad = diff;
         else grad = __dadd_rn(diff, a.pgrad[n]);
         const double gq = known ? __dmul_rn(g, q) : q;
@@ -874,11 +879,19 @@ __global__ void __launch_bounds__(NT) trace_large(LargeArgs a) {
 __global__ void __launch_bounds__(NT) prior_large(LargeArgs a, const double* xv) {
     __shared__ double sred[SRED];
     if (a.flag[0]) return;
-    double acc = 0.0;
+    double acc = 0.0, quad = 0.0;
     const int n = blockIdx.x * NT + threadIdx.x;   // grid-stride not needed: one pass
     for (int m = n; m < a.N; m += gridDim.x * NT) {
         const double x = xv[m];
-        if (a.kind == PSCA_MAP_UR) {
+        if (a.kind == PSCA_MAP_K && a.c2_ptr) {
+            // pairwise MVB prior (priors.py:145-159): -(c1 + c2 x)/M, CSR row order
+            double s = 0.0;
+            for (int j = a.c2_ptr[m]; j < a.c2_ptr[m + 1]; ++j)
+                s = __dadd_rn(s, __dmul_rn(a.c2_val[j], xv[a.c2_idx[j]]));
+            a.pgrad[m] = __ddiv_rn(-__dadd_rn(a.c1[m], s), (double)a.n_antennas);
+            acc = fma(a.c1[m], x, acc);
+            quad = fma(x, s, quad);
+        } else if (a.kind == PSCA_MAP_UR) {
             double dens, der;
             eff_density(x, a.prior_p[m], a.eff, dens, der);
             const double mag = a.eff.dead_zone_grad;
@@ -891,6 +904,10 @@ __global__ void __launch_bounds__(NT) prior_large(LargeArgs a, const double* xv)
     }
     if (gridDim.x == 1 && a.record_objective) {
         acc = block_sum(acc, sred);
+        if (a.kind == PSCA_MAP_K && a.c2_ptr) {
+            quad = block_sum(quad, sred);
+            acc = -(acc + 0.5 * quad) / a.n_antennas;
+        }
         // this shard's penalty: summed over the ranks with the next exchange
         if (threadIdx.x == 0)
             a.red[1] = (a.kind == PSCA_MAP_K) ? acc : (a.kind == PSCA_MAP_UR ? -acc / a.n_antennas : 0.0);

@@ -48,6 +48,8 @@ class LargeArgsC(ctypes.Structure):
         ("x_a", ctypes.c_void_p), ("x_b", ctypes.c_void_p), ("update_norm", ctypes.c_void_p),
         ("objective", ctypes.c_void_p), ("iterates", ctypes.c_void_p),
         ("status", ctypes.c_void_p), ("n_iter", ctypes.c_void_p), ("cond_est", ctypes.c_void_p),
+        ("prior_c1", ctypes.c_void_p), ("prior_c2_indptr", ctypes.c_void_p),
+        ("prior_c2_indices", ctypes.c_void_p), ("prior_c2_data", ctypes.c_void_p),
     ]
 
 
@@ -85,7 +87,7 @@ class GpuLargeStepper:
 
     def __init__(self, kind, pilots, gains, emp_cov, noise, n_antennas, steps, *, max_iter,
                  tol=0.0, prior_lin=None, prior_p=None, eff_prior=None,
-                 record_objective=False, record_iterates=False):
+                 record_objective=False, record_iterates=False, prior_c1=None, prior_c2=None):
         torch = device._torch()
         self.torch = torch
         self.lib = _lib()
@@ -99,6 +101,19 @@ class GpuLargeStepper:
         self.steps = device._dev(torch, steps, f64, dev).reshape(-1)
         self.pl = device._dev(torch, prior_lin, f64, dev) if prior_lin is not None else None
         self.pp = device._dev(torch, prior_p, f64, dev) if prior_p is not None else None
+        # pairwise MVB prior (priors.py:56-159): c1 and the CSR interaction matrix
+        self.c1 = self.c2p = self.c2i = self.c2d = None
+        if prior_c1 is not None or prior_c2 is not None:
+            if prior_c1 is None or prior_c2 is None:
+                raise ValueError("the pairwise prior needs both prior_c1 and prior_c2")
+            indptr, indices, data = prior_c2
+            self.c1 = device._dev(torch, np.broadcast_to(np.asarray(prior_c1, dtype=float), (N,)).copy(),
+                                  f64, dev)
+            self.c2p = device._dev(torch, np.asarray(indptr, dtype=np.int32), torch.int32, dev)
+            self.c2i = device._dev(torch, np.asarray(indices, dtype=np.int32), torch.int32, dev)
+            self.c2d = device._dev(torch, np.asarray(data, dtype=float), f64, dev)
+            if self.c2p.numel() != N + 1:
+                raise ValueError("prior_c2 indptr must have N + 1 entries")
         T = max(self.T, 1)
         self.x_a = torch.empty(N, dtype=f64, device=dev)
         self.x_b = torch.empty(N, dtype=f64, device=dev)
@@ -116,7 +131,9 @@ class GpuLargeStepper:
             steps=ptr(self.steps), prior_lin=ptr(self.pl), prior_p=ptr(self.pp),
             eff=device.eff_prior_struct(eff_prior), x_a=ptr(self.x_a), x_b=ptr(self.x_b),
             update_norm=ptr(self.un), objective=ptr(self.obj), iterates=ptr(self.its),
-            status=ptr(self.status), n_iter=ptr(self.n_iter), cond_est=ptr(self.cond))
+            status=ptr(self.status), n_iter=ptr(self.n_iter), cond_est=ptr(self.cond),
+            prior_c1=ptr(self.c1), prior_c2_indptr=ptr(self.c2p), prior_c2_indices=ptr(self.c2i),
+            prior_c2_data=ptr(self.c2d))
         nbytes = self.lib.psca_large_workspace_bytes(ctypes.byref(self.args))
         if nbytes == 0:
             raise PscaNativeError("psca_large rejected the arguments (shape/kind/pointers)")
@@ -213,12 +230,14 @@ def psca_run_large(kind, pilots, gains, emp_cov, noise, n_antennas, steps, *, ma
                    prior_lin=None, prior_p=None, eff_prior=None, record_objective=False,
                    record_iterates=False, group=None, prior_c1=None, prior_c2=None) -> dict:
     """Solve one instance with the large-L step loop (columns = this rank's shard)."""
-    if prior_c1 is not None or prior_c2 is not None:
-        raise NotImplementedError("pairwise MAP-K prior on the large-L path (L > 128)")
+    if prior_c1 is not None and group is not None and group.size() > 1:
+        # the row sums c2 x couple devices of different shards (an all-gather of x
+        # per iteration would be needed); the reference's group priors are small-N
+        raise NotImplementedError("pairwise MAP-K prior with column shards")
     st = GpuLargeStepper(kind, pilots, gains, emp_cov, noise, n_antennas, steps,
                          max_iter=max_iter, tol=tol, prior_lin=prior_lin, prior_p=prior_p,
                          eff_prior=eff_prior, record_objective=record_objective,
-                         record_iterates=record_iterates)
+                         record_iterates=record_iterates, prior_c1=prior_c1, prior_c2=prior_c2)
     res = ShardedDriver(st, group=group).run(max_iter)
     res["launches"] = st.launches
     return res
