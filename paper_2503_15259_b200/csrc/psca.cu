@@ -2178,13 +2178,24 @@ static int solve_enqueue(const psca_solve_args* a, void* workspace, size_t works
     // Large batches: two half-batches on two internal streams, so the
     // latency-bound factor kernel of one half runs under the column kernel of
     // the other (1 column CTA + 2 factor CTAs fit one SM).
-    const bool split = n_chunks == 1 && a->B >= 4 * sm_count() && !split_disabled();
+    static const int split_min = [] {   // batch size (in SM counts) from which to split
+        const char* e = getenv("PSCA_SPLIT_MIN");
+        const int v = e ? atoi(e) : 4;
+        return v >= 2 ? v : 4;
+    }();
+    const bool split = n_chunks == 1 && a->B >= split_min * sm_count() && !split_disabled();
     if (split) {
         g_last_path = 2;
         cudaStream_t ss[2];
         if (!ok_or_record(side_streams(st, ss))) return PSCA_E_CUDA;
-        const int Bh[2] = {a->B / 2, a->B - a->B / 2};
-        const int b0[2] = {0, a->B / 2};
+        // first half rounded up to whole waves of column CTAs (two per SM, one
+        // for L > 40), so an odd-sized batch does not pay a partial last wave in
+        // BOTH halves (B = 2024: 4 + 3 waves instead of 4 + 4)
+        const int wave = (g.NRB <= 10 ? 2 : 1) * sm_count();
+        int h0 = ((a->B / 2 + wave - 1) / wave) * wave;
+        if (h0 >= a->B) h0 = a->B / 2;
+        const int Bh[2] = {h0, a->B - h0};
+        const int b0[2] = {0, h0};
         ColArgs ch[2];
         FacArgs fh[2];
         for (int h = 0; h < 2; ++h) {

@@ -34,6 +34,12 @@
 #ifndef PSCA_WCOL_KDESC
 #define PSCA_WCOL_KDESC 0
 #endif
+// B fragments of the next block through a per-warp cp.async landing zone in
+// SMEM (aliased on the rebuild gather buffers, which are idle during the pass)
+// instead of LDG into registers: NRB <= 10 only (the zone needs 2 gather buffers)
+#ifndef PSCA_WCOL_STAGEB
+#define PSCA_WCOL_STAGEB 1
+#endif
 // blocks per update group (4: 32 columns per update; 1: the update after every block)
 #ifndef PSCA_WCOL_UGRP
 #define PSCA_WCOL_UGRP 4
@@ -49,11 +55,16 @@ struct TWC {
     static constexpr int NKK = 2 * NRB;   // k-steps = B fragments per lane per block
     static constexpr size_t FR_BYTES = (size_t)G::NB * FRAG_SLOTS * 16;
     static constexpr size_t W_BYTES = (size_t)G::LP8 * G::WCAP * 16;
+    static constexpr size_t W_BYTES_ = W_BYTES;
     static constexpr int GPT = (G::LP8 * G::WCAP + NT - 1) / NT;   // gather elements per thread
     // L > 40: the 24-slot fragments of the whole triangle fill most of SMEM
     // (L = 80: 161 KB), so one gather buffer and one CTA (up to 255 registers)
     // per SM
     static constexpr int NGB = NRB <= 10 ? PSCA_WCOL_GBUF : 1;
+    // per-warp landing zone [LP rows][8 columns] double2; fits the gather buffers
+    static constexpr bool STAGEB =
+        PSCA_WCOL_STAGEB && NRB <= 10 &&
+        (size_t)NWARP * G::LP * 8 * 16 <= (size_t)2 * (NRB <= 10 ? PSCA_WCOL_GBUF : 1) * W_BYTES_;
     static constexpr int MINB = NRB <= 10 ? PSCA_WCOL_MINB : 1;
     // dynamic SMEM: fragments, NGB x (WS, SP), per-warp partials, then the lists
     static constexpr size_t FIXED = FR_BYTES + 2 * NGB * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
@@ -82,11 +93,14 @@ __device__ __forceinline__ void wc_load_b(double (&bf)[2 * NRB], const double* _
 // Rows run in descending order, so after row i only k-steps < 2i are still
 // needed: its two B fragments are then reloaded with the next block's
 // (nsrc != nullptr), which keeps one fragment set per lane in registers.
+// With zsrc != nullptr the next block's fragments come from the warp's SMEM
+// landing zone (lane-resolved pointer: component c4 & 1 of row c4 >> 1, column
+// r8; row stride 16 doubles) after its cp.async group has landed.
 template <int NRB, class Mid>
 __device__ __forceinline__ void wc_quad(double (&bf)[2 * NRB], const double2* __restrict__ FRl,
                                         double (&qa)[2], double (&ra)[2], int r8, int c4,
                                         const double* __restrict__ nsrc, size_t row2, int L,
-                                        bool nok, Mid&& mid) {
+                                        bool nok, Mid&& mid, const double* zsrc = nullptr) {
     qa[0] = qa[1] = ra[0] = ra[1] = 0.0;
     const int src0 = 8 * c4 + (r8 & 3);
     const bool hi = (r8 >> 2) != 0;
@@ -123,7 +137,14 @@ __device__ __forceinline__ void wc_quad(double (&bf)[2 * NRB], const double2* __
 #ifdef PSCA_DBG_NO_BLOAD   // probe (results invalid): B fragments never reloaded
         if (false) {
 #else
-        if (nsrc) {
+        if (zsrc) {
+            if (i == NRB - 1) {   // the zone was filled during the previous block
+                cp_async_wait<0>();
+                __syncwarp();
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) bf[2 * i + u] = zsrc[(2 * (2 * i + u)) * 16];
+        } else if (nsrc) {
 #endif
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
@@ -271,7 +292,36 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
         return sbd + 2 * (size_t)n + (c4 & 1);
     };
     int jb = warp;
-    if (jb < nblk) wc_load_b<NRB>(bf, bsrc(jb), row2, a.L, n_begin + 8 * jb + r8 < n_end, c4);
+    // landing zone of this warp: [LP rows][8 columns] double2 (rows >= L and
+    // columns >= n_end zero-filled by the copy)
+    double* zone = reinterpret_cast<double*>(WS) + (size_t)warp * G::LP * 16;
+    const double* zlane = zone + ((c4 >> 1) * 8 + r8) * 2 + (c4 & 1);
+    auto zone_issue = [&](int jblk) {
+#pragma unroll
+        for (int u = 0; u < (G::LP * 8 + 31) / 32; ++u) {
+            const int e = lane + 32 * u;
+            const int row = e >> 3, c = e & 7;
+            const int n = n_begin + 8 * jblk + c;
+            if (e < G::LP * 8) {
+                const bool ok = row < a.L && n < n_end;
+                cp_async16(zone + e * 2, ok ? sb + (size_t)row * a.N + n : sb, ok ? 16 : 0);
+            }
+        }
+        cp_async_commit();
+    };
+    if (W::STAGEB) {
+        if (jb < nblk) {
+            zone_issue(jb);
+            cp_async_wait<0>();
+            __syncwarp();
+#pragma unroll
+            for (int kk = 0; kk < 2 * NRB; ++kk) bf[kk] = zlane[(2 * kk) * 16];
+            __syncwarp();
+            if (jb + NWARP < nblk) zone_issue(jb + NWARP);
+        }
+    } else if (jb < nblk) {
+        wc_load_b<NRB>(bf, bsrc(jb), row2, a.L, n_begin + 8 * jb + r8 < n_end, c4);
+    }
     mbar_wait(&s_bar, 0);   // fragments staged
     // per-device update (estimators.py:272-276) of one block's columns, lane
     // j < 8 -> column j; appends the moving columns to the warp's list and
@@ -348,14 +398,20 @@ __global__ void __launch_bounds__(NT, TWC<NRB>::MINB) column_kernel_w(ColArgs a)
             else if (a.kind == PSCA_MAP_K) pg = a.prior_lin[ncol];
         }
         double qa[2], ra[2];
-        wc_quad<NRB>(bf, FRl, qa, ra, r8, c4, jn < nblk ? bsrc(jn) : nullptr, row2, a.L,
+        wc_quad<NRB>(bf, FRl, qa, ra, r8, c4,
+                     (!W::STAGEB && jn < nblk) ? bsrc(jn) : nullptr, row2, a.L,
                      n_begin + 8 * jn + r8 < n_end, [&] {
                          if (pend) {
                              update(pq, pr, px, pgn, ppg, pcol, pvalid);
                              pend = false;
                              pvalid = false;
                          }
-                     });
+                     }, (W::STAGEB && jn < nblk) ? zlane : nullptr);
+        if (W::STAGEB && jn < nblk) {
+            // every lane has read the zone: refill it with the block after the next
+            __syncwarp();
+            if (jn + NWARP < nblk) zone_issue(jn + NWARP);
+        }
         // lane l takes column j = l & 7 = 2 c4' + h from lane c4' = j >> 1
         const int srcl = (lane >> 1) & 3;
         const double q0 = __shfl_sync(0xffffffffu, qa[0], srcl);

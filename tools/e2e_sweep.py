@@ -25,6 +25,12 @@ schedules = {
     "w/2,w,7w,B": [0, w // 2, w, 7 * w, B],
     "2w,7w,B": [0, 2 * w, 7 * w, B],
     "equal4": [(B * c) // 4 for c in range(5)],
+    "2w,B": [0, 2 * w, B],
+    "w,3w,B": [0, w, 3 * w, B],
+    "2w,6w,B": [0, 2 * w, 6 * w, B],
+    "w,2w,4w,8w,B": [0, w, 2 * w, 4 * w, 8 * w, B],
+    "2w,4w,8w,B": [0, 2 * w, 4 * w, 8 * w, B],
+    "w/2,3w/2,7w/2,B": [0, w // 2, 3 * w // 2, 7 * w // 2, B],
 }
 
 
