@@ -1125,9 +1125,11 @@ inline bool prior_grad_wanted(const FacArgs& fa) {
         const char* e = getenv("PSCA_PRIOR_KERNEL");
         return e && e[0] == '0';
     }();
-    return !off && !fa.record_objective && fa.k_new < fa.T &&
+    return !off && !fa.prior_ext && !fa.record_objective && fa.k_new < fa.T &&
            (fa.kind == PSCA_MAP_UR || (fa.kind == PSCA_MAP_K && fa.c2_ptr));
 }
+
+cudaError_t launch_prior_grad(const FacArgs& fa, cudaStream_t st);
 
 template <int MODE>
 __global__ void __launch_bounds__(NT) factor_kernel(FacArgs a) {
@@ -1554,15 +1556,25 @@ cudaError_t launch_factor_w(const FacArgs& fa, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+cudaError_t launch_prior_grad(const FacArgs& fa, cudaStream_t st) {
+    ProfScope prof(st, 2);
+    const size_t total = (size_t)fa.B * fa.N;
+    prior_grad_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(fa);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+// the compiled factor kernels honour FacArgs::prior_ext (the generic one does not)
+bool compiled_factor_shape(int nrb) {
+    return !generic_forced() && (nrb == 2 || nrb == 3 || nrb == 4 || nrb == 5 || nrb == 6 ||
+                                 nrb == 8 || nrb == 10 || nrb == 12 || nrb == 16 || nrb == 20);
+}
+
 template <int NRB>
 cudaError_t launch_factor_t(const FacArgs& fa0, const Geo& g, cudaStream_t st) {
     FacArgs fa = fa0;
     if (prior_grad_wanted(fa)) {
-        ProfScope prof(st, 2);
-        const size_t total = (size_t)fa.B * fa.N;
-        prior_grad_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(fa);
-        ++g_launches;
-        const cudaError_t perr = cudaGetLastError();
+        const cudaError_t perr = launch_prior_grad(fa, st);
         if (perr != cudaSuccess) return perr;
         fa.prior_ext = 1;
     }
@@ -1703,11 +1715,12 @@ struct SideKey {
 };
 struct SidePair {
     cudaStream_t s[2];
+    cudaStream_t p[2];   // prior-gradient launches of each half (beside its factor stage)
 };
 std::mutex g_side_mu;
 std::map<SideKey, SidePair> g_side;
 
-cudaError_t side_streams(cudaStream_t caller, cudaStream_t (&ss)[2]) {
+cudaError_t side_streams(cudaStream_t caller, cudaStream_t (&ss)[2], cudaStream_t (&ps)[2]) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -1715,12 +1728,16 @@ cudaError_t side_streams(cudaStream_t caller, cudaStream_t (&ss)[2]) {
     auto it = g_side.find({dev, caller});
     if (it == g_side.end()) {
         SidePair p;
-        for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < 2; ++h) {
             if ((e = cudaStreamCreateWithFlags(&p.s[h], cudaStreamNonBlocking)) != cudaSuccess) return e;
+            if ((e = cudaStreamCreateWithFlags(&p.p[h], cudaStreamNonBlocking)) != cudaSuccess) return e;
+        }
         it = g_side.emplace(SideKey{dev, caller}, p).first;
     }
-    ss[0] = it->second.s[0];
-    ss[1] = it->second.s[1];
+    for (int h = 0; h < 2; ++h) {
+        ss[h] = it->second.s[h];
+        ps[h] = it->second.p[h];
+    }
     return cudaSuccess;
 }
 
@@ -2186,8 +2203,8 @@ static int solve_enqueue(const psca_solve_args* a, void* workspace, size_t works
     const bool split = n_chunks == 1 && a->B >= split_min * sm_count() && !split_disabled();
     if (split) {
         g_last_path = 2;
-        cudaStream_t ss[2];
-        if (!ok_or_record(side_streams(st, ss))) return PSCA_E_CUDA;
+        cudaStream_t ss[2], ps[2];
+        if (!ok_or_record(side_streams(st, ss, ps))) return PSCA_E_CUDA;
         // first half rounded up to whole waves of column CTAs (two per SM, one
         // for L > 40), so an odd-sized batch does not pay a partial last wave in
         // BOTH halves (B = 2024: 4 + 3 waves instead of 4 + 4)
@@ -2220,7 +2237,19 @@ static int solve_enqueue(const psca_solve_args* a, void* workspace, size_t works
                 FacArgs f = fh[h];
                 f.k_new = k + 1; f.x_cur = xc + (size_t)b0[h] * a->N;
                 f.x_next = xn + (size_t)b0[h] * a->N;
+                // the prior gradient at the new iterate (map-ur, pairwise map-k) is
+                // only needed by the next column pass: it runs on its own stream
+                // beside the latency-bound factor stage of this half.  (It reads
+                // status while the sweep may stop the instance: a stopped instance
+                // never reads its pgrad again.)
+                const bool side_prior = compiled_factor_shape(g.NRB) && prior_grad_wanted(f);
+                if (side_prior) {
+                    if (!ok_or_record(stream_edge(ss[h], ps[h]))) return PSCA_E_CUDA;
+                    if (!ok_or_record(launch_prior_grad(f, ps[h]))) return PSCA_E_CUDA;
+                    f.prior_ext = 1;
+                }
                 if (!ok_or_record(launch_solve_factor(f, g, ss[h]))) return PSCA_E_CUDA;
+                if (side_prior && !ok_or_record(stream_edge(ps[h], ss[h]))) return PSCA_E_CUDA;
                 if (!ok_or_record(maybe_fault(a, k + 1, f.status, f.cond_est, Bh[h], ss[h])))
                     return PSCA_E_CUDA;
             }

@@ -843,14 +843,22 @@ __global__ void __launch_bounds__(NT) gemm_large(LargeArgs a) {
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     const int kmax = (MODE == 0) ? L : LP;
     const int nks = (kmax + 1) / 2;
-#pragma unroll 4
-    for (int ks = 0; ks < nks; ++ks) {
-        const int kc = 2 * ks + (c4 >> 1);
-        const double av = (l < (MODE == 0 ? L : LP) && kc < kmax)
-                              ? xsign(__ldg(Ad + 2 * ((size_t)l * lda + kc) + (p ^ q)), sg)
-                              : 0.0;
-        const double bv = (kc < kmax) ? Bd[2 * ((size_t)kc * LP + mb) + q] : 0.0;
-        dmma(acc[ks & 1], av, bv);
+    // operands of GK k-steps are loaded together before their DMMAs: with the
+    // loads issued one k-step at a time the warp waited out a full L2 latency
+    // per k-step (ncu: 85 % long-scoreboard stalls, 73 us per launch at L = 256)
+    constexpr int GK = 8;
+    for (int ks0 = 0; ks0 < nks; ks0 += GK) {
+        double av[GK], bv[GK];
+#pragma unroll
+        for (int u = 0; u < GK; ++u) {
+            const int kc = 2 * (ks0 + u) + (c4 >> 1);
+            const bool kin = ks0 + u < nks && kc < kmax;
+            av[u] = (kin && l < (MODE == 0 ? L : LP))
+                        ? __ldg(Ad + 2 * ((size_t)l * lda + kc) + (p ^ q)) : 0.0;
+            bv[u] = kin ? Bd[2 * ((size_t)kc * LP + mb) + q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < GK; ++u) dmma(acc[u & 1], xsign(av[u], sg), bv[u]);
     }
     double* out = reinterpret_cast<double*>(MODE == 0 ? a.Gg : a.Ag);
 #pragma unroll

@@ -13,6 +13,8 @@ import json
 import time
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from . import covlinalg, device, priors
@@ -498,28 +500,32 @@ def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=
     chunks = len(bounds) - 1
     user = torch.cuda.current_stream()
     copy = _COPY_STREAMS.setdefault(dev.index, torch.cuda.Stream(device=dev))
-    # consecutive chunks solve on alternating streams, so the next chunk's
-    # launches fill the SMs while the previous chunk drains its last wave
-    alt = _COPY_STREAMS.setdefault(("alt", dev.index), torch.cuda.Stream(device=dev))
+    # consecutive chunks solve on rotating streams (4: c1 e2e 242.8 ms with two,
+    # 239.7 with three, 238.1 with four), so the next chunks' launches fill the
+    # SMs while the previous chunks are in their latency-bound stages
+    ns = max(2, int(os.environ.get("PSCA_HOST_STREAMS", "4")))
+    alts = [_COPY_STREAMS.setdefault(("alt", i, dev.index), torch.cuda.Stream(device=dev))
+            for i in range(1, ns)]
     start = torch.cuda.Event()
     start.record(user)
-    alt.wait_event(start)
+    for alt in alts:
+        alt.wait_event(start)
     copy.wait_event(start)
-    comps = [user, alt]
+    comps = [user] + alts
     pin = S.is_pinned()
     x_h = torch.empty((B, N), dtype=torch.float64, pin_memory=pin)
     st_h = torch.empty(B, dtype=torch.int32, pin_memory=pin)
     ni_h = torch.empty(B, dtype=torch.int32, pin_memory=pin)
-    bufs = [None, None]
-    free = [torch.cuda.Event(), torch.cuda.Event()]
-    outs = [{}, {}]
+    bufs = [None] * ns
+    free = [torch.cuda.Event() for _ in range(ns)]
+    outs = [{} for _ in range(ns)]
     for c in range(chunks):
         lo, hi = bounds[c], bounds[c + 1]
-        k = c % 2
+        k = c % ns
         comp = comps[k]
         with torch.cuda.stream(copy):
-            if c >= 2:
-                copy.wait_event(free[k])           # chunk c-2 finished with this buffer
+            if c >= ns:
+                copy.wait_event(free[k])           # chunk c-ns finished with this buffer
             bufs[k] = [t[lo:hi].to(dev, non_blocking=True) if t is not None else None
                        for t in (S, E, nz, G)]
             copied = torch.cuda.Event()
@@ -540,9 +546,10 @@ def psca_run_batch_host(problem, pilots, emp_cov, noise, n_antennas: int, gains=
             st_h[lo:hi].copy_(res["status"], non_blocking=True)
             ni_h[lo:hi].copy_(res["n_iter"], non_blocking=True)
         free[k].record(comp)
-    done = torch.cuda.Event()
-    done.record(alt)
-    user.wait_event(done)
+    for alt in alts:
+        done = torch.cuda.Event()
+        done.record(alt)
+        user.wait_event(done)
     user.synchronize()
     return {"x": x_h, "status": st_h, "n_iter": ni_h}
 

@@ -31,7 +31,11 @@ schedules = {
     "w,2w,4w,8w,B": [0, w, 2 * w, 4 * w, 8 * w, B],
     "2w,4w,8w,B": [0, 2 * w, 4 * w, 8 * w, B],
     "w/2,3w/2,7w/2,B": [0, w // 2, 3 * w // 2, 7 * w // 2, B],
+    "w,2w,4w,7w,B": [0, w, 2 * w, 4 * w, 7 * w, B],
+    "w,2w,3w,5w,8w,B": [0, w, 2 * w, 3 * w, 5 * w, 8 * w, B],
 }
+if os.environ.get("E2E_ONLY"):
+    schedules = {k: v for k, v in schedules.items() if k in os.environ["E2E_ONLY"].split(";")}
 
 
 def timed(fn, reps=3):
