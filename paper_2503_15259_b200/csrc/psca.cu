@@ -1919,6 +1919,11 @@ struct LargeLayout {
     double* inst;
     int* flag;
     double* frob_part;
+    int* mcnt;
+    int* mcol_t;
+    double* mv_t;
+    int* mcol;
+    double* mv;
     int LP, NRB, NBLK, n_red, ks, ntiles;
     size_t total;
 };
@@ -1957,6 +1962,11 @@ LargeLayout large_layout(const psca_large_args* a, void* ws) {
     l.inst = cv.take<double>(4 * 8);
     l.frob_part = cv.take<double>(FROB_CTAS * 8);
     l.flag = cv.take<int>(sizeof(int));
+    l.mcnt = cv.take<int>((size_t)(l.n_red + 1) * 4);
+    l.mcol_t = cv.take<int>((size_t)l.n_red * NT * 4);
+    l.mv_t = cv.take<double>((size_t)l.n_red * NT * 8);
+    l.mcol = cv.take<int>((size_t)l.n_red * NT * 4);
+    l.mv = cv.take<double>((size_t)l.n_red * NT * 8);
     l.total = cv.off;
     return l;
 }
@@ -1983,6 +1993,7 @@ LargeArgs large_kargs(const psca_large_args* a, const LargeLayout& l, int k) {
     g.red_part = l.red_part; g.n_red = l.n_red; g.dsig_part = l.dsig_part; g.ks = l.ks;
     g.n_rtiles_lower = l.ntiles; g.dsig = l.dsig; g.red = l.red; g.dmat = l.dmat; g.Xg = l.Xg;
     g.Gg = l.Gg; g.Ag = l.Ag; g.inst = l.inst; g.flag = l.flag; g.frob_part = l.frob_part;
+    g.mcnt = l.mcnt; g.mcol_t = l.mcol_t; g.mv_t = l.mv_t; g.mcol = l.mcol; g.mv = l.mv;
     return g;
 }
 
@@ -2636,6 +2647,7 @@ int psca_large_columns(const psca_large_args* a, int k, void* workspace, size_t 
         PSCA_K((quad_large<<<grid, NT, sm, st>>>(g)));
     }
     PSCA_K((update_large<<<l.n_red, NT, 0, st>>>(g)));
+    PSCA_K((compact_large<<<1, 1024, 0, st>>>(g)));
     {
         const size_t sm = (size_t)(32 + 64) * RL_NC * 16;
         PSCA_K((rebuild_large<<<dim3(l.ntiles, l.ks), NT, sm, st>>>(g)));

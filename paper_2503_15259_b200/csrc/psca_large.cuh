@@ -79,6 +79,12 @@ struct LargeArgs {
     double* inst;               // [4] frob, logdet, trace, prior value
     int* flag;                  // [1] finalize decision
     double* frob_part;          // [FROB_CTAS] partial sums of |Sigma_ij|^2
+    // moving columns of the iteration, compacted in device order (stable):
+    int* mcnt;                  // [n_red + 1] per update block, then the total
+    int* mcol_t;                // [n_red][NT] block-local lists (update_large)
+    double* mv_t;
+    int* mcol;                  // [N] dense list (compact_large)
+    double* mv;
 };
 
 __device__ __forceinline__ int lblock_base(int i) {   // rebuild C-block index of (i, 0)
@@ -212,8 +218,10 @@ __global__ void __launch_bounds__(NT, 2) quad_large(LargeArgs a) {
 __global__ void __launch_bounds__(NT) update_large(LargeArgs a) {
     if (a.flag[0]) return;   // stopped: the step loop may run on without a host check
     __shared__ double sred[2 * NWARP];
+    __shared__ int wcnt[NWARP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = blockIdx.x * NT + tid;
+    double vmov = 0.0;
     const bool known = (a.kind == PSCA_ML_K || a.kind == PSCA_MAP_K);
     const double hi = known ? 1.0 : (a.kind == PSCA_ML_UD ? INFINITY : a.eff.g_high);
     const double rho = a.steps[a.k];
@@ -241,7 +249,8 @@ __global__ void __launch_bounds__(NT) update_large(LargeArgs a) {
         const double xn = __dadd_rn(__dmul_rn(omr, x), rc);
         a.x_next[n] = xn;
         if (a.iterates) a.iterates[(size_t)(a.k + 1) * a.N + n] = xn;
-        a.v[n] = known ? __dmul_rn(rc, g) : rc;
+        vmov = known ? __dmul_rn(rc, g) : rc;
+        a.v[n] = vmov;
         const double d = __dsub_rn(xn, x);
         dx2 = d * d;
         mq = q;
@@ -251,11 +260,27 @@ __global__ void __launch_bounds__(NT) update_large(LargeArgs a) {
         const double t = __shfl_xor_sync(0xffffffffu, mq, o);
         mq = (t < mq) ? t : mq;
     }
+    // moving columns (non-zero rebuild weight) of this block, in device order
+    const unsigned mvm = __ballot_sync(0xffffffffu, vmov != 0.0);
     if (lane == 0) {
         sred[2 * warp] = dx2;
         sred[2 * warp + 1] = mq;
+        wcnt[warp] = __popc(mvm);
     }
     __syncthreads();
+    {
+        int off = 0, tot = 0;
+        for (int w = 0; w < NWARP; ++w) {
+            if (w < warp) off += wcnt[w];
+            tot += wcnt[w];
+        }
+        if (vmov != 0.0) {
+            const size_t o = (size_t)blockIdx.x * NT + off + __popc(mvm & ((1u << lane) - 1u));
+            a.mcol_t[o] = n;
+            a.mv_t[o] = vmov;
+        }
+        if (tid == 0) a.mcnt[blockIdx.x] = tot;
+    }
     if (tid == 0) {
         double s = 0.0, m = INFINITY;
         for (int w = 0; w < NWARP; ++w) {
@@ -265,6 +290,46 @@ __global__ void __launch_bounds__(NT) update_large(LargeArgs a) {
         a.red_part[2 * blockIdx.x] = s;
         a.red_part[2 * blockIdx.x + 1] = m;
     }
+}
+
+// ---------------------------------------------------------------------------
+// One CTA: exclusive prefix of the per-block counts (fixed order), then the
+// block-local lists concatenated into the dense list the rebuild walks, so its
+// chunks of 32 columns are full (with 2.5 % of the devices moving, scanning v
+// in device order found one or two columns per chunk).
+__global__ void __launch_bounds__(1024) compact_large(LargeArgs a) {
+    if (a.flag[0]) return;
+    __shared__ int s_off[1025];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int carry = 0;
+    for (int b0 = 0; b0 < a.n_red; b0 += 1024) {
+        const int nb = min(1024, a.n_red - b0);
+        if (warp == 0) {
+            for (int c = 0; c < nb; c += 32) {
+                const int v = (c + lane < nb) ? a.mcnt[b0 + c + lane] : 0;
+                int inc = v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                if (c + lane < nb) s_off[c + lane] = carry + inc - v;
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (lane == 0) s_off[nb] = carry;
+        }
+        __syncthreads();
+        for (int b = warp; b < nb; b += 32) {
+            const int o = s_off[b], c = s_off[b + 1] - o;
+            const size_t src = (size_t)(b0 + b) * NT;
+            for (int i = lane; i < c; i += 32) {
+                a.mcol[o + i] = a.mcol_t[src + i];
+                a.mv[o + i] = a.mv_t[src + i];
+            }
+        }
+        carry = s_off[nb];
+        __syncthreads();
+    }
+    if (tid == 0) a.mcnt[a.n_red] = carry;
 }
 
 // ---------------------------------------------------------------------------
@@ -287,8 +352,11 @@ __global__ void __launch_bounds__(NT) rebuild_large(LargeArgs a) {
         }
     }
     const int i = 8 * rt + warp;
-    const int per = (a.N + gridDim.y - 1) / gridDim.y;
-    const int c_begin = blockIdx.y * per, c_end = min(a.N, c_begin + per);
+    // this split's share of the dense moving list, in whole chunks of RL_NC
+    const int total = a.mcnt[a.n_red];
+    const int nchunk = (total + RL_NC - 1) / RL_NC;
+    const int per = ((nchunk + gridDim.y - 1) / gridDim.y) * RL_NC;
+    const int c_begin = min(total, (int)blockIdx.y * per), c_end = min(total, c_begin + per);
     double acc[8][2];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) acc[jj][0] = acc[jj][1] = 0.0;
@@ -297,8 +365,9 @@ __global__ void __launch_bounds__(NT) rebuild_large(LargeArgs a) {
     const int la = 4 * warp + (r8 >> 1);   // local WS row of the A fragment
 
     for (int c0 = c_begin; c0 < c_end; c0 += RL_NC) {
-        const int col = c0 + lane;
-        const double v = (col < c_end) ? a.v[col] : 0.0;
+        const int li = c0 + lane;
+        const int col = (li < c_end) ? a.mcol[li] : 0;
+        const double v = (li < c_end) ? a.mv[li] : 0.0;
         const unsigned mask = __ballot_sync(0xffffffffu, v != 0.0);
         if (mask == 0u) continue;                          // CTA-uniform (same v)
         const int nnz = __popc(mask);
