@@ -889,7 +889,8 @@ __device__ void assemble_sigma(const FacArgs& a, const Geo& geo, int b, double2*
 // chunk partials in batches of 8 (measured faster than the block-batched
 // assemble_sigma for c0's 32 chunks: 45.0 vs 46.7 us per iteration).
 __device__ void assemble_sigma_seq(const FacArgs& a, const Geo& geo, int b, double2* X, int ld,
-                               bool zero_weights) {
+                               bool zero_weights, int part = 0, int n_parts = 1,
+                               double* ssq_out = nullptr) {
     const int L = a.L;
     double* Xd = reinterpret_cast<double*>(X);
     double2* D = a.incremental ? a.dmat + (size_t)b * dmat_stride(geo, L) : nullptr;
@@ -900,7 +901,10 @@ __device__ void assemble_sigma_seq(const FacArgs& a, const Geo& geo, int b, doub
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int r8 = lane >> 2, c4 = lane & 3;
     int i = 0, base = 0;   // row block of blk, index of its first block (monotone walk)
-    for (int blk = threadIdx.x >> 5; blk < geo.NBLK; blk += nw) {
+    double ssq = 0.0;
+    // (part, n_parts): this CTA's share of the blocks (factor_cluster_t; X may
+    // then be another CTA's shared memory)
+    for (int blk = (threadIdx.x >> 5) * n_parts + part; blk < geo.NBLK; blk += nw * n_parts) {
         while (base + (4 * i + 3) / 8 + 1 <= blk) {
             base += (4 * i + 3) / 8 + 1;
             ++i;
@@ -908,9 +912,22 @@ __device__ void assemble_sigma_seq(const FacArgs& a, const Geo& geo, int b, doub
         const int j = blk - base;
         const int e = blk * 32 + lane;
         double2 s = make_double2(0.0, 0.0);
+        // D_k is fetched with the first batch of partials, not after their sum
+        const double2 dprev = (D && !zero_weights) ? D[e] : make_double2(0.0, 0.0);
         if (!zero_weights) {
-            // loads in batches of 8 (memory-level parallelism), adds in chunk order
+            // loads in batches of 32 / 8 (memory-level parallelism: a batch is one
+            // L2 round trip), adds in chunk order
             int c = 0;
+            for (; c + 32 <= a.n_chunks; c += 32) {
+                double2 v[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) v[u] = sp[(size_t)(c + u) * cs + e];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    s.x += v[u].x;
+                    s.y += v[u].y;
+                }
+            }
             for (; c + 8 <= a.n_chunks; c += 8) {
                 double2 v[8];
 #pragma unroll
@@ -931,8 +948,7 @@ __device__ void assemble_sigma_seq(const FacArgs& a, const Geo& geo, int b, doub
             if (zero_weights) {
                 s = make_double2(0.0, 0.0);
             } else {
-                const double2 d = D[e];
-                s = make_double2(fma(omr, d.x, s.x), fma(omr, d.y, s.y));
+                s = make_double2(fma(omr, dprev.x, s.x), fma(omr, dprev.y, s.y));
             }
             D[e] = s;
         }
@@ -945,12 +961,17 @@ __device__ void assemble_sigma_seq(const FacArgs& a, const Geo& geo, int b, doub
                 if (m < l) {
                     Xd[2 * (l * ld + m) + p] = v;
                     Xd[2 * (m * ld + l) + p] = p ? -v : v;
+                    ssq = fma(2.0 * v, v, ssq);   // the entry and its mirror
                 } else if (m == l) {
-                    Xd[2 * (l * ld + l) + p] = p ? 0.0 : v + s2;
+                    const double d = p ? 0.0 : v + s2;
+                    Xd[2 * (l * ld + l) + p] = d;
+                    ssq = fma(d, d, ssq);
                 }
             }
         }
     }
+    // this thread's share of ||Sigma||_F^2 over the entries it stored
+    if (ssq_out) *ssq_out = ssq;
     __syncthreads();
 }
 
@@ -1493,6 +1514,33 @@ cudaError_t launch_solve_column(const ColArgs& ca, const Geo& g, int n_chunks, c
     return launch_column<COL_SOLVE>(ca, g, n_chunks, st);
 }
 
+// lone instances: the factor stage on a cluster of FCS CTAs (PSCA_FAC_CLUSTER=0
+// keeps the single wide CTA)
+bool factor_cluster_disabled() {
+#if PSCA_DSWEEP
+    return true;   // the experimental fragment sweep does not publish its outcome to the cluster
+#else
+    static const bool off = [] {
+        const char* e = getenv("PSCA_FAC_CLUSTER");
+        return e && e[0] == '0';
+    }();
+    return off;
+#endif
+}
+
+template <int NRB>
+cudaError_t launch_factor_cluster(const FacArgs& fa, cudaStream_t st) {
+    const size_t sm = fac_smem<NRB>();
+    auto kfn = factor_cluster_t<NRB>;
+    cudaError_t err =
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (err != cudaSuccess) return err;
+    ProfScope prof(st, 1);
+    kfn<<<fa.B * FCS, 512, sm, st>>>(fa);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
 template <int NRB, int NTH>
 cudaError_t launch_factor_nt(const FacArgs& fa, const Geo& g, cudaStream_t st) {
     const size_t sm = fac_smem<NRB>();
@@ -1581,6 +1629,8 @@ cudaError_t launch_factor_t(const FacArgs& fa0, const Geo& g, cudaStream_t st) {
     if constexpr (NRB <= 10) {
         if (fa.pfrag) return launch_factor_w<NRB>(fa, st);
     }
+    if (2 * fa.B * FCS <= sm_count() && !factor_cluster_disabled() && small_factor_threads() == 512)
+        return launch_factor_cluster<NRB>(fa, st);
     if (fa.B < sm_count()) {
         switch (small_factor_threads()) {
             case 512: return launch_factor_nt<NRB, 512>(fa, g, st);

@@ -762,7 +762,7 @@ __device__ __forceinline__ bool dmma_sweep(double2* X, int ld, int L, bool want_
 template <int NRB, int NTH>
 __device__ __forceinline__ void products_pass(const FacArgs& a, int b, double2* X, double2* G,
                                               const double2* Es, double* od, double* sred,
-                                              double& trace) {
+                                              double& trace, int jr = 0, int js = 1) {
     const int tid = threadIdx.x;
     const int L = a.L;
     constexpr int LP = 4 * NRB;
@@ -774,8 +774,10 @@ __device__ __forceinline__ void products_pass(const FacArgs& a, int b, double2* 
     auto Ev = [&](int i, int c) -> double2 {
         return Es ? Es[i * ld + c] : __ldg(Eg + (size_t)i * L + c);
     };
+    // (jr, js): this CTA forms the column tiles j = jr (mod js) of G and A only
+    // (factor_cluster_t splits the products over the CTAs of a cluster)
     trace = 0.0;
-    if (a.record_objective) {
+    if (a.record_objective && jr == 0) {
         double s = 0.0;
         for (int e = tid; e < L * L; e += NTH) {
             const int i = e / L, j = e - i * L;
@@ -818,9 +820,11 @@ __device__ __forceinline__ void products_pass(const FacArgs& a, int b, double2* 
                 const double* brow = Xd + 2 * (kc * ld) + q;
 #pragma unroll
                 for (int j = 0; j < NCJ; ++j) {
-                    const int m = 8 * j + r8;
-                    const double bv = (m < LP) ? brow[2 * m] : 0.0;
-                    dmma(acc[j], av, bv);
+                    if (js == 1 || j % js == jr) {
+                        const int m = 8 * j + r8;
+                        const double bv = (m < LP) ? brow[2 * m] : 0.0;
+                        dmma(acc[j], av, bv);
+                    }
                 }
             }
 #pragma unroll
@@ -828,7 +832,7 @@ __device__ __forceinline__ void products_pass(const FacArgs& a, int b, double2* 
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int m = 8 * j + 2 * c4 + h;
-                    if (m < LP) Gd[2 * (l * ld + m) + p] = acc[j][h];
+                    if (m < LP && (js == 1 || j % js == jr)) Gd[2 * (l * ld + m) + p] = acc[j][h];
                 }
         }
         __syncthreads();
@@ -852,7 +856,7 @@ __device__ __forceinline__ void products_pass(const FacArgs& a, int b, double2* 
                 const double* brow = Gc + 2 * (kc * ld) + q;
 #pragma unroll
                 for (int j = 0; j < NCJ; ++j) {
-                    if (j < ncj) {
+                    if (j < ncj && (js == 1 || j % js == jr)) {
                         const int m = 8 * j + r8;
                         const double bv = (m < LP) ? brow[2 * m] : 0.0;
                         dmma(acc[j], av, bv);
@@ -862,7 +866,7 @@ __device__ __forceinline__ void products_pass(const FacArgs& a, int b, double2* 
             const int i4 = l >> 2;
 #pragma unroll
             for (int j = 0; j < NCJ; ++j) {
-                if (j < ncj) {
+                if (j < ncj && (js == 1 || j % js == jr)) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int m = 8 * j + 2 * c4 + h;
@@ -906,13 +910,14 @@ template <int NRB, int NTH>
 __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, int b, double2* X,
                                             double2* G, double2* cbuf, double2* /*unused*/,
                                             const double2* Es, double* od, double* sred,
-                                            double& frob, double& logdet, double& trace) {
+                                            double& frob, double& logdet, double& trace,
+                                            int cs = 1, int* cflag = nullptr) {
     using F = TF<NRB, NTH>;
     const int tid = threadIdx.x;
     const int L = a.L;
     constexpr int LP = F::LP;
     const int ld = LP + 1;
-    {
+    if (cs == 1) {   // (the cluster kernel sums the squares while it assembles Sigma)
         double s = 0.0;
         for (int e = tid; e < L * L; e += NTH) {
             const int i = e / L, j = e - i * L;
@@ -1313,11 +1318,26 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
     }
 #endif
     PROBE(5);
+    // packed lower triangle of P for the cluster's other CTAs: the instance's
+    // chunk partials are dead once Sigma is assembled (LP (LP + 1) / 2 entries
+    // fit in the lower tiles of one chunk)
+    double2* pshare = const_cast<double2*>(a.sig_part) + (size_t)b * a.n_chunks * geo.NBLK * 32;
+    if (cs > 1) {
+        // cluster factor (factor_cluster_t): the sweep's outcome goes to every
+        // CTA's flag before the cluster barrier they wait at
+        namespace cg = cooperative_groups;
+        auto cl = cg::this_cluster();
+        if (tid < cs) *cl.map_shared_rank(cflag, tid) = ok ? 1 : 2;
+        if (!ok) {
+            cl.sync();
+            return false;
+        }
+    }
     if (!ok) {
         __syncthreads();
         return false;
     }
-    // ---- P = -(swept): full Hermitian into X ----------------------------------
+    // ---- P = -(swept): full Hermitian into X (of every CTA of the cluster) -----
 #pragma unroll
     for (int u = 0; u < F::SL; ++u) {
         if (bi[u] < 0) continue;
@@ -1329,14 +1349,20 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                 if (i >= j) {
                     const double2 pv = (i < L && j < L) ? make_double2(-v[u][di][dj].x, -v[u][di][dj].y)
                                                         : make_double2(0.0, 0.0);
-                    X[i * ld + j] = (i == j) ? make_double2(pv.x, 0.0) : pv;
-                    if (i != j) X[j * ld + i] = make_double2(pv.x, -pv.y);
+                    const double2 dv = (i == j) ? make_double2(pv.x, 0.0) : pv;
+                    const double2 mv = make_double2(pv.x, -pv.y);
+                    X[i * ld + j] = dv;
+                    if (i != j) X[j * ld + i] = mv;
+                    // the other CTAs of the cluster fetch P through L2 (DSMEM
+                    // moves ~20 B / cycle out of one SM: 8.8 us for 7 copies)
+                    if (cs > 1) pshare[i * (i + 1) / 2 + j] = dv;
                 }
             }
     }
 #endif  // PSCA_DSWEEP
     PROBE(6);
-    products_pass<NRB, NTH>(a, b, X, G, Es, od, sred, trace);
+    if (cs > 1) cooperative_groups::this_cluster().sync();
+    products_pass<NRB, NTH>(a, b, X, G, Es, od, sred, trace, 0, cs);
     return true;
 }
 
@@ -1462,6 +1488,119 @@ __global__ void __launch_bounds__(NTH, (NTH == 128 && NRB <= 10) ? 4 : 1) factor
         in[1] = logdet;
         in[2] = trace;
         in[3] = prior_value;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// factor_cluster_t: the factor stage of a lone instance (or a handful) spread
+// over a cluster of FCS CTAs -- the latency-bound small-batch case (BASELINE
+// c0: B = 1), where one CTA spent 4.4 us summing the 32 chunk partials
+// (0.9 MB through one SM) and 7.2 us in the two DMMA products:
+//   * every CTA sums the chunk partials of the fragment blocks
+//     blk = rank (mod FCS) and stores its Sigma entries into CTA 0's X through
+//     distributed shared memory;                          [cluster barrier]
+//   * CTA 0 alone runs the pivot sweep (a dependent chain), then stores
+//     P = Sigma^-1 into every CTA's X and the sweep's outcome into every
+//     CTA's flag;                                          [cluster barrier]
+//   * CTA r forms the column tiles j = r (mod FCS) of G = Sigma_hat P and
+//     A = P G (both are column-local given all of P and Sigma_hat) and packs
+//     their P'/A' fragments.
+// CTA 0 finalises the previous iteration before a first cluster barrier and
+// the others read its outcome (status[b]) after it, so all CTAs stop or go on
+// together.  No CTA touches another's shared memory after the last barrier,
+// and CTA 0 (the only remote-store target before it) outlives all of them.
+// ---------------------------------------------------------------------------
+constexpr int FCS = 8;
+template <int NRB>
+__global__ void __cluster_dims__(FCS, 1, 1) __launch_bounds__(512, 1) factor_cluster_t(FacArgs a) {
+    namespace cg = cooperative_groups;
+    constexpr int NTH = 512;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double sred[SRED];
+    __shared__ int s_flag;
+    __shared__ int s_cflag;
+    __shared__ double s_ssq[FCS];
+    auto cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const Geo geo = make_geo(a.L, a.nrb);
+    const int b = blockIdx.x / FCS;
+    const int tid = threadIdx.x;
+    const int LP = geo.LP;
+    const int ld = LP + 1;
+    // CTA 0 finalises the previous iteration (the only writer of status[b] in
+    // this launch) before the first barrier; the others read the outcome after it
+    bool stop = false;
+#if PSCA_PROBE
+    const long long probe_t0 = clock64();
+#endif
+    if (rank == 0) {
+        if (a.status[b] != PSCA_RUNNING) stop = true;
+        else if (a.k_new > 0) stop = fac_finalize(a, b, &s_flag);
+    }
+    if (tid == 0) s_cflag = 0;
+    cl.sync();   // every CTA of the cluster is running: remote stores may start
+    if (rank != 0) stop = a.status[b] != PSCA_RUNNING || (a.k_new > 0 && a.k_new >= a.T);
+    if (stop) return;
+#if PSCA_PROBE
+    if (blockIdx.x == PSCA_PROBE_BLOCK && tid == 0) g_probe[0] = probe_t0;
+#endif
+    PROBE(1);
+    double2* sm = reinterpret_cast<double2*>(smem_raw);
+    double2* rowb = sm;
+    double2* colb = sm + 2 * LP;
+    double2* X = sm + 4 * LP;
+    double2* G = X + (size_t)LP * ld;
+    const double2* Es = G;
+    if (rank < (LP + 7) / 8) stage_emp(a, b, G, ld);   // the CTAs that own a column tile
+    double prior_value = 0.0;
+    if (rank == 0) prior_value = fac_prior_terms(a, b, sred);
+    PROBE(2);
+    double ssq;
+    assemble_sigma_seq(a, geo, b, cl.map_shared_rank(X, 0), ld, a.k_new == 0, rank, FCS, &ssq);
+    ssq = block_sum(ssq, sred);
+    if (tid == 0) *cl.map_shared_rank(&s_ssq[rank], 0) = ssq;
+    cl.sync();
+    double frob = 0.0, logdet = 0.0, trace = 0.0;
+    if (rank == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int r = 0; r < FCS; ++r) t += s_ssq[r];   // rank order: deterministic
+        frob = sqrt(t);
+    }
+    PROBE(3);
+    PROBE(4);
+    double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
+    if (rank == 0) {
+        if (!factor_pass<NRB, NTH>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet, trace,
+                                    FCS, &s_cflag)) {
+            if (tid == 0) {
+                a.status[b] = PSCA_CHOL_FAIL;
+                if (a.cond_est) a.cond_est[b] = INFINITY;
+            }
+            return;
+        }
+        PROBE(9);
+        if (tid == 0) {
+            double* in = a.inst + (size_t)b * 4;
+            in[0] = frob;
+            in[1] = logdet;
+            in[2] = trace;
+            in[3] = prior_value;
+        }
+    } else {
+        cl.sync();
+        if (s_cflag != 1) return;
+        if (rank < (LP + 7) / 8) {   // CTAs that own a column tile
+            const double2* pshare = a.sig_part + (size_t)b * a.n_chunks * geo.NBLK * 32;
+            for (int e = tid; e < LP * (LP + 1) / 2; e += NTH) {
+                int i, j;
+                lower_block(e, i, j);   // (i, j), i >= j, of packed entry e
+                const double2 pv = __ldcg(pshare + e);
+                X[i * ld + j] = pv;
+                if (i != j) X[j * ld + i] = make_double2(pv.x, -pv.y);
+            }
+            products_pass<NRB, NTH>(a, b, X, G, Es, od, sred, trace, rank, FCS);
+        }
     }
 }
 

@@ -121,3 +121,50 @@ def test_warp_kernel_options_match_tile_kernel(cuda_device):
         if "objective" in res[0]:
             assert max_rel(res[1]["objective"], res[0]["objective"]) <= 1e-11, name
     assert int(res[0]["n_iter"].min()) < 15   # the tol case stopped early
+
+
+CLUSTER_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2503_15259_b200 import estimators, scenes
+out = {}
+for L, kind, B, tol in ((40, "ml-k", 1, 0.0), (33, "map-k", 3, 0.0), (20, "map-ur", 2, 0.0),
+                        (52, "ml-ud", 1, 0.0), (72, "map-ur", 2, 0.0), (40, "ml-ud", 4, 3e-2)):
+    cfg = scenes.SceneConfig(11, kind, 600, L, 64, 20, 30, B)
+    ss = [scenes.make_scene(cfg, i) for i in range(B)]
+    b = scenes.stack_batch(ss)
+    res = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"], b["noise"],
+                                    64, gains=b["gains"], max_iter=30, tol=tol,
+                                    record_objective=True)
+    out[f"{L}-{kind}-{B}"] = {"x": res["x"].cpu().numpy().tolist(),
+                              "obj": res["objective"].cpu().numpy().tolist(),
+                              "un": res["update_norm"].cpu().numpy().tolist(),
+                              "n_iter": res["n_iter"].cpu().numpy().tolist(),
+                              "status": res["status"].cpu().numpy().tolist()}
+print(json.dumps(out))
+"""
+
+
+def test_cluster_factor_equals_single_cta_factor_bitwise(cuda_device):
+    """Few instances: the factor stage on a cluster of eight CTAs (factor_cluster_t:
+    chunk partials summed by slices, the sweep on CTA 0, the products by column
+    tiles) against one wide CTA per instance (PSCA_FAC_CLUSTER=0).  Same summation
+    orders in every phase, so iterates, update norms, objectives, stop iterations
+    and statuses are bit-identical (only the Frobenius norm of the q-floor guard
+    is summed in another order)."""
+    env = dict(os.environ)
+
+    def run(extra):
+        p = subprocess.run([sys.executable, "-c", CLUSTER_SCRIPT, str(ROOT)],
+                           env=dict(env, **extra), capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        return json.loads(p.stdout.strip().splitlines()[-1])
+
+    clus = run({"PSCA_FAC_CLUSTER": "1"})
+    one = run({"PSCA_FAC_CLUSTER": "0"})
+    assert any(min(v["n_iter"]) < 30 for v in clus.values())   # the tol stop is exercised
+    for key in clus:
+        for field in ("x", "un", "obj", "n_iter", "status"):
+            np.testing.assert_array_equal(np.array(clus[key][field]), np.array(one[key][field]),
+                                          err_msg=f"{key} {field}")
