@@ -1003,7 +1003,28 @@ __device__ int fac_finalize_core(const FacArgs& a, int b, int k, double dx2, dou
 // factorisation needed).
 __device__ bool fac_finalize(const FacArgs& a, int b, int* s_flag) {
     const int tid = threadIdx.x;
-    if (tid == 0) {
+    if (a.n_chunks >= 16) {
+        // many chunks (a lone instance spread over CTAs): the chunk reductions are
+        // fetched by as many threads in one L2 round trip, then added in chunk
+        // order by thread 0 from shared memory (same sums as below)
+        __shared__ double2 s_red[64];
+        const double* rp = a.red_part + (size_t)b * a.n_chunks * 4;
+        double dx2 = 0.0, minq = INFINITY;
+        for (int c0 = 0; c0 < a.n_chunks; c0 += 64) {
+            const int nc = min(64, a.n_chunks - c0);
+            if (tid < nc) s_red[tid] = *reinterpret_cast<const double2*>(rp + 4 * (c0 + tid));
+            __syncthreads();
+            if (tid == 0) {
+                for (int c = 0; c < nc; ++c) {
+                    dx2 += s_red[c].x;
+                    minq = (s_red[c].y < minq) ? s_red[c].y : minq;
+                }
+            }
+            __syncthreads();
+        }
+        if (tid == 0)
+            *s_flag = fac_finalize_core(a, b, a.k_new - 1, dx2, minq, a.inst + (size_t)b * 4);
+    } else if (tid == 0) {
         double dx2 = 0.0, minq = INFINITY;
         const double* rp = a.red_part + (size_t)b * a.n_chunks * 4;
         int c = 0;

@@ -483,10 +483,17 @@ __device__ __forceinline__ void finish_sigma(double2* X, int ld, int L, double s
 // (uniformly) when a pivot is not positive.  Ends synchronised.
 // ---------------------------------------------------------------------------
 // Issue the cp.async copy of Sigma_hat (L x L, row stride ld) into Es.
-__device__ __forceinline__ void stage_emp(const FacArgs& a, int b, double2* Es, int ld) {
+// (t0, nt > 0: issued by the nt threads from t0 on only)
+__device__ __forceinline__ void stage_emp(const FacArgs& a, int b, double2* Es, int ld, int t0 = 0,
+                                          int nt = 0) {
     const double2* E = a.emp_cov + (size_t)b * a.L * a.L;
     const int L = a.L;
-    for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
+    if (nt <= 0) nt = blockDim.x;
+    if ((int)threadIdx.x < t0 || (int)threadIdx.x >= t0 + nt) {
+        cp_async_commit();
+        return;
+    }
+    for (int e = threadIdx.x - t0; e < L * L; e += nt) {
         const int i = e / L, j = e - i * L;
         cp_async16(Es + i * ld + j, E + e, 16);
     }
@@ -1551,7 +1558,8 @@ __global__ void __cluster_dims__(FCS, 1, 1) __launch_bounds__(512, 1) factor_clu
     double2* X = sm + 4 * LP;
     double2* G = X + (size_t)LP * ld;
     const double2* Es = G;
-    if (rank < (LP + 7) / 8) stage_emp(a, b, G, ld);   // the CTAs that own a column tile
+    // (CTA 0's copy is issued later, by the warps that own no block of the sweep)
+    if (rank > 0 && rank < (LP + 7) / 8) stage_emp(a, b, G, ld);   // the CTAs that own a column tile
     double prior_value = 0.0;
     if (rank == 0) prior_value = fac_prior_terms(a, b, sred);
     PROBE(2);
@@ -1571,6 +1579,7 @@ __global__ void __cluster_dims__(FCS, 1, 1) __launch_bounds__(512, 1) factor_clu
     PROBE(4);
     double* od = reinterpret_cast<double*>(a.frags + (size_t)b * geo.NB * FRAG_SLOTS);
     if (rank == 0) {
+        stage_emp(a, b, G, ld, NTH / 2, NTH / 2);   // lands during the sweep
         if (!factor_pass<NRB, NTH>(a, geo, b, X, G, rowb, colb, Es, od, sred, frob, logdet, trace,
                                     FCS, &s_cflag)) {
             if (tid == 0) {

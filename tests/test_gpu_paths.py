@@ -130,10 +130,14 @@ sys.path.insert(0, sys.argv[1])
 from paper_2503_15259_b200 import estimators, scenes
 out = {}
 for L, kind, B, tol in ((40, "ml-k", 1, 0.0), (33, "map-k", 3, 0.0), (20, "map-ur", 2, 0.0),
-                        (52, "ml-ud", 1, 0.0), (72, "map-ur", 2, 0.0), (40, "ml-ud", 4, 3e-2)):
+                        (52, "ml-ud", 1, 0.0), (72, "map-ur", 2, 0.0), (40, "ml-ud", 4, 1.0)):
     cfg = scenes.SceneConfig(11, kind, 600, L, 64, 20, 30, B)
     ss = [scenes.make_scene(cfg, i) for i in range(B)]
     b = scenes.stack_batch(ss)
+    if tol > 0:   # a tol some instances reach mid-run: the 10th update norm of the first
+        r0 = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"],
+                                       b["noise"], 64, gains=b["gains"], max_iter=30)
+        tol = float(r0["update_norm"].cpu().numpy()[0, 10])
     res = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"], b["noise"],
                                     64, gains=b["gains"], max_iter=30, tol=tol,
                                     record_objective=True)
