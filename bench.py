@@ -358,6 +358,34 @@ def dist_setup(args):
     return world, rank, local
 
 
+def instance_ids(rank: int, per_rank: int) -> list[int]:
+    """Instance sharding (c1-c3): rank r owns the scene seeds [r B, (r + 1) B) -- disjoint
+    blocks, no data-path collective."""
+    return list(range(rank * per_rank, (rank + 1) * per_rank))
+
+
+def rank_barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int, dev) -> float:
+    """The slowest rank's device time (the only collective of the instance-sharded arms)."""
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(world: int, per_rank: int, steps: int, ms: float) -> float:
+    """instances/s of the whole job: every rank's instances over the slowest rank's time."""
+    return world * per_rank * steps / (ms * 1e-3)
+
+
 REF_PER_CORE = 4
 
 
@@ -493,7 +521,7 @@ def ours_arm(args):
     wl = Workload(args.config, args.iters, args.batch)
     cfg, problem = wl.cfg, wl.problem
     B, iters = wl.batch, wl.iters
-    ids = list(range(rank * B, (rank + 1) * B))
+    ids = instance_ids(rank, B)
     devb, host, gen_timing = generate_device(wl.scene_name, ids, os.cpu_count() or 1)
     dev = torch.device("cuda", torch.cuda.current_device())
     pil_h = torch.from_numpy(host["pilots"]).pin_memory()
@@ -506,15 +534,7 @@ def ours_arm(args):
     m = int(host["n_antennas"])
 
     def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-
-    def max_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        rank_barrier(world)
 
     def solve(out):
         return estimators.psca_run_batch(problem, pil_d, emp_d, noi_d, m, gains=gain_d,
@@ -539,8 +559,8 @@ def ours_arm(args):
         e1.record()
         torch.cuda.synchronize()
     barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1))
-    value = world * B * args.steps / (ms * 1e-3)
+    ms = max_over_ranks(e0.elapsed_time(e1), world, dev)
+    value = whole_job_rate(world, B, args.steps, ms)
     x_check = out["x"]
     finite = bool(torch.isfinite(x_check).all().item())
 
@@ -621,8 +641,8 @@ def ours_arm(args):
         f1.record()
         torch.cuda.synchronize()
         barrier()
-        ems = max_over_ranks(f0.elapsed_time(f1))
-        e2e = {"value": world * B * args.steps / (ems * 1e-3), "unit": UNIT,
+        ems = max_over_ranks(f0.elapsed_time(f1), world, dev)
+        e2e = {"value": whole_job_rate(world, B, args.steps, ems), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": ems / args.steps,
                "api": "paper_2503_15259_b200.psca_run_batch_host (pinned host in, pinned host "
@@ -712,12 +732,8 @@ def c4_arm(args):
         e1.record()
         torch.cuda.synchronize()
         launches += nl
-        ms = e0.elapsed_time(e1)
-        if group is not None:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
-        times.append(ms)
+        times.append(max_over_ranks(e0.elapsed_time(e1), world,
+                                    torch.device("cuda", torch.cuda.current_device())))
     ms = sum(times) / len(times)
     if rank == 0:
         flops = 24.0 * cfg.n_devices * cfg.pilot_len ** 2 * T
