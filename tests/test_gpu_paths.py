@@ -172,3 +172,38 @@ def test_cluster_factor_equals_single_cta_factor_bitwise(cuda_device):
         for field in ("x", "un", "obj", "n_iter", "status"):
             np.testing.assert_array_equal(np.array(clus[key][field]), np.array(one[key][field]),
                                           err_msg=f"{key} {field}")
+
+
+FAIL_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2503_15259_b200 import estimators, scenes
+cfg = scenes.SceneConfig(13, "ml-ud", 400, 24, 32, 12, 12, 3)
+ss = [scenes.make_scene(cfg, i) for i in range(3)]
+b = scenes.stack_batch(ss)
+b["pilots"][1, 3, 7] = np.nan          # instance 1: Sigma is NaN from the second factorisation on
+res = estimators.psca_run_batch(scenes.problem_for(cfg), b["pilots"], b["emp_cov"], b["noise"],
+                                32, gains=b["gains"], max_iter=12)
+x = res["x"].cpu().numpy()
+print(json.dumps({"status": res["status"].cpu().numpy().tolist(),
+                  "n_iter": res["n_iter"].cpu().numpy().tolist(),
+                  "x0": x[0].tolist(), "x2": x[2].tolist()}))
+"""
+
+
+def test_cluster_factor_pivot_failure_stops_only_that_instance(cuda_device):
+    """A sweep that meets a non-positive pivot on CTA 0 must release the other seven
+    CTAs of its cluster (outcome flag + barrier) and freeze that instance only."""
+    def run(extra):
+        p = subprocess.run([sys.executable, "-c", FAIL_SCRIPT, str(ROOT)],
+                           env=dict(os.environ, **extra), capture_output=True, text=True,
+                           timeout=180)
+        assert p.returncode == 0, p.stderr[-2000:]
+        return json.loads(p.stdout.strip().splitlines()[-1])
+
+    clus = run({"PSCA_FAC_CLUSTER": "1"})
+    one = run({"PSCA_FAC_CLUSTER": "0"})
+    assert clus["status"][1] == 1 and clus["n_iter"][1] < 12      # PSCA_CHOL_FAIL, stopped early
+    assert clus["status"][0] == 0 and clus["status"][2] == 0 and clus["n_iter"][0] == 12
+    assert clus == one
