@@ -1069,6 +1069,10 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                     ua[dj] = ub0[j0 + dj];
                     ubv[dj] = ub1[j0 + dj];
                 }
+#if PSCA_PROBE
+                if (k == 10 && u == 0) PROBE(20);
+                if (k == 10 && u == 0 && ua[0].x + ubv[1].y != 1.2345e300) PROBE(21);
+#endif
 #pragma unroll
                 for (int di = 0; di < 2; ++di) {
                     const double2 pp = c0[i0 + di], qq = c1[i0 + di];   // C_i
@@ -1082,7 +1086,13 @@ __device__ __forceinline__ bool factor_pass(const FacArgs& a, const Geo& geo, in
                         v[u][di][dj] = make_double2(nx, ny);
                     }
                 }
+#if PSCA_PROBE
+                if (k == 10 && u == 0 && v[u][0][0].x + v[u][1][1].y != 1.2345e300) PROBE(22);
+#endif
             }
+#if PSCA_PROBE
+            if (k == 10 && u == 0) PROBE(23);
+#endif
             // stage K' = {k+2, k+3}: its columns for every row, K' zeroed
             if (bi[u] == kb + 1 && bj[u] == kb + 1) {
                 kv[ph ^ 1][0] = v[u][0][0].x;

@@ -34,5 +34,6 @@ for rep in range(3):
                [v[i + 1] - v[i] for i in range(10, 29)])
 names = ["finalize", "prior", "assembly", "frob", "sweep", "P+trace", "emp_wait", "G", "A+pack",
          "total"] + [f"step{i}" for i in range(19)]
+print(json.dumps({"raw_10_24": [v[i] - v[10] for i in range(10, 24)]}))
 print(json.dumps({"config": name, "B": B, "lib": sys.argv[1],
                   "cycles": {k: res[-1][i] for i, k in enumerate(names)}}))
