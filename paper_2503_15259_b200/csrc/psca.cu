@@ -1615,12 +1615,12 @@ cudaError_t launch_factor_w(const FacArgs& fa, cudaStream_t st) {
     }
     if (fa.k_new >= fa.T) return cudaSuccess;   // no further column pass: no products
     const size_t sm = (size_t)2 * (4 * NRB) * (4 * NRB + 1) * 16;
-    auto kfn = fac_prod_t<NRB, 128>;
+    auto kfn = fac_prod_t<NRB, prod_threads<NRB>()>;
     if ((err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) !=
         cudaSuccess)
         return err;
     ProfScope prof(st, 1);
-    kfn<<<fa.B, 128, sm, st>>>(fa);
+    kfn<<<fa.B, prod_threads<NRB>(), sm, st>>>(fa);
     ++g_launches;
     return cudaGetLastError();
 }

@@ -620,6 +620,11 @@ __global__ void __launch_bounds__(32 * PSCA_FACW_IPC, PSCA_FACW_MINB) fac_sweep_
     }
 }
 
+// product CTA width: a warp owns whole row tiles, so eight warps cut the
+// longest warp of L = 40 from three row tiles to two (c1: 0.227 -> 0.200 ms per
+// 4096 instances at 256 x 4 CTAs per SM; 320 x 3: 0.197; 256 x 3: 0.214)
+template <int NRB>
+__host__ __device__ constexpr int prod_threads() { return NRB >= 8 ? 256 : 128; }
 template <int NRB, int NTH>
 __global__ void __launch_bounds__(NTH, 4) fac_prod_t(FacArgs a) {
     constexpr int LP = 4 * NRB;
