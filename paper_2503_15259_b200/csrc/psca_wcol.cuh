@@ -49,6 +49,14 @@
 #define PSCA_WCOL_GBUF 2
 #endif
 
+// CTAs per SM for L <= 20: with ten B fragments per lane the kernel fits 85
+// registers, and a third resident CTA covers the relatively longer per-block
+// epilogue (c3 L = 20: column launch 0.728 -> 0.703 ms per 2048 instances,
+// 26.46 -> 25.72 ms per 30 iterations; four CTAs at 64 registers: 0.819)
+#ifndef PSCA_WCOL_MINB_SMALL
+#define PSCA_WCOL_MINB_SMALL 3
+#endif
+
 template <int NRB>
 struct TWC {
     using G = TG<NRB>;
@@ -65,7 +73,7 @@ struct TWC {
     static constexpr bool STAGEB =
         PSCA_WCOL_STAGEB && NRB <= 10 &&
         (size_t)NWARP * G::LP * 8 * 16 <= (size_t)2 * (NRB <= 10 ? PSCA_WCOL_GBUF : 1) * W_BYTES_;
-    static constexpr int MINB = NRB <= 10 ? PSCA_WCOL_MINB : 1;
+    static constexpr int MINB = NRB <= 5 ? PSCA_WCOL_MINB_SMALL : (NRB <= 10 ? PSCA_WCOL_MINB : 1);
     // dynamic SMEM: fragments, NGB x (WS, SP), per-warp partials, then the lists
     static constexpr size_t FIXED = FR_BYTES + 2 * NGB * W_BYTES + (size_t)NWARP * 2 * 8 + 16 * 8;
     static __host__ __device__ constexpr int list_cap(int chunk_cols) {
